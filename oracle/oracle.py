@@ -1,0 +1,384 @@
+"""CPU oracle for the FSR hot path -- TEST INFRASTRUCTURE ONLY.
+
+Restates the reference pipeline (fsrkit 0.1.0, /root/reference/pkg/src/fsrkit)
+in numpy plus the C loop in ``fsr_oracle.c``.  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline and
+``--impl reference``) may import this module, and only as the checker or the
+timed CPU baseline; the product package never imports it.
+
+Parity status: PINNED.  ``tests/test_oracle.py`` checks this module against
+golden vectors generated from the reference itself
+(``tests/golden/make_golden.py`` imports fsrkit read-only): the loop is
+bitwise equal to ``_kernels.reconstruct_iterations`` (objectives, selections,
+ties, residual, model) and whole images are bitwise equal to
+``reconstruction.reconstruct_image``, because the FFTs below are the same
+numpy.fft (pocketfft, numpy 2.3.5) calls on the same arrays.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+_lib_lock = threading.Lock()
+
+LANE_GROUP_WIDTH = 32          # reduce.py:22
+MAX_BLOCK_RECORDS = 32 * 32    # reduce.py:23
+EARLY_STOP_RELATIVE = 1e-12    # reconstruction.py:27
+SPAN_BLOCKS = 128              # reconstruction.py:213
+REDUCERS = ("tree", "linear")  # reconstruction.py:24
+
+
+def build() -> str:
+    """Compile liboracle.so with its Makefile (strict IEEE flags)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(_LIB_PATH):
+                build()
+            L = ctypes.CDLL(_LIB_PATH)
+            P = ctypes.c_void_p
+            i64 = ctypes.c_int64
+            L.oracle_reconstruct_iterations.restype = i64
+            L.oracle_reconstruct_iterations.argtypes = [
+                P, P, P, P, i64, ctypes.c_double, i64, i64, ctypes.c_int,
+                ctypes.c_double, P, P, P]
+            L.oracle_reconstruct_batch.restype = None
+            L.oracle_reconstruct_batch.argtypes = [
+                i64, i64, P, P, P, P, ctypes.c_double, i64, i64, ctypes.c_int, P,
+                ctypes.c_int, P, P, P, P]
+            L.oracle_tree_argmax.restype = ctypes.c_double
+            L.oracle_tree_argmax.argtypes = [P, i64, i64, P]
+            L.oracle_linear_argmax.restype = ctypes.c_double
+            L.oracle_linear_argmax.argtypes = [P, i64, P]
+            L.oracle_max_threads.restype = ctypes.c_int
+            _lib = L
+        return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ---------------------------------------------------------------- weights.py
+def decay_grid(support: int, rho: float) -> np.ndarray:
+    """weights.py:18-27: rho ** distance to the centre (support-1)/2."""
+    center = (support - 1) / 2.0
+    m = np.arange(support, dtype=np.float64)
+    d2 = (m - center) ** 2
+    dist = np.sqrt(d2[:, None] + d2[None, :])
+    return rho ** dist
+
+
+def frequency_weight(support: int) -> np.ndarray:
+    """weights.py:40-56: (1 - sqrt2 * sqrt(k~^2/S^2 + l~^2/S^2))^2, clamped >= 0."""
+    if support < 2:
+        raise ValueError("support must be at least 2")
+    idx = np.arange(support, dtype=np.float64)
+    folded = support / 2.0 - np.abs(idx - support / 2.0)
+    norm = folded * folded / float(support * support)
+    inner = 1.0 - math.sqrt(2.0) * np.sqrt(norm[:, None] + norm[None, :])
+    wf = inner * inner
+    np.maximum(wf, 0.0, out=wf)
+    return wf
+
+
+# --------------------------------------------------------------- sampling.py
+_GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+_MIX1 = np.uint64(0xBF58476D1CE4E5B9)
+_MIX2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(seed: int, count: int) -> np.ndarray:
+    """sampling.py:23-29."""
+    base = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+    z = base + np.arange(1, count + 1, dtype=np.uint64) * _GOLDEN
+    z = (z ^ (z >> np.uint64(30))) * _MIX1
+    z = (z ^ (z >> np.uint64(27))) * _MIX2
+    return z ^ (z >> np.uint64(31))
+
+
+def quarter_sample_mask(shape, seed: int) -> np.ndarray:
+    """sampling.py:53-80: one known pixel per 2x2 cell (edge cells shrink)."""
+    y, x = shape
+    rows, cols = (y + 1) // 2, (x + 1) // 2
+    z = splitmix64(seed, rows * cols).reshape(rows, cols)
+    cell_h = np.full((rows, 1), 2, dtype=np.uint64)
+    if y % 2:
+        cell_h[-1, 0] = 1
+    cell_w = np.full((1, cols), 2, dtype=np.uint64)
+    if x % 2:
+        cell_w[0, -1] = 1
+    sel = z % (cell_h * cell_w)
+    dr = (sel // cell_w).astype(np.int64)
+    dc = (sel % cell_w).astype(np.int64)
+    rr = (np.arange(rows, dtype=np.int64)[:, None] * 2 + dr).ravel()
+    cc = (np.arange(cols, dtype=np.int64)[None, :] * 2 + dc).ravel()
+    mask = np.zeros((y, x), dtype=bool)
+    mask[rr, cc] = True
+    return mask
+
+
+def quarter_sample(pixels: np.ndarray, seed: int):
+    """(sampled pixels with unknowns zeroed, mask)."""
+    mask = quarter_sample_mask(pixels.shape, seed)
+    return np.where(mask, pixels, 0.0), mask
+
+
+def mean_fill(pixels: np.ndarray, mask: np.ndarray) -> np.ndarray:
+    """sampling.py:83-90."""
+    count = int(np.count_nonzero(mask))
+    if count == 0:
+        raise ValueError("no known samples")
+    return np.where(mask, pixels, float(pixels.sum()) / count)
+
+
+def extract_support_block(pixels, mask, support_row, support_col, support):
+    """sampling.py:93-107: window, positions outside the image unknown."""
+    y, x = pixels.shape
+    signal = np.zeros((support, support))
+    m = np.zeros((support, support), dtype=bool)
+    r0, r1 = max(support_row, 0), min(support_row + support, y)
+    c0, c1 = max(support_col, 0), min(support_col + support, x)
+    if r1 > r0 and c1 > c0:
+        wr, wc = r0 - support_row, c0 - support_col
+        signal[wr:wr + r1 - r0, wc:wc + c1 - c0] = pixels[r0:r1, c0:c1]
+        m[wr:wr + r1 - r0, wc:wc + c1 - c0] = mask[r0:r1, c0:c1]
+    return signal, m
+
+
+# ------------------------------------------------------------------- metrics
+def psnr(reference: np.ndarray, test: np.ndarray) -> float:
+    """metrics.py:35-48: test clamped to [0, 255], peak 255."""
+    diff = np.clip(test, 0.0, 255.0) - reference
+    mse = float(np.mean(diff * diff))
+    return math.inf if mse == 0.0 else 10.0 * math.log10(255.0 * 255.0 / mse)
+
+
+# --------------------------------------------------- synthetic test images
+def make_natural_image(size: int = 512, seed: int = 7) -> np.ndarray:
+    """Restatement of the reference test fixture (pkg/tests/conftest.py:8-25)."""
+    rng = np.random.default_rng(seed)
+    noise = rng.standard_normal((size, size))
+    fy = np.fft.fftfreq(size)[:, None]
+    fx = np.fft.fftfreq(size)[None, :]
+    radial = np.hypot(fy, fx)
+    smooth = np.fft.ifft2(np.fft.fft2(noise) / (1.0 + (radial * size / 6.0) ** 2)).real
+    smooth = (smooth - smooth.min()) / np.ptp(smooth)
+    yy, xx = np.mgrid[0:size, 0:size] / size
+    img = 30.0 + 150.0 * smooth + 35.0 * yy
+    disc = (yy - 0.35) ** 2 + (xx - 0.6) ** 2 < 0.04
+    img = np.where(disc, 0.5 * img + 110.0, img)
+    band = (yy > 0.7) & (yy < 0.85)
+    img = img + band * 12.0 * np.sin(2 * np.pi * 14 * xx) * np.sin(2 * np.pi * 9 * yy)
+    return np.clip(img, 0.0, 255.0)
+
+
+def synthetic_frame(height: int, width: int, seed: int, kind: str = "natural") -> np.ndarray:
+    """Non-square natural image = crop of a square natural image."""
+    if kind == "uniform":
+        return np.random.default_rng(seed).uniform(0.0, 255.0, (height, width))
+    side = max(height, width)
+    return np.ascontiguousarray(make_natural_image(side, seed)[:height, :width])
+
+
+# ---------------------------------------------------------------- the loop
+def reconstruct_iterations(residual, model, spectrum, wf_flat, gamma, iterations,
+                           use_tree=True, stop_threshold=0.0):
+    """_kernels.py:62-126 in place; returns (done, objectives, selections, ties)."""
+    S = residual.shape[0]
+    n = max(iterations, 1)
+    objectives = np.zeros(n, np.float64)
+    selections = np.zeros(n, np.int64)
+    ties = np.zeros(n, np.uint8)
+    assert residual.dtype == np.complex128 and residual.flags.c_contiguous
+    assert model.dtype == np.complex128 and model.flags.c_contiguous
+    spectrum = np.ascontiguousarray(spectrum, dtype=np.complex128)
+    wf_flat = np.ascontiguousarray(wf_flat, dtype=np.float64).ravel()
+    done = lib().oracle_reconstruct_iterations(
+        _ptr(residual), _ptr(model), _ptr(spectrum), _ptr(wf_flat), S, float(gamma),
+        int(iterations), LANE_GROUP_WIDTH, 1 if use_tree else 0, float(stop_threshold),
+        _ptr(objectives), _ptr(selections), _ptr(ties))
+    return int(done), objectives[:done], selections[:done], ties[:done].astype(bool)
+
+
+def reconstruct_batch(residuals, models, spectra, wf_flat, gamma, iterations, use_tree=True,
+                      stop_thresholds=None, threads=0, trace=False):
+    """_kernels.py:129-149 in place; optional per-block traces [count, I]."""
+    count, S, _ = residuals.shape
+    wf_flat = np.ascontiguousarray(wf_flat, dtype=np.float64).ravel()
+    if stop_thresholds is None:
+        stop_thresholds = np.zeros(count)
+    stop_thresholds = np.ascontiguousarray(stop_thresholds, dtype=np.float64)
+    it = max(iterations, 1)
+    sel = np.zeros((count, it), np.int64) if trace else None
+    obj = np.zeros((count, it), np.float64) if trace else None
+    ties = np.zeros((count, it), np.uint8) if trace else None
+    done = np.zeros(count, np.int64) if trace else None
+    lib().oracle_reconstruct_batch(
+        count, S, _ptr(residuals), _ptr(models), _ptr(spectra), _ptr(wf_flat), float(gamma),
+        int(iterations), LANE_GROUP_WIDTH, 1 if use_tree else 0, _ptr(stop_thresholds),
+        int(threads), _ptr(sel), _ptr(obj), _ptr(ties), _ptr(done))
+    if trace:
+        return sel, obj, ties, done
+    return None
+
+
+def tree_argmax(obj):
+    o = np.ascontiguousarray(obj, dtype=np.float64)
+    idx = ctypes.c_int64(0)
+    v = lib().oracle_tree_argmax(_ptr(o), o.size, LANE_GROUP_WIDTH, ctypes.byref(idx))
+    return v, idx.value
+
+
+def linear_argmax(obj):
+    o = np.ascontiguousarray(obj, dtype=np.float64)
+    idx = ctypes.c_int64(0)
+    v = lib().oracle_linear_argmax(_ptr(o), o.size, ctypes.byref(idx))
+    return v, idx.value
+
+
+def tree_rank(support: int) -> np.ndarray:
+    """Closed form of the tree winner: among maxima the record
+    with the lexicographically smallest (bitrev5(t >> 5), bitrev5(t & 31))."""
+    t = np.arange(support * support)
+
+    def bitrev5(x):
+        r = np.zeros_like(x)
+        for b in range(5):
+            r |= ((x >> b) & 1) << (4 - b)
+        return r
+
+    return bitrev5(t >> 5) * 32 + bitrev5(t & 31)
+
+
+# ------------------------------------------------------- image pipeline
+def block_origins(height: int, width: int, block: int):
+    """core.py:136-162, vectorised: target origins in row-major order."""
+    if height < 1 or width < 1:
+        raise ValueError("image must have at least one pixel")
+    rr, cc = np.meshgrid(np.arange(0, height, block), np.arange(0, width, block), indexing="ij")
+    return rr.ravel(), cc.ravel()
+
+
+def reconstruct_image(pixels, mask, block=4, border=14, iterations=100, rho=0.7, gamma=0.5,
+                      reducer="tree", early_stop=False, threads=0, trace=False):
+    """reconstruction.py:216-290 restated: spans of 128 blocks, numpy FFTs,
+    the C loop, inverse FFT, merge and stitch.  With ``trace`` the per-block
+    selections/objectives/ties/done are returned as well (they are the
+    reference's reconstruct_block_full traces, reconstruction.py:159-203)."""
+    if reducer not in REDUCERS:
+        raise ValueError(f"unknown argmax strategy {reducer!r}, expected one of {REDUCERS}")
+    use_tree = reducer == "tree"
+    pixels = np.ascontiguousarray(pixels, dtype=np.float64)
+    mask = np.ascontiguousarray(mask, dtype=bool)
+    height, width = pixels.shape
+    rows, cols = block_origins(height, width, block)
+    s = block + 2 * border
+    wf_flat = np.ascontiguousarray(frequency_weight(s)).ravel()
+    decay = decay_grid(s, rho)
+    known = int(np.count_nonzero(mask))
+    fill_value = float(pixels.sum()) / known if known else 0.0
+    out = np.array(pixels)
+    n = rows.size
+    it = max(iterations, 1)
+    tr = {}
+    if trace:
+        tr = dict(sel=np.zeros((n, it), np.int64), obj=np.zeros((n, it)),
+                  ties=np.zeros((n, it), np.uint8), done=np.zeros(n, np.int64))
+
+    def run_span(lo, hi):
+        count = hi - lo
+        signals = np.zeros((count, s, s))
+        masks = np.zeros((count, s, s), dtype=bool)
+        for i in range(count):
+            signals[i], masks[i] = extract_support_block(
+                pixels, mask, int(rows[lo + i]) - border, int(cols[lo + i]) - border, s)
+        weights = decay * masks
+        spectra = np.fft.fft2(weights, axes=(-2, -1))
+        residuals = np.fft.fft2(signals * weights, axes=(-2, -1))
+        models = np.zeros_like(residuals)
+        if early_stop:
+            thresholds = EARLY_STOP_RELATIVE * np.sum(signals * signals * weights, axis=(1, 2))
+        else:
+            thresholds = np.zeros(count)
+        res = reconstruct_batch(residuals, models, spectra, wf_flat, gamma, iterations,
+                                use_tree, thresholds, threads=1, trace=trace)
+        if trace:
+            tr["sel"][lo:hi], tr["obj"][lo:hi], tr["ties"][lo:hi], tr["done"][lo:hi] = res
+        merged = np.where(masks, signals, np.fft.ifft2(models, axes=(-2, -1)).real)
+        for i in range(count):
+            r, c = int(rows[lo + i]), int(cols[lo + i])
+            h, w = min(block, height - r), min(block, width - c)
+            if spectra[i, 0, 0].real <= 0.0:
+                if known == 0:
+                    raise ValueError("no known samples")
+                tile = np.full((h, w), fill_value)
+            else:
+                tile = merged[i, border:border + h, border:border + w]
+            out[r:r + h, c:c + w] = tile
+
+    spans = [(lo, min(lo + SPAN_BLOCKS, n)) for lo in range(0, n, SPAN_BLOCKS)]
+    nthreads = threads if threads > 0 else (os.cpu_count() or 1)
+    if nthreads == 1 or len(spans) == 1:
+        for lo, hi in spans:
+            run_span(lo, hi)
+    else:
+        with ThreadPoolExecutor(max_workers=nthreads) as pool:
+            list(pool.map(lambda sp: run_span(*sp), spans))
+    if trace:
+        return out, tr
+    return out
+
+
+def block_spectra(pixels, mask, block, border, rho, which=None):
+    """R0 and W of the support windows of the given block indices (numpy FFT),
+    exactly as reconstruction.py:246-260 forms them."""
+    pixels = np.ascontiguousarray(pixels, dtype=np.float64)
+    height, width = pixels.shape
+    rows, cols = block_origins(height, width, block)
+    if which is None:
+        which = np.arange(rows.size)
+    s = block + 2 * border
+    decay = decay_grid(s, rho)
+    signals = np.zeros((len(which), s, s))
+    masks = np.zeros((len(which), s, s), dtype=bool)
+    for i, b in enumerate(which):
+        signals[i], masks[i] = extract_support_block(
+            pixels, mask, int(rows[b]) - border, int(cols[b]) - border, s)
+    weights = decay * masks
+    spectra = np.fft.fft2(weights, axes=(-2, -1))
+    residuals = np.fft.fft2(signals * weights, axes=(-2, -1))
+    return residuals, spectra, signals, masks
+
+
+# -------------------------------------------------------------- comparators
+def mirror_index(sel: np.ndarray, support: int) -> np.ndarray:
+    """Conjugate mirror of flat bins: (u, v) -> (-u mod N, -v mod N)."""
+    u, v = np.divmod(np.asarray(sel), support)
+    return ((-u) % support) * support + ((-v) % support)
+
+
+def compare_sequences(sel_a, sel_b, support, done_a=None, done_b=None):
+    """Per-block classification: 'equal', 'mirror' (whole sequence mirrored)
+    or 'diverged'.  Returns (counts dict, boolean diverged mask)."""
+    sel_a = np.asarray(sel_a)
+    sel_b = np.asarray(sel_b)
+    eq = np.all(sel_a == sel_b, axis=1)
+    mir = np.all(sel_a == mirror_index(sel_b, support), axis=1) & ~eq
+    div = ~(eq | mir)
+    return {"equal": int(eq.sum()), "mirror": int(mir.sum()), "diverged": int(div.sum())}, div
