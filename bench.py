@@ -1,0 +1,333 @@
+"""FSR benchmark: fps and Mpixel/s of quarter-sampled frames on 1..8 B200.
+
+Default workload (BASELINE.json configs[2], the north-star target): one
+3840x2160 quarter-sampled synthetic frame per step, SPEC-default parameters
+(B=4, N=32, I=100, rho=0.7, gamma=0.5), strip-partitioned over the ranks
+(block rows split into contiguous strips, halo L=(N-B)/2 rows read on both
+sides; no collective on the data path -> "scaling": "strong").
+``--workload 1080p`` gives configs[1].
+
+One JSON line on rank 0:
+  value   fps with inputs resident in HBM, device time (CUDA events on the
+          launching stream), max over ranks; L2 flushed between steps.
+  e2e     the same through the public C-ABI call with pinned HOST buffers
+          (H2D of the strip + halo, D2H of the strip's output inside the timed
+          region), wall time, max over ranks.
+  roofline  dominant kernel (warp32_kernel): algorithmic flops per launch
+          (blocks x N^2 (12 I + 30 log2 N)) / its mean device time.
+  cpu_baseline  the oracle port of the reference (numpy FFT + strict-IEEE C
+          loop, all host cores) on a bounded sample of the same frame.
+
+``--impl reference`` times only that CPU port (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FSR fps & Mpixel/s at 1080p/4K at 1/2/4/8 B200; PSNR delta vs CPU reference"
+WORKLOADS = {"4k": (2160, 3840), "1080p": (1080, 1920)}
+
+
+def flops_per_block(N: int, I: int) -> float:
+    return N * N * (12.0 * I + 30.0 * math.log2(N))
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="4k", choices=list(WORKLOADS))
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64", "fp32_unguarded"])
+    ap.add_argument("--argmax", default="shfl", choices=["shfl", "smem", "redux"])
+    ap.add_argument("--reducer", default="tree", choices=["tree", "linear"])
+    ap.add_argument("--iterations", type=int, default=100)
+    ap.add_argument("--support", type=int, default=32)
+    ap.add_argument("--block", type=int, default=4)
+    ap.add_argument("--image", default="natural", choices=["natural", "uniform"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def make_frame(H, W, kind):
+    from paper_2202_13926_b200 import frames, synth
+    img = synth.frame(H, W, 7, kind)
+    mask = frames.quarter_sample_mask(H, W, 42)
+    return np.where(mask, img, 0.0), mask, img
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clock / throttle sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [ln for ln in out.strip().splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_port_sample(sampled, mask, B, N, I, reducer, target_s, threads):
+    """Time the oracle port on the first k block rows (k sized to ~target_s)."""
+    from oracle import port
+    H, W = sampled.shape
+    L = (N - B) // 2
+    bcols = -(-W // B)
+
+    def run(k):
+        h = min(H, k * B)
+        t0 = time.perf_counter()
+        port.reconstruct_image(sampled[:h], mask[:h], B, L, I, 0.7, 0.5, reducer, threads=threads)
+        return time.perf_counter() - t0, -(-h // B) * bcols
+
+    port.lib()
+    t, nb = run(1)  # includes one-off warm-up
+    t, nb = run(2)
+    per_block = t / nb
+    k = max(2, int(target_s / (per_block * bcols)))
+    k = min(k, -(-H // B))
+    t, nb = run(k)
+    return t, nb, k
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    H, W = WORKLOADS[args.workload]
+    B, N, I = args.block, args.support, args.iterations
+    sampled, mask, _ = make_frame(H, W, args.image)
+    total = -(-H // B) * -(-W // B)
+    threads = os.cpu_count() or 1
+    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        t, nb, k = cpu_port_sample(sampled, mask, B, N, I, args.reducer, per_step_s, threads)
+        if i >= args.warmup:
+            times.append(t * total / nb)  # seconds per full frame
+    s_per_frame = float(np.mean(times))
+    fps = 1.0 / s_per_frame
+    line = {
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "fps",
+        "mpixel_per_s": fps * H * W / 1e6, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": s_per_frame * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{W}x{H} quarter-sampled frame (BASELINE configs[2])"
+                   if args.workload == "4k" else f"{W}x{H} (configs[1])",
+                   "B": B, "N": N, "iterations": I, "rho": 0.7, "gamma": 0.5,
+                   "reducer": args.reducer, "image": args.image},
+        "cpu_baseline": {"value": fps, "unit": "fps", "cores": threads, "kind": "port",
+                         "sample": f"first {k} block rows ({nb} of {total} blocks) per step, "
+                                   "extrapolated by block count (per-block cost is "
+                                   "data-independent at fixed I)"},
+        "e2e": {"value": fps, "unit": "fps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2202_13926_b200 import _lib
+
+    H, W = WORKLOADS[args.workload]
+    B, N, I = args.block, args.support, args.iterations
+    L = (N - B) // 2
+    sampled, mask, original = make_frame(H, W, args.image)
+    px32 = sampled.astype(np.float32)
+    m8 = mask.astype(np.uint8)
+    brows, bcols = -(-H // B), -(-W // B)
+    row0, row1 = brows * rank // world, brows * (rank + 1) // world
+    my_blocks = (row1 - row0) * bcols
+
+    eng = _lib.Engine([local])
+    params = _lib.make_params(B, L, I, 0.7, 0.5, args.reducer, False, args.precision, args.argmax)
+    dev = torch.device("cuda", local)
+    d_px = torch.from_numpy(px32).to(dev)
+    d_mask = torch.from_numpy(m8).to(dev)
+    d_out = torch.zeros((H, W), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.reconstruct_device(d_px.data_ptr(), W, d_mask.data_ptr(), W, H, W, row0, row1,
+                               d_out.data_ptr(), W, params, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else 3):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    main_ms, launches, reruns = [], 0, 0
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict the frame from L2 between steps
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            st = eng.last_stats()  # waits for this step (outside the events)
+            main_ms.append(st["main_ms"])
+            launches += st["kernel_launches"]
+            reruns += st["rerun_blocks"]
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    fps = 1000.0 / ms_max
+
+    # ---- end to end through the public C-ABI call with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(px32).pin_memory()
+        hm = torch.from_numpy(m8).pin_memory()
+        ho = torch.zeros((H, W), dtype=torch.float32).pin_memory()
+        hpn, hmn, hon = hp.numpy(), hm.numpy(), ho.numpy()
+        for _ in range(2):
+            eng.reconstruct_rows(hpn, hmn, params, row0, row1, hon)
+        e2e_t = []
+        for _ in range(args.steps):
+            barrier()
+            t0 = time.perf_counter()
+            eng.reconstruct_rows(hpn, hmn, params, row0, row1, hon)
+            e2e_t.append(time.perf_counter() - t0)
+        e = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        ya, yb = max(0, row0 * B - L), min(H, row1 * B + L)
+        oa, ob = min(H, row0 * B), min(H, row1 * B)
+        e2e = {"value": 1.0 / float(e.item()), "unit": "fps",
+               "h2d_bytes_per_step": int((yb - ya) * W * 5),
+               "d2h_bytes_per_step": int((ob - oa) * W * 4),
+               "ms_per_step": float(e.item()) * 1e3}
+        # quality of this run against the original frame (rank 0 holds its strip only)
+        out_full = ho.numpy()
+    # ---- roofline for the dominant kernel
+    pk, src = peaks()
+    mean_main = float(np.mean(main_ms))
+    flop = my_blocks * flops_per_block(N, I)
+    achieved = flop / (mean_main * 1e-3) / 1e12
+    peak_fp32 = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
+                + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
+    line = {
+        "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{W}x{H} quarter-sampled frame, strip-partitioned over "
+                               f"{world} GPU(s)", "B": B, "N": N, "iterations": I, "rho": 0.7,
+                   "gamma": 0.5, "reducer": args.reducer, "precision": args.precision,
+                   "argmax": args.argmax, "image": args.image, "parallelism": f"strips{world}",
+                   "l2": "flushed between steps (256 MiB write)"},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_fp32,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fp32, "traffic": None,
+                     "kernel": "warp32_kernel" if (N == 32 and B * B <= 32) else "image_generic_kernel",
+                     "main_ms": mean_main,
+                     "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz "
+                                    f"({src} MEASURED_PEAKS.json has no FP32 figure)",
+                     "hbm_io": {"achieved_gbs": io_bytes / (ms_max * 1e-3) / 1e9,
+                                "peak_gbs": pk.get("hbm_gbs"),
+                                "frac": io_bytes / (ms_max * 1e-3) / 1e9 / pk.get("hbm_gbs", 1)}},
+        "gpu_launches": launches,
+        "rerun_blocks_per_step": reruns / max(1, args.steps),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        t, nb, k = cpu_port_sample(sampled, mask, B, N, I, args.reducer, args.cpu_seconds, threads)
+        total = brows * bcols
+        cfps = nb / t / total
+        line["cpu_baseline"] = {"value": cfps, "unit": "fps", "cores": threads, "kind": "port",
+                                "sample": f"first {k} block rows ({nb} of {total} blocks), "
+                                          f"{t:.1f} s, extrapolated by block count"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/*
+ * fsr.h -- C ABI of the B200 Frequency Selective Reconstruction engine (libfsr.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams are passed as void*, a cudaStream_t).  Every entry point returns an
+ * fsr_status; fsr_last_error() gives the message, whose text for the
+ * FSR_EINVAL/FSR_ENOSAMPLES cases is the reference's ValueError text so that
+ * the Python shim can raise the same exception.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference):
+ *   fsr_reconstruct_f64/_f32      <- fsrkit.reconstruction.reconstruct_image
+ *                                    pkg/src/fsrkit/reconstruction.py:216-290
+ *   fsr_iterate_spectra           <- fsrkit._kernels.reconstruct_batch /
+ *                                    reconstruct_iterations
+ *                                    pkg/src/fsrkit/_kernels.py:62-149
+ *   fsr_params_init / validation  <- fsrkit.core.FsrParams
+ *                                    pkg/src/fsrkit/core.py:45-85
+ * The reference has no compiled FFI; INTEGRATION.md shows the ctypes binding
+ * (the package's own shim, paper_2202_13926_b200/_lib.py) a maintainer of
+ * the reference would add.
+ */
+#ifndef FSR_H_
+#define FSR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSR_ABI_VERSION 1
+
+typedef enum {
+    FSR_OK = 0,
+    FSR_EINVAL = 1,      /* invalid argument -> ValueError (reference messages) */
+    FSR_ENOSAMPLES = 2,  /* "no known samples" (reconstruction.py:273-274) -> ValueError */
+    FSR_ECUDA = 3,       /* CUDA runtime failure -> RuntimeError */
+    FSR_EUNSUPPORTED = 4 /* valid in the reference but not built here -> ValueError */
+} fsr_status;
+
+typedef enum { FSR_REDUCER_TREE = 0, FSR_REDUCER_LINEAR = 1 } fsr_reducer;
+
+typedef enum {
+    FSR_PREC_FP64 = 0,         /* validation mode: fp64 loop and transforms */
+    FSR_PREC_FP32 = 1,         /* production: fp32 loop, near-tie blocks re-run in fp64 */
+    FSR_PREC_FP32_UNGUARDED = 2 /* ablation: pure fp32, no re-run */
+} fsr_precision;
+
+typedef enum {
+    FSR_ARGMAX_SHFL = 0,  /* register argmax: __shfl_xor_sync butterflies (the paper's) */
+    FSR_ARGMAX_SMEM = 1,  /* shared-memory tree argmax (the paper's comparison point) */
+    FSR_ARGMAX_REDUX = 2  /* redux.sync.max on packed keys + ballot */
+} fsr_argmax_impl;
+
+/* Mirrors FsrParams (core.py:45-85) plus the engine knobs. */
+typedef struct {
+    int32_t block;       /* B, target block side (>= 1) */
+    int32_t border;      /* L, support = B + 2L (the "N" of BASELINE.json) */
+    int32_t iterations;  /* I (>= 0) */
+    int32_t reducer;     /* fsr_reducer: tie-break rule of the reference reducers */
+    int32_t early_stop;  /* reconstruction.py:27, 262-266 */
+    int32_t precision;   /* fsr_precision */
+    int32_t argmax_impl; /* fsr_argmax_impl */
+    int32_t reserved;
+    double rho;          /* (0, 1) */
+    double gamma;        /* (0, 1] */
+    double guard_tau;    /* fp32 near-tie guard: relative top-2 gap that forces an fp64 re-run */
+} fsr_params;
+
+typedef struct fsr_engine fsr_engine;
+
+/* Defaults of the BASELINE configs: B=4, L=14 (N=32), I=100, rho=0.7, gamma=0.5, tree. */
+void fsr_params_init(fsr_params *p);
+
+/* Validate like FsrParams.__post_init__ (core.py:63-80); the S^2<=1024 cap is
+ * lifted except for the tree reducer, whose two-phase lane groups cover at
+ * most 1024 records (reduce.py:112-117). */
+int fsr_params_validate(const fsr_params *p, char *msg, int msg_len);
+
+/* Create an engine over the listed CUDA devices (NULL/0 -> device 0).  Image
+ * calls split the block rows into contiguous strips, one per device. */
+int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **out);
+void fsr_engine_destroy(fsr_engine *eng);
+const char *fsr_last_error(const fsr_engine *eng);
+const char *fsr_status_string(int status);
+int32_t fsr_abi_version(void);
+
+/*
+ * Whole-path call with HOST buffers (reconstruct_image).  px: H*W pixels on the
+ * 0..255 scale, row-major; unknown pixels are ignored (the reference requires
+ * them to be zero).  mask: H*W bytes, nonzero = known.  out: H*W, never
+ * aliases px.  sel (nullable): [n_blocks, iterations] selected flat bins
+ * (u*N+v) per block in partition order, -1 after an early stop; done
+ * (nullable): [n_blocks] iterations run.  Synchronous.
+ */
+int fsr_reconstruct_f64(fsr_engine *eng, const fsr_params *p, const double *px,
+                        const uint8_t *mask, int64_t height, int64_t width, double *out,
+                        int32_t *sel, int32_t *done);
+int fsr_reconstruct_f32(fsr_engine *eng, const fsr_params *p, const float *px,
+                        const uint8_t *mask, int64_t height, int64_t width, float *out,
+                        int32_t *sel, int32_t *done);
+
+/*
+ * Strip variant of fsr_reconstruct_f32 for sharded callers (one process per
+ * GPU): only target-block rows [row0, row1) are reconstructed; only the image
+ * rows their windows touch are copied to the device and only the strip's
+ * output rows of `out` (a full H*W host buffer) are written.
+ */
+int fsr_reconstruct_rows_f32(fsr_engine *eng, const fsr_params *p, const float *px,
+                             const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
+                             int64_t row1, float *out);
+
+/*
+ * Device-resident call on the engine's first device, asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  d_px/d_mask/d_out are
+ * device pointers with row pitches in ELEMENTS.  row0/row1 restrict the work
+ * to target-block rows [row0, row1) of the full image (strip partitioning);
+ * pass 0 and ceil(H/B) for the whole frame.  The halo (L rows above/below)
+ * is read from d_px/d_mask, which must hold the full image rows the strip's
+ * windows touch.  precision must be FP32 or FP32_UNGUARDED (f32 I/O).
+ */
+int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
+                               int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
+                               int64_t height, int64_t width, int64_t row0, int64_t row1,
+                               float *d_out, int64_t out_pitch, void *stream);
+
+/*
+ * Array-level loop operator (_kernels.reconstruct_batch plus the traces of
+ * reconstruct_iterations).  Host arrays, complex128 interleaved (re, im):
+ * R [count, N, N] in/out residual spectra, G [count, N, N] in/out model
+ * spectra (accumulated into, as the reference does), W [count, N, N] weight
+ * spectra, wf [N, N], thr [count] early-stop thresholds (nullable = 0).
+ * Traces (nullable) are [count, iterations]: sel, obj, ties; done [count].
+ * Blocks with W[0,0].re <= 0 are skipped (done = 0).  fp64 strict IEEE, no
+ * FMA: bitwise equal to the reference.  p->block/border/rho are ignored.
+ */
+int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int32_t N,
+                        double *R, double *G, const double *W, const double *wf,
+                        const double *thr, int32_t *sel, double *obj, uint8_t *ties,
+                        int32_t *done);
+
+/* Statistics of the last image call on the first device. */
+typedef struct {
+    int64_t blocks;          /* target blocks processed */
+    int64_t rerun_blocks;    /* blocks re-run in fp64 by the near-tie guard */
+    int64_t empty_blocks;    /* blocks with no known sample in the window */
+    int32_t kernel_launches; /* kernels launched by the call (all devices) */
+    int32_t reserved;
+    double kernel_ms;        /* device time of the last call's kernels (first device) */
+    double main_ms;          /* device time of the dominant kernel (first device) */
+} fsr_stats;
+int fsr_last_stats(const fsr_engine *eng, fsr_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSR_H_ */

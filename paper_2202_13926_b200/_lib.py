@@ -1,0 +1,230 @@
+"""ctypes binding of libfsr.so (include/fsr.h).
+
+This is the one place the Python package touches native code.  There is no
+fallback: if the shared library is missing or no CUDA device is present,
+every call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfsr.so")
+
+FSR_OK, FSR_EINVAL, FSR_ENOSAMPLES, FSR_ECUDA, FSR_EUNSUPPORTED = 0, 1, 2, 3, 4
+REDUCER = {"tree": 0, "linear": 1}
+PRECISION = {"fp64": 0, "fp32": 1, "fp32_unguarded": 2}
+ARGMAX = {"shfl": 0, "smem": 1, "redux": 2}
+
+
+class FsrParamsC(ctypes.Structure):
+    _fields_ = [
+        ("block", ctypes.c_int32),
+        ("border", ctypes.c_int32),
+        ("iterations", ctypes.c_int32),
+        ("reducer", ctypes.c_int32),
+        ("early_stop", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
+        ("argmax_impl", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("rho", ctypes.c_double),
+        ("gamma", ctypes.c_double),
+        ("guard_tau", ctypes.c_double),
+    ]
+
+
+class FsrStatsC(ctypes.Structure):
+    _fields_ = [
+        ("blocks", ctypes.c_int64),
+        ("rerun_blocks", ctypes.c_int64),
+        ("empty_blocks", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("kernel_ms", ctypes.c_double),
+        ("main_ms", ctypes.c_double),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libfsr.so (built by ``__graft_entry__.build()``); raise if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (make -C paper_2202_13926_b200/csrc); there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        i32, i64 = ctypes.c_int32, ctypes.c_int64
+        pp = ctypes.POINTER(FsrParamsC)
+        L.fsr_params_init.argtypes = [pp]
+        L.fsr_params_init.restype = None
+        L.fsr_params_validate.argtypes = [pp, ctypes.c_char_p, ctypes.c_int]
+        L.fsr_params_validate.restype = ctypes.c_int
+        L.fsr_engine_create.argtypes = [P, i32, ctypes.POINTER(P)]
+        L.fsr_engine_create.restype = ctypes.c_int
+        L.fsr_engine_destroy.argtypes = [P]
+        L.fsr_engine_destroy.restype = None
+        L.fsr_last_error.argtypes = [P]
+        L.fsr_last_error.restype = ctypes.c_char_p
+        L.fsr_status_string.argtypes = [ctypes.c_int]
+        L.fsr_status_string.restype = ctypes.c_char_p
+        L.fsr_abi_version.restype = i32
+        L.fsr_reconstruct_f64.argtypes = [P, pp, P, P, i64, i64, P, P, P]
+        L.fsr_reconstruct_f64.restype = ctypes.c_int
+        L.fsr_reconstruct_f32.argtypes = [P, pp, P, P, i64, i64, P, P, P]
+        L.fsr_reconstruct_f32.restype = ctypes.c_int
+        L.fsr_reconstruct_rows_f32.argtypes = [P, pp, P, P, i64, i64, i64, i64, P]
+        L.fsr_reconstruct_rows_f32.restype = ctypes.c_int
+        L.fsr_reconstruct_device_f32.argtypes = [P, pp, P, i64, P, i64, i64, i64, i64, i64, P,
+                                                 i64, P]
+        L.fsr_reconstruct_device_f32.restype = ctypes.c_int
+        L.fsr_iterate_spectra.argtypes = [P, pp, i64, i32, P, P, P, P, P, P, P, P, P]
+        L.fsr_iterate_spectra.restype = ctypes.c_int
+        L.fsr_last_stats.argtypes = [P, ctypes.POINTER(FsrStatsC)]
+        L.fsr_last_stats.restype = ctypes.c_int
+        _lib = L
+        return L
+
+
+EXPORTED = ["fsr_params_init", "fsr_params_validate", "fsr_engine_create", "fsr_engine_destroy",
+            "fsr_last_error", "fsr_status_string", "fsr_abi_version", "fsr_reconstruct_f64",
+            "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_device_f32", "fsr_iterate_spectra",
+            "fsr_last_stats"]
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return ctypes.c_void_p(a)
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer="tree",
+                early_stop=False, precision="fp32", argmax="shfl", guard_tau=1e-4) -> FsrParamsC:
+    p = FsrParamsC()
+    load().fsr_params_init(ctypes.byref(p))
+    if reducer not in REDUCER:
+        raise ValueError(f"unknown argmax strategy {reducer!r}, expected one of ('tree', 'linear')")
+    if precision not in PRECISION:
+        raise ValueError(f"unknown precision {precision!r}, expected one of {tuple(PRECISION)}")
+    if argmax not in ARGMAX:
+        raise ValueError(f"unknown argmax implementation {argmax!r}, expected one of {tuple(ARGMAX)}")
+    p.block, p.border, p.iterations = int(block), int(border), int(iterations)
+    p.rho, p.gamma = float(rho), float(gamma)
+    p.reducer, p.early_stop = REDUCER[reducer], 1 if early_stop else 0
+    p.precision, p.argmax_impl, p.guard_tau = PRECISION[precision], ARGMAX[argmax], float(guard_tau)
+    return p
+
+
+class Engine:
+    """One libfsr engine over a set of CUDA devices (strip-partitioned)."""
+
+    def __init__(self, devices=None):
+        L = load()
+        self._L = L
+        h = ctypes.c_void_p()
+        if devices:
+            arr = (ctypes.c_int32 * len(devices))(*devices)
+            rc = L.fsr_engine_create(ctypes.cast(arr, ctypes.c_void_p), len(devices), ctypes.byref(h))
+        else:
+            rc = L.fsr_engine_create(None, 0, ctypes.byref(h))
+        if rc != FSR_OK:
+            raise RuntimeError(L.fsr_last_error(None).decode())
+        self._h = h
+        self.devices = tuple(devices) if devices else (0,)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.fsr_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc == FSR_OK:
+            return
+        msg = self._L.fsr_last_error(self._h).decode()
+        if rc in (FSR_EINVAL, FSR_ENOSAMPLES, FSR_EUNSUPPORTED):
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    def reconstruct(self, px, mask, params: FsrParamsC, sel=None, done=None):
+        """Host-buffer whole-image call; returns a new array (never aliases px)."""
+        px = np.ascontiguousarray(px)
+        if px.dtype not in (np.float32, np.float64):
+            px = px.astype(np.float64)
+        mask = np.ascontiguousarray(mask, dtype=np.uint8) if mask.dtype != np.bool_ \
+            else np.ascontiguousarray(mask).view(np.uint8)
+        h, w = px.shape
+        out = np.empty_like(px)
+        fn = self._L.fsr_reconstruct_f64 if px.dtype == np.float64 else self._L.fsr_reconstruct_f32
+        self._check(fn(self._h, ctypes.byref(params), _ptr(px), _ptr(mask), h, w, _ptr(out),
+                       _ptr(sel), _ptr(done)))
+        return out
+
+    def reconstruct_rows(self, px, mask, params: FsrParamsC, row0: int, row1: int, out):
+        """Strip call on host buffers: block rows [row0, row1) into ``out`` (full size)."""
+        h, w = px.shape
+        assert px.dtype == np.float32 and out.dtype == np.float32 and mask.dtype == np.uint8
+        assert px.flags.c_contiguous and out.flags.c_contiguous and mask.flags.c_contiguous
+        self._check(self._L.fsr_reconstruct_rows_f32(self._h, ctypes.byref(params), _ptr(px),
+                                                     _ptr(mask), h, w, row0, row1, _ptr(out)))
+        return out
+
+    def reconstruct_device(self, d_px, px_pitch, d_mask, mask_pitch, height, width, row0, row1,
+                           d_out, out_pitch, params: FsrParamsC, stream=0):
+        """Device pointers (ints), asynchronous on ``stream`` (a cudaStream_t as int)."""
+        self._check(self._L.fsr_reconstruct_device_f32(
+            self._h, ctypes.byref(params), ctypes.c_void_p(d_px), px_pitch,
+            ctypes.c_void_p(d_mask), mask_pitch, height, width, row0, row1,
+            ctypes.c_void_p(d_out), out_pitch, ctypes.c_void_p(stream)))
+
+    def iterate_spectra(self, R, G, W, wf, params: FsrParamsC, thr=None, sel=None, obj=None,
+                        ties=None, done=None):
+        """Array-level loop operator, in place on complex128 R and G."""
+        for name, a in (("R", R), ("G", G)):
+            if a.dtype != np.complex128 or not a.flags.c_contiguous:
+                raise ValueError(f"{name} must be C-contiguous complex128")
+        count, n, _ = R.shape
+        W = np.ascontiguousarray(W, dtype=np.complex128)
+        wf = np.ascontiguousarray(wf, dtype=np.float64)
+        thr = None if thr is None else np.ascontiguousarray(thr, dtype=np.float64)
+        self._check(self._L.fsr_iterate_spectra(
+            self._h, ctypes.byref(params), count, n, _ptr(R), _ptr(G), _ptr(W), _ptr(wf),
+            _ptr(thr), _ptr(sel), _ptr(obj), _ptr(ties), _ptr(done)))
+
+    def last_stats(self) -> dict:
+        s = FsrStatsC()
+        self._L.fsr_last_stats(self._h, ctypes.byref(s))
+        return {f: getattr(s, f) for f, _ in FsrStatsC._fields_ if f != "reserved"}
+
+
+_default = {}
+_default_lock = threading.Lock()
+
+
+def default_engine(devices=None) -> Engine:
+    key = tuple(devices) if devices else (0,)
+    with _default_lock:
+        eng = _default.get(key)
+        if eng is None:
+            eng = Engine(list(key))
+            _default[key] = eng
+        return eng

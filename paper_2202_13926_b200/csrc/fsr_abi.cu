@@ -1,0 +1,769 @@
+// fsr_abi.cu -- the C ABI of libfsr.so (include/fsr.h) and the engine behind it.
+//
+// Host side: parameter validation with the reference's messages
+// (core.py:63-80, reconstruction.py:58-61, 273-274), per-(N, rho) constant
+// tables (weights.py:18-27, 40-56), per-device buffers and streams, strip
+// partitioning of the block rows over the engine's devices, and
+// kernel dispatch:
+//   precision FP64            -> image_generic_kernel<double>  (validation)
+//   precision FP32, N=32,B<=5 -> warp32_kernel (+ fp64 re-run of guarded blocks)
+//   precision FP32, other N   -> image_generic_kernel<float>  (+ fp64 re-run)
+// No CPU fallback: without a CUDA device every entry point returns FSR_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/fsr.h"
+#include "fsr_common.cuh"
+#include "fsr_generic.cuh"
+#include "fsr_warp32.cuh"
+
+using namespace fsr;
+
+namespace {
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    int dev = -1;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct TableSet {
+    DevBuf f64, f32;  // decay[N*N] | wf[N*N] | cs[2N]
+};
+
+struct Counters {  // device-side, zeroed per call
+    unsigned int empty_count;
+    unsigned int rerun_count;
+    unsigned int ticket;
+    int status;
+    double acc[2];
+    double fill;
+};
+
+struct Device {
+    int id = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
+    DevBuf px, mask, out, sel, done, empty_list, rerun_list, counters;
+    DevBuf R, G, W, wf, thr, obj, ties;
+    std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
+    int launches = 0;
+};
+
+}  // namespace
+
+struct fsr_engine {
+    std::vector<std::unique_ptr<Device>> devs;
+    std::string err;
+    std::mutex mu;
+    fsr_stats stats{};
+    bool device_stats_pending = false;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(fsr_engine *eng, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (eng) eng->err = buf;
+    g_err = buf;
+    return code;
+}
+
+#define CUDA_TRY(eng, expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(eng, FSR_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__, #expr);                                           \
+    } while (0)
+
+// ----------------------------------------------------------------- tables
+// Host restatement of the reference tables in fp64 (the product computes its
+// own; bitwise identity with numpy is not required past the FFT boundary).
+void host_tables(int N, double rho, std::vector<double> &decay, std::vector<double> &wf,
+                 std::vector<double> &cs) {
+    decay.resize((size_t)N * N);
+    wf.resize((size_t)N * N);
+    cs.resize(2 * (size_t)N);
+    const double center = (N - 1) / 2.0;  // weights.py:21
+    for (int k = 0; k < N; ++k)
+        for (int l = 0; l < N; ++l) {
+            double dk = (k - center) * (k - center), dl = (l - center) * (l - center);
+            decay[(size_t)k * N + l] = std::pow(rho, std::sqrt(dk + dl));
+        }
+    // weights.py:50-56: folded = N/2 - |idx - N/2|; wf = (1 - sqrt2*sqrt(nk + nl))^2, >= 0
+    std::vector<double> norm(N);
+    for (int k = 0; k < N; ++k) {
+        double folded = N / 2.0 - std::fabs(k - N / 2.0);
+        norm[k] = folded * folded / (double)(N * N);
+    }
+    for (int k = 0; k < N; ++k)
+        for (int l = 0; l < N; ++l) {
+            double inner = 1.0 - std::sqrt(2.0) * std::sqrt(norm[k] + norm[l]);
+            double v = inner * inner;
+            wf[(size_t)k * N + l] = v > 0.0 ? v : 0.0;
+        }
+    // twiddles with exact quadrant symmetry
+    for (int j = 0; j < N; ++j) {
+        long double th = 2.0L * 3.14159265358979323846264338327950288L * (long double)j / N;
+        cs[2 * j] = (double)cosl(th);
+        cs[2 * j + 1] = (double)sinl(th);
+    }
+    for (int j = 0; j < N; ++j) {
+        int m = (N - j) % N;  // cos(-x) = cos(x), sin(-x) = -sin(x): exact mirror
+        if (m < j) {
+            cs[2 * j] = cs[2 * m];
+            cs[2 * j + 1] = -cs[2 * m + 1];
+        }
+        if (4 * j == N || 4 * j == 3 * N) cs[2 * j] = 0.0;
+        if (2 * j == N) cs[2 * j + 1] = 0.0;
+        if (j == 0) cs[1] = 0.0;
+    }
+}
+
+template <typename Real>
+int get_tables(fsr_engine *eng, Device &d, int N, double rho, Tables<Real> &out) {
+    auto key = std::make_pair(N, rho);
+    auto it = d.tables.find(key);
+    if (it == d.tables.end()) {
+        std::vector<double> decay, wf, cs;
+        host_tables(N, rho, decay, wf, cs);
+        auto ts = std::make_unique<TableSet>();
+        size_t n = (size_t)N * N, tot = 2 * n + 2 * (size_t)N;
+        std::vector<double> all;
+        all.insert(all.end(), decay.begin(), decay.end());
+        all.insert(all.end(), wf.begin(), wf.end());
+        all.insert(all.end(), cs.begin(), cs.end());
+        std::vector<float> allf(all.begin(), all.end());
+        CUDA_TRY(eng, ts->f64.ensure(tot * sizeof(double)));
+        CUDA_TRY(eng, ts->f32.ensure(tot * sizeof(float)));
+        CUDA_TRY(eng, cudaMemcpy(ts->f64.p, all.data(), tot * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_TRY(eng, cudaMemcpy(ts->f32.p, allf.data(), tot * sizeof(float), cudaMemcpyHostToDevice));
+        it = d.tables.emplace(key, std::move(ts)).first;
+    }
+    const size_t n = (size_t)N * N;
+    const Real *base = sizeof(Real) == 8 ? (const Real *)it->second->f64.p : (const Real *)it->second->f32.p;
+    out.decay = base;
+    out.wf = base + n;
+    out.cs = base + 2 * n;
+    return FSR_OK;
+}
+
+// ------------------------------------------------------------ validation
+int validate(const fsr_params *p, char *msg, int len) {
+    auto set = [&](const char *m) {
+        if (msg && len > 0) snprintf(msg, len, "%s", m);
+        return FSR_EINVAL;
+    };
+    if (!p) return set("null parameters");
+    if (p->block < 1) return set("target block size must be at least 1");
+    if (p->border < 0) return set("border must be non-negative");
+    if (!(p->rho > 0.0 && p->rho < 1.0)) return set("decay factor rho must lie in (0, 1)");
+    if (!(p->gamma > 0.0 && p->gamma <= 1.0))
+        return set("compensation factor gamma must lie in (0, 1]");
+    if (p->iterations < 0) return set("iteration count must be non-negative");
+    if (p->reducer != FSR_REDUCER_TREE && p->reducer != FSR_REDUCER_LINEAR)
+        return set("unknown argmax strategy, expected one of ('tree', 'linear')");
+    if (p->precision < FSR_PREC_FP64 || p->precision > FSR_PREC_FP32_UNGUARDED)
+        return set("unknown precision");
+    if (p->argmax_impl < FSR_ARGMAX_SHFL || p->argmax_impl > FSR_ARGMAX_REDUX)
+        return set("unknown argmax implementation");
+    const int64_t s = (int64_t)p->block + 2 * (int64_t)p->border;
+    if (s < 2) return set("support must be at least 2");
+    if (s > 64) {
+        if (msg && len > 0)
+            snprintf(msg, len, "support block %lldx%lld exceeds the 64x64 engine limit",
+                     (long long)s, (long long)s);
+        return FSR_EUNSUPPORTED;
+    }
+    if (p->reducer == FSR_REDUCER_TREE && s * s > 1024) {
+        if (msg && len > 0)
+            snprintf(msg, len,
+                     "support block %lldx%lld exceeds the 1024-lane reduction capacity",
+                     (long long)s, (long long)s);
+        return FSR_EINVAL;
+    }
+    if (!(p->guard_tau >= 0.0 && p->guard_tau < 1.0)) return set("guard_tau must lie in [0, 1)");
+    return FSR_OK;
+}
+
+int check_params(fsr_engine *eng, const fsr_params *p) {
+    char msg[256] = {0};
+    int rc = validate(p, msg, sizeof msg);
+    if (rc != FSR_OK) return fail(eng, rc, "%s", msg);
+    return FSR_OK;
+}
+
+size_t generic_smem(int N, size_t real_bytes) { return (size_t)2 * N * N * 2 * real_bytes; }
+
+template <typename Real, typename IO>
+int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, cudaStream_t st) {
+    size_t smem = generic_smem(a.N, sizeof(Real));
+    auto k = image_generic_kernel<Real, IO>;
+    if (smem > 48 * 1024) CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, GEN_THREADS, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+template <int WARPS, bool TREE, int AM, bool GUARD>
+int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, cudaStream_t st) {
+    auto k = warp32_kernel<WARPS, TREE, AM, GUARD>;
+    const size_t smem = sizeof(Warp32Smem<WARPS>);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (a.nblocks + WARPS - 1) / WARPS;
+    int grid = (int)std::min<int64_t>(want, (int64_t)d.sms * per_sm);
+    if (grid < 1) grid = 1;
+    k<<<grid, WARPS * 32, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+constexpr int kWarps = 4;
+
+int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, bool tree, int am, bool guard,
+                  cudaStream_t st) {
+#define FSR_W32(T, A, G) \
+    if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, st);
+    FSR_W32(true, AM_SHFL, true) FSR_W32(true, AM_SHFL, false)
+    FSR_W32(false, AM_SHFL, true) FSR_W32(false, AM_SHFL, false)
+    FSR_W32(true, AM_REDUX, true) FSR_W32(true, AM_REDUX, false)
+    FSR_W32(false, AM_REDUX, true) FSR_W32(false, AM_REDUX, false)
+    FSR_W32(true, AM_SMEM, true) FSR_W32(true, AM_SMEM, false)
+    FSR_W32(false, AM_SMEM, true) FSR_W32(false, AM_SMEM, false)
+#undef FSR_W32
+    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+}
+
+bool warp32_eligible(const fsr_params *p) {
+    const int N = p->block + 2 * p->border;
+    return N == 32 && p->block * p->block <= 32 && p->precision != FSR_PREC_FP64;
+}
+
+// Enqueue the whole image path for target-block rows [row0, row1) on device d.
+// px/mask/out are "virtual" row-0 pointers (absolute row y at ptr + y*pitch).
+// device_fill: compute the empty-support fill value on the device from rows [0, H).
+template <typename IO>
+int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, int64_t px_pitch,
+                  const uint8_t *mask, int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H,
+                  int64_t W, int64_t row0, int64_t row1, int32_t *sel, int32_t *done,
+                  bool device_fill, double host_fill, cudaStream_t st) {
+    const int N = p->block + 2 * p->border;
+    const int64_t bcols = (W + p->block - 1) / p->block;
+    const int64_t first = row0 * bcols, nblocks = (row1 - row0) * bcols;
+    if (nblocks <= 0) return FSR_OK;
+    CUDA_TRY(eng, d.counters.ensure(sizeof(Counters)));
+    CUDA_TRY(eng, d.empty_list.ensure((size_t)nblocks * sizeof(int32_t)));
+    CUDA_TRY(eng, cudaMemsetAsync(d.counters.p, 0, sizeof(Counters), st));
+    Counters *ctr = d.counters.as<Counters>();
+    const bool guarded = p->precision == FSR_PREC_FP32;
+    if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
+    const int gen_grid = d.sms * 8;
+    int rc = FSR_OK;
+    if (p->precision == FSR_PREC_FP64 || !(std::is_same<IO, float>::value && warp32_eligible(p))) {
+        if (p->precision == FSR_PREC_FP64) {
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            ImageArgs<double, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
+                                    p->block, p->border, N, p->iterations, bcols, first, nblocks,
+                                    nullptr, nullptr, p->gamma, p->reducer == FSR_REDUCER_TREE,
+                                    p->early_stop, tab, sel, done, &ctr->empty_count,
+                                    d.empty_list.as<int32_t>()};
+            if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
+            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+        } else {
+            // fp32 on the generic kernel: no near-tie guard there, so a guarded
+            // request is served in fp64 (exact) for these supports
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            if (p->precision == FSR_PREC_FP32_UNGUARDED) {
+                Tables<float> tf;
+                if ((rc = get_tables<float>(eng, d, N, p->rho, tf))) return rc;
+                ImageArgs<float, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
+                                       p->block, p->border, N, p->iterations, bcols, first,
+                                       nblocks, nullptr, nullptr, (float)p->gamma,
+                                       p->reducer == FSR_REDUCER_TREE, p->early_stop, tf, sel,
+                                       done, &ctr->empty_count, d.empty_list.as<int32_t>()};
+                if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
+                CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+            } else {
+                ImageArgs<double, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
+                                        p->block, p->border, N, p->iterations, bcols, first,
+                                        nblocks, nullptr, nullptr, p->gamma,
+                                        p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel,
+                                        done, &ctr->empty_count, d.empty_list.as<int32_t>()};
+                if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
+                CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+            }
+        }
+    } else {
+        Tables<float> tf;
+        if ((rc = get_tables<float>(eng, d, N, p->rho, tf))) return rc;
+        Warp32Args a{};
+        a.px = (const float *)px;
+        a.px_pitch = px_pitch;
+        a.mask = mask;
+        a.mask_pitch = mask_pitch;
+        a.out = (float *)out;
+        a.out_pitch = out_pitch;
+        a.H = H;
+        a.W = W;
+        a.B = p->block;
+        a.L = p->border;
+        a.iterations = p->iterations;
+        a.early_stop = p->early_stop;
+        a.bcols = bcols;
+        a.first = first;
+        a.nblocks = nblocks;
+        a.gamma = (float)p->gamma;
+        a.tau = (float)p->guard_tau;
+        a.decay = tf.decay;
+        a.wf = tf.wf;
+        a.sel = sel;
+        a.done = done;
+        a.empty_count = &ctr->empty_count;
+        a.empty_list = d.empty_list.as<int32_t>();
+        a.rerun_count = &ctr->rerun_count;
+        a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
+        if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl, guarded, st)))
+            return rc;
+        CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+        if (guarded) {
+            // fp64 re-run of the blocks whose fp32 greedy decisions were ambiguous
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            ImageArgs<double, IO> r{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
+                                    p->block, p->border, N, p->iterations, bcols, 0, 0,
+                                    d.rerun_list.as<int32_t>(), &ctr->rerun_count, p->gamma,
+                                    p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel, done,
+                                    &ctr->ticket /* scratch: empties already counted */, nullptr};
+            if ((rc = launch_generic(eng, d, r, gen_grid, st))) return rc;
+        }
+    }
+    if (device_fill) {
+        mean_known_kernel<IO><<<d.sms * 4, 256, 0, st>>>(px, px_pitch, mask, mask_pitch, H, W,
+                                                         &ctr->empty_count, ctr->acc, &ctr->ticket,
+                                                         &ctr->fill, &ctr->status);
+        d.launches++;
+        CUDA_TRY(eng, cudaGetLastError());
+        fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
+                                                      d.empty_list.as<int32_t>(),
+                                                      &ctr->empty_count, &ctr->fill, 0.0);
+        d.launches++;
+        CUDA_TRY(eng, cudaGetLastError());
+    } else if (host_fill == host_fill) {  // not NaN: fill value known on the host
+        fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
+                                                      d.empty_list.as<int32_t>(),
+                                                      &ctr->empty_count, nullptr, host_fill);
+        d.launches++;
+        CUDA_TRY(eng, cudaGetLastError());
+    }
+    return FSR_OK;
+}
+
+int select_device(fsr_engine *eng, Device &d) {
+    CUDA_TRY(eng, cudaSetDevice(d.id));
+    return FSR_OK;
+}
+
+// Host-buffer whole-image call: split block rows over devices, H2D strip+halo,
+// enqueue, D2H target rows.  The empty-support fill value is computed on the
+// host (from the caller's full image) only if some block had an empty window.
+template <typename IO>
+int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const uint8_t *mask,
+                     int64_t H, int64_t W, IO *out, int32_t *sel, int32_t *done,
+                     int64_t rbeg = 0, int64_t rend = -1) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    int rc = check_params(eng, p);
+    if (rc) return rc;
+    if (H < 1 || W < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
+    if (!px || !mask || !out) return fail(eng, FSR_EINVAL, "null image buffer");
+    if (p->precision == FSR_PREC_FP64 && !std::is_same<IO, double>::value)
+        return fail(eng, FSR_EINVAL, "fp64 validation mode needs float64 I/O");
+    const int B = p->block, L = p->border;
+    const int64_t brows_all = (H + B - 1) / B, bcols = (W + B - 1) / B;
+    if (rend < 0) rend = brows_all;
+    if (rbeg < 0 || rend > brows_all || rbeg > rend)
+        return fail(eng, FSR_EINVAL, "block-row range out of bounds");
+    const int64_t brows = rend - rbeg;
+    const int nd = (int)eng->devs.size();
+    const int64_t it_stride = std::max(p->iterations, 1);
+    eng->stats = fsr_stats{};
+    eng->device_stats_pending = false;
+    eng->stats.blocks = brows * bcols;
+    struct Part { int64_t row0, row1, ya, yb, oa, ob; };
+    std::vector<Part> parts(nd);
+    for (int g = 0; g < nd; ++g) {
+        Part &q = parts[g];
+        q.row0 = rbeg + brows * g / nd;
+        q.row1 = rbeg + brows * (g + 1) / nd;
+        q.ya = std::max<int64_t>(0, q.row0 * B - L);          // halo above
+        q.yb = std::min<int64_t>(H, q.row1 * B + L);          // halo below
+        q.oa = std::min<int64_t>(H, q.row0 * B);
+        q.ob = std::min<int64_t>(H, q.row1 * B);
+    }
+    for (int g = 0; g < nd; ++g) {
+        Device &d = *eng->devs[g];
+        const Part &q = parts[g];
+        if (q.row1 <= q.row0) continue;
+        if ((rc = select_device(eng, d))) return rc;
+        d.launches = 0;
+        const int64_t rows_in = q.yb - q.ya, rows_out = q.ob - q.oa;
+        CUDA_TRY(eng, d.px.ensure((size_t)rows_in * W * sizeof(IO)));
+        CUDA_TRY(eng, d.mask.ensure((size_t)rows_in * W));
+        CUDA_TRY(eng, d.out.ensure((size_t)rows_out * W * sizeof(IO)));
+        const int64_t nb = (q.row1 - q.row0) * bcols;
+        if (sel) CUDA_TRY(eng, d.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
+        if (done) CUDA_TRY(eng, d.done.ensure((size_t)nb * sizeof(int32_t)));
+        CUDA_TRY(eng, cudaMemcpyAsync(d.px.p, px + q.ya * W, (size_t)rows_in * W * sizeof(IO),
+                                      cudaMemcpyHostToDevice, d.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(d.mask.p, mask + q.ya * W, (size_t)rows_in * W,
+                                      cudaMemcpyHostToDevice, d.stream));
+        CUDA_TRY(eng, cudaEventRecord(d.ev0, d.stream));
+        const IO *vpx = d.px.as<IO>() - q.ya * W;
+        const uint8_t *vmask = d.mask.as<uint8_t>() - q.ya * W;
+        IO *vout = d.out.as<IO>() - q.oa * W;
+        int32_t *vsel = sel ? d.sel.as<int32_t>() - q.row0 * bcols * it_stride : nullptr;
+        int32_t *vdone = done ? d.done.as<int32_t>() - q.row0 * bcols : nullptr;
+        rc = enqueue_image<IO>(eng, d, p, vpx, W, vmask, W, vout, W, H, W, q.row0, q.row1, vsel,
+                               vdone, false, NAN, d.stream);
+        if (rc) return rc;
+        CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(out + q.oa * W, d.out.p, (size_t)rows_out * W * sizeof(IO),
+                                      cudaMemcpyDeviceToHost, d.stream));
+        if (sel)
+            CUDA_TRY(eng, cudaMemcpyAsync(sel + q.row0 * bcols * it_stride, d.sel.p,
+                                          (size_t)nb * it_stride * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, d.stream));
+        if (done)
+            CUDA_TRY(eng, cudaMemcpyAsync(done + q.row0 * bcols, d.done.p, (size_t)nb * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, d.stream));
+    }
+    unsigned empty_total = 0;
+    std::vector<Counters> ctrs(nd);
+    for (int g = 0; g < nd; ++g) {
+        Device &d = *eng->devs[g];
+        if (parts[g].row1 <= parts[g].row0) continue;
+        if ((rc = select_device(eng, d))) return rc;
+        CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
+        CUDA_TRY(eng, cudaMemcpy(&ctrs[g], d.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost));
+        empty_total += ctrs[g].empty_count;
+        eng->stats.rerun_blocks += ctrs[g].rerun_count;
+        eng->stats.kernel_launches += d.launches;
+        if (g == 0) {
+            float ms = 0.f, mm = 0.f;
+            if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+            if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
+            (void)cudaGetLastError();
+            eng->stats.kernel_ms = ms;
+            eng->stats.main_ms = mm;
+        }
+    }
+    eng->stats.empty_blocks = empty_total;
+    if (empty_total > 0) {
+        // reconstruction.py:236-237, 272-275
+        double s = 0.0;
+        int64_t known = 0;
+        for (int64_t i = 0; i < H * W; ++i)
+            if (mask[i]) {
+                s += (double)px[i];
+                ++known;
+            }
+        if (known == 0) return fail(eng, FSR_ENOSAMPLES, "no known samples");
+        const double fill = s / (double)known;
+        const int64_t bc = bcols;
+        for (int g = 0; g < nd; ++g) {
+            Device &d = *eng->devs[g];
+            const Part &q = parts[g];
+            if (q.row1 <= q.row0 || ctrs[g].empty_count == 0) continue;
+            // host-side fill of the listed blocks (rare path)
+            std::vector<int32_t> list(ctrs[g].empty_count);
+            if ((rc = select_device(eng, d))) return rc;
+            CUDA_TRY(eng, cudaMemcpy(list.data(), d.empty_list.p, list.size() * sizeof(int32_t),
+                                     cudaMemcpyDeviceToHost));
+            for (int32_t bid : list) {
+                int64_t r0 = (bid / bc) * B, c0 = (bid % bc) * B;
+                for (int64_t y = r0; y < std::min<int64_t>(H, r0 + B); ++y)
+                    for (int64_t x = c0; x < std::min<int64_t>(W, c0 + B); ++x) out[y * W + x] = (IO)fill;
+            }
+        }
+    }
+    return FSR_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+void fsr_params_init(fsr_params *p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    p->block = 4;
+    p->border = 14;
+    p->iterations = 100;
+    p->reducer = FSR_REDUCER_TREE;
+    p->early_stop = 0;
+    p->precision = FSR_PREC_FP32;
+    p->argmax_impl = FSR_ARGMAX_SHFL;
+    p->rho = 0.7;
+    p->gamma = 0.5;
+    p->guard_tau = 1e-4;
+}
+
+int fsr_params_validate(const fsr_params *p, char *msg, int msg_len) {
+    return validate(p, msg, msg_len);
+}
+
+int32_t fsr_abi_version(void) { return FSR_ABI_VERSION; }
+
+const char *fsr_status_string(int status) {
+    switch (status) {
+        case FSR_OK: return "ok";
+        case FSR_EINVAL: return "invalid argument";
+        case FSR_ENOSAMPLES: return "no known samples";
+        case FSR_ECUDA: return "CUDA error";
+        case FSR_EUNSUPPORTED: return "unsupported";
+        default: return "unknown status";
+    }
+}
+
+const char *fsr_last_error(const fsr_engine *eng) {
+    return eng ? eng->err.c_str() : g_err.c_str();
+}
+
+int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **out) {
+    if (!out) return fail(nullptr, FSR_EINVAL, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count < 1)
+        return fail(nullptr, FSR_ECUDA, "no CUDA device available (%s); libfsr has no CPU fallback",
+                    cudaGetErrorString(e));
+    auto eng = std::make_unique<fsr_engine>();
+    std::vector<int> ids;
+    if (!devices || n_devices <= 0) ids.push_back(0);
+    else ids.assign(devices, devices + n_devices);
+    for (int id : ids) {
+        if (id < 0 || id >= count) return fail(nullptr, FSR_EINVAL, "invalid device id %d", id);
+        auto d = std::make_unique<Device>();
+        d->id = id;
+        CUDA_TRY(nullptr, cudaSetDevice(id));
+        cudaDeviceProp prop;
+        CUDA_TRY(nullptr, cudaGetDeviceProperties(&prop, id));
+        if (prop.major < 10)
+            return fail(nullptr, FSR_ECUDA, "device %d is sm_%d%d; libfsr is built for sm_100a",
+                        id, prop.major, prop.minor);
+        d->sms = prop.multiProcessorCount;
+        CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+        CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
+        CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));
+        CUDA_TRY(nullptr, cudaEventCreate(&d->ev_mid));
+        eng->devs.push_back(std::move(d));
+    }
+    *out = eng.release();
+    return FSR_OK;
+}
+
+void fsr_engine_destroy(fsr_engine *eng) {
+    if (!eng) return;
+    for (auto &dp : eng->devs) {
+        Device &d = *dp;
+        cudaSetDevice(d.id);
+        cudaStreamSynchronize(d.stream);
+        for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list,
+                          &d.counters, &d.R, &d.G, &d.W, &d.wf, &d.thr, &d.obj, &d.ties})
+            b->release();
+        for (auto &kv : d.tables) {
+            kv.second->f64.release();
+            kv.second->f32.release();
+        }
+        cudaEventDestroy(d.ev0);
+        cudaEventDestroy(d.ev1);
+        cudaEventDestroy(d.ev_mid);
+        cudaStreamDestroy(d.stream);
+    }
+    delete eng;
+}
+
+int fsr_reconstruct_f64(fsr_engine *eng, const fsr_params *p, const double *px,
+                        const uint8_t *mask, int64_t height, int64_t width, double *out,
+                        int32_t *sel, int32_t *done) {
+    return reconstruct_host<double>(eng, p, px, mask, height, width, out, sel, done);
+}
+
+int fsr_reconstruct_f32(fsr_engine *eng, const fsr_params *p, const float *px,
+                        const uint8_t *mask, int64_t height, int64_t width, float *out,
+                        int32_t *sel, int32_t *done) {
+    return reconstruct_host<float>(eng, p, px, mask, height, width, out, sel, done);
+}
+
+int fsr_reconstruct_rows_f32(fsr_engine *eng, const fsr_params *p, const float *px,
+                             const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
+                             int64_t row1, float *out) {
+    return reconstruct_host<float>(eng, p, px, mask, height, width, out, nullptr, nullptr, row0,
+                                   row1);
+}
+
+int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
+                               int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
+                               int64_t height, int64_t width, int64_t row0, int64_t row1,
+                               float *d_out, int64_t out_pitch, void *stream) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    int rc = check_params(eng, p);
+    if (rc) return rc;
+    if (p->precision == FSR_PREC_FP64)
+        return fail(eng, FSR_EINVAL, "fp64 validation mode needs float64 I/O");
+    if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
+    const int64_t brows = (height + p->block - 1) / p->block;
+    if (row0 < 0 || row1 > brows || row0 > row1) return fail(eng, FSR_EINVAL, "block-row range out of bounds");
+    Device &d = *eng->devs[0];
+    if ((rc = select_device(eng, d))) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    d.launches = 0;
+    CUDA_TRY(eng, cudaEventRecord(d.ev0, st));
+    rc = enqueue_image<float>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
+                              height, width, row0, row1, nullptr, nullptr, true, NAN, st);
+    CUDA_TRY(eng, cudaEventRecord(d.ev1, st));
+    eng->stats = fsr_stats{};
+    eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
+    eng->stats.kernel_launches = d.launches;
+    eng->device_stats_pending = rc == FSR_OK;
+    return rc;
+}
+
+int fsr_last_stats(const fsr_engine *eng_c, fsr_stats *out) {
+    if (!eng_c || !out) return FSR_EINVAL;
+    fsr_engine *eng = const_cast<fsr_engine *>(eng_c);
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (eng->device_stats_pending) {
+        // the device-API call was asynchronous: wait for it, then read the counters
+        Device &d = *eng->devs[0];
+        int rc = select_device(eng, d);
+        if (rc) return rc;
+        CUDA_TRY(eng, cudaEventSynchronize(d.ev1));
+        float ms = 0.f, mm = 0.f;
+        if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+        if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
+        (void)cudaGetLastError();
+        Counters c;
+        CUDA_TRY(eng, cudaMemcpy(&c, d.counters.p, sizeof c, cudaMemcpyDeviceToHost));
+        eng->stats.kernel_ms = ms;
+        eng->stats.main_ms = mm;
+        eng->stats.rerun_blocks = c.rerun_count;
+        eng->stats.empty_blocks = c.empty_count;
+        eng->device_stats_pending = false;
+    }
+    *out = eng->stats;
+    return FSR_OK;
+}
+
+int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int32_t N,
+                        double *R, double *G, const double *W, const double *wf,
+                        const double *thr, int32_t *sel, double *obj, uint8_t *ties,
+                        int32_t *done) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (!p) return fail(eng, FSR_EINVAL, "null parameters");
+    if (N < 1 || N > 64) return fail(eng, FSR_EUNSUPPORTED, "support %d outside [1, 64]", N);
+    if (p->iterations < 0) return fail(eng, FSR_EINVAL, "iteration count must be non-negative");
+    if (p->reducer != FSR_REDUCER_TREE && p->reducer != FSR_REDUCER_LINEAR)
+        return fail(eng, FSR_EINVAL, "unknown argmax strategy, expected one of ('tree', 'linear')");
+    if (p->reducer == FSR_REDUCER_TREE && N * N > 1024)
+        return fail(eng, FSR_EINVAL, "record count exceeds two-phase capacity");
+    if (count < 0 || !R || !G || !W || !wf) return fail(eng, FSR_EINVAL, "null or empty arrays");
+    if (count == 0) return FSR_OK;
+    Device &d = *eng->devs[0];
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    const size_t n = (size_t)N * N, cbytes = (size_t)count * n * 16;
+    const int64_t its = std::max(p->iterations, 1);
+    CUDA_TRY(eng, d.R.ensure(cbytes));
+    CUDA_TRY(eng, d.G.ensure(cbytes));
+    CUDA_TRY(eng, d.W.ensure(cbytes));
+    CUDA_TRY(eng, d.wf.ensure(n * 8));
+    if (thr) CUDA_TRY(eng, d.thr.ensure((size_t)count * 8));
+    if (sel) CUDA_TRY(eng, d.sel.ensure((size_t)count * its * 4));
+    if (obj) CUDA_TRY(eng, d.obj.ensure((size_t)count * its * 8));
+    if (ties) CUDA_TRY(eng, d.ties.ensure((size_t)count * its));
+    if (done) CUDA_TRY(eng, d.done.ensure((size_t)count * 4));
+    cudaStream_t st = d.stream;
+    CUDA_TRY(eng, cudaMemcpyAsync(d.R.p, R, cbytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(eng, cudaMemcpyAsync(d.G.p, G, cbytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(eng, cudaMemcpyAsync(d.W.p, W, cbytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(eng, cudaMemcpyAsync(d.wf.p, wf, n * 8, cudaMemcpyHostToDevice, st));
+    if (thr) CUDA_TRY(eng, cudaMemcpyAsync(d.thr.p, thr, (size_t)count * 8, cudaMemcpyHostToDevice, st));
+    IterateArgs a{count, N, p->iterations, p->reducer == FSR_REDUCER_TREE, p->gamma,
+                  d.R.as<cpx<double>>(), d.G.as<cpx<double>>(), d.W.as<const cpx<double>>(),
+                  d.wf.as<const double>(), thr ? d.thr.as<const double>() : nullptr,
+                  sel ? d.sel.as<int32_t>() : nullptr, obj ? d.obj.as<double>() : nullptr,
+                  ties ? d.ties.as<uint8_t>() : nullptr, done ? d.done.as<int32_t>() : nullptr};
+    const size_t smem = 2 * n * 16;
+    if (smem > 48 * 1024)
+        CUDA_TRY(eng, cudaFuncSetAttribute(iterate_spectra_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<int64_t>(count, (int64_t)d.sms * 8);
+    CUDA_TRY(eng, cudaEventRecord(d.ev0, st));
+    iterate_spectra_kernel<<<grid, GEN_THREADS, smem, st>>>(a);
+    CUDA_TRY(eng, cudaGetLastError());
+    CUDA_TRY(eng, cudaEventRecord(d.ev1, st));
+    CUDA_TRY(eng, cudaMemcpyAsync(R, d.R.p, cbytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(eng, cudaMemcpyAsync(G, d.G.p, cbytes, cudaMemcpyDeviceToHost, st));
+    if (sel) CUDA_TRY(eng, cudaMemcpyAsync(sel, d.sel.p, (size_t)count * its * 4, cudaMemcpyDeviceToHost, st));
+    if (obj) CUDA_TRY(eng, cudaMemcpyAsync(obj, d.obj.p, (size_t)count * its * 8, cudaMemcpyDeviceToHost, st));
+    if (ties) CUDA_TRY(eng, cudaMemcpyAsync(ties, d.ties.p, (size_t)count * its, cudaMemcpyDeviceToHost, st));
+    if (done) CUDA_TRY(eng, cudaMemcpyAsync(done, d.done.p, (size_t)count * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(eng, cudaStreamSynchronize(st));
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+    (void)cudaGetLastError();
+    eng->stats = fsr_stats{};
+    eng->stats.blocks = count;
+    eng->stats.kernel_launches = 1;
+    eng->stats.kernel_ms = ms;
+    return FSR_OK;
+}
+
+}  // extern "C"

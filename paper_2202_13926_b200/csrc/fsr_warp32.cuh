@@ -1,0 +1,352 @@
+// fsr_warp32.cuh -- production FSR kernel for support N = 32, fp32, one warp
+// per target block, everything register/shared-memory resident.
+//
+// Per block (reference path reconstruction.py:246-280 + _kernels.py:62-126):
+//   gather     lane l loads window column l (coalesced 128 B rows), mask-gated
+//              rho^d weights, packed z = f*w + i*w           (sampling.py:93-107,
+//                                                              weights.py:18-37)
+//   FFT        32-point in-register FFT along rows, smem transpose, FFT along
+//              columns; split Z into R = F{f w} and W = F{w}, exactly Hermitian
+//   loop       lane v owns spectral column v (R[u][v], u = 0..31, 64 regs);
+//              W lives in shared memory with duplicated rows so the circular
+//              shift W[(u-pu) mod 32][(v-pv) mod 32] is a per-lane base plus an
+//              immediate offset; the residual update of iteration it-1 is fused
+//              with the objective pass of iteration it, so R never leaves
+//              registers and W is read once per bin per iteration.
+//   argmax     per-lane running max over packed keys (objective bits with the
+//              5 low mantissa bits replaced by the row's tie rank), then a
+//              cross-lane step: __shfl_xor_sync butterfly on (key, lane rank)
+//              (the paper's register argmax), or redux.sync, or a shared-memory
+//              tree (the paper's comparison point) -- template ARGMAX.
+//   synthesis  lanes p < B*B accumulate g(m,n) += Re(gp e^{2 pi i(u m + v n)/32})
+//              directly (no inverse FFT, only the B x B target pixels), then
+//              merge (known pixels copied) and stitch.
+//   guard      fp32 near-tie guard: per-lane top-2 keys give the best and the
+//              second-best objective of every iteration (excluding the exact
+//              conjugate mirror while the state is exactly Hermitian); a block
+//              whose relative gap ever drops below tau is queued for an fp64
+//              re-run, which is what makes fp32 production match the fp64
+//              reference within tolerance.
+#pragma once
+
+#include "fsr_common.cuh"
+#include "fsr_fft.cuh"
+
+namespace fsr {
+
+enum ArgmaxImpl { AM_SHFL = 0, AM_SMEM = 1, AM_REDUX = 2 };
+
+constexpr int W32_N = 32;
+constexpr int W32_WROW = 32;                         // complex per W row
+constexpr int W32_WBYTES = 2 * 32 * W32_WROW * 8;    // duplicated rows: 16 KiB
+constexpr int W32_TILE_STRIDE = 33;                  // padded transpose tile row
+
+struct Warp32Args {
+    const float *px;
+    int64_t px_pitch;
+    const uint8_t *mask;
+    int64_t mask_pitch;
+    float *out;
+    int64_t out_pitch;
+    int64_t H, W;
+    int B, L, iterations, early_stop;
+    int64_t bcols, first, nblocks;
+    float gamma;
+    float tau;             // guard: relative gap threshold
+    const float *decay;    // [32*32]
+    const float *wf;       // [32*32]
+    int32_t *sel;          // [total blocks, iterations] or null
+    int32_t *done;         // [total blocks] or null
+    unsigned int *empty_count;
+    int32_t *empty_list;
+    unsigned int *rerun_count;
+    int32_t *rerun_list;
+};
+
+template <int WARPS>
+struct Warp32Smem {
+    float2 wbuf[WARPS][2 * 32 * W32_WROW];  // duplicated-row W, also the transpose tile
+    float2 cs[32];                          // cos/sin(2 pi j / 32)
+    unsigned int red_key[WARPS][32];        // AM_SMEM scratch
+    unsigned int red_rank[WARPS][32];
+};
+
+__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+
+// Extract R[u] for a warp-uniform dynamic u (jump table, no divergence).
+__device__ __forceinline__ float2 pick32(const cpx<float> (&R)[32], int u) {
+    float2 c;
+    switch (u) {
+#define FSR_PICK(i) \
+    case i: c = make_float2(R[i].re, R[i].im); break;
+        FSR_PICK(0) FSR_PICK(1) FSR_PICK(2) FSR_PICK(3) FSR_PICK(4) FSR_PICK(5) FSR_PICK(6)
+        FSR_PICK(7) FSR_PICK(8) FSR_PICK(9) FSR_PICK(10) FSR_PICK(11) FSR_PICK(12)
+        FSR_PICK(13) FSR_PICK(14) FSR_PICK(15) FSR_PICK(16) FSR_PICK(17) FSR_PICK(18)
+        FSR_PICK(19) FSR_PICK(20) FSR_PICK(21) FSR_PICK(22) FSR_PICK(23) FSR_PICK(24)
+        FSR_PICK(25) FSR_PICK(26) FSR_PICK(27) FSR_PICK(28) FSR_PICK(29) FSR_PICK(30)
+        default: c = make_float2(R[31].re, R[31].im); break;
+#undef FSR_PICK
+    }
+    return c;
+}
+
+// Cross-lane argmax on (key desc, rank asc); every lane gets the winner.
+template <int ARGMAX>
+__device__ __forceinline__ void cross_lane_best(uint32_t &key, uint32_t &rank,
+                                                unsigned int *skey, unsigned int *srank) {
+    const int lane = lane_id();
+    if (ARGMAX == AM_SHFL) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            uint32_t ok = __shfl_xor_sync(0xffffffffu, key, off);
+            uint32_t orank = __shfl_xor_sync(0xffffffffu, rank, off);
+            bool take = ok > key || (ok == key && orank < rank);
+            key = take ? ok : key;
+            rank = take ? orank : rank;
+        }
+    } else if (ARGMAX == AM_REDUX) {
+        uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+        uint32_t cand = key == kmax ? rank : 0xffffffffu;
+        rank = __reduce_min_sync(0xffffffffu, cand);
+        key = kmax;
+    } else {  // AM_SMEM: classic shared-memory tree reduction
+        skey[lane] = key;
+        srank[lane] = rank;
+        __syncwarp();
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) {
+            if (lane < s) {
+                uint32_t ok = skey[lane + s], orank = srank[lane + s];
+                uint32_t mk = skey[lane], mr = srank[lane];
+                if (ok > mk || (ok == mk && orank < mr)) {
+                    skey[lane] = ok;
+                    srank[lane] = orank;
+                }
+            }
+            __syncwarp();
+        }
+        key = skey[0];
+        rank = srank[0];
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t x) {
+    return __reduce_max_sync(0xffffffffu, x);
+}
+
+// One objective/update pass over the 32 rows a lane owns.
+// HERM: the state is exactly Hermitian, keys of non-canonical bins are zeroed.
+template <bool TREE, bool GUARD, bool HERM, bool UPDATE>
+__device__ __forceinline__ void pass32(cpx<float> (&R)[32], const float (&wfr)[17],
+                                       const float2 *wrow, float gr, float gi,
+                                       uint32_t canon, uint32_t &m1, uint32_t &m2) {
+    m1 = 0;
+    m2 = 0;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        float re = R[u].re, im = R[u].im;
+        if (UPDATE) {
+            const float2 w = wrow[u * W32_WROW];  // W[(u - pu) mod 32][(v - pv) mod 32]
+            re = fmaf(-gr, w.x, re);
+            re = fmaf(gi, w.y, re);
+            im = fmaf(-gr, w.y, im);
+            im = fmaf(-gi, w.x, im);
+            R[u].re = re;
+            R[u].im = im;
+        }
+        const float mag = fmaf(re, re, im * im);
+        const float o = mag * wfr[u <= 16 ? u : 32 - u];
+        const uint32_t rk = TREE ? ((u & 1) << 4 | (u & 2) << 2 | (u & 4) | (u & 8) >> 2 | (u & 16) >> 4)
+                                     : (uint32_t)u;
+        uint32_t key = (f2u(o) | 31u) ^ rk;  // low 5 bits = 31 - rank(u)
+        if (HERM && GUARD) key = ((canon >> u) & 1u) ? key : 0u;
+        if (GUARD) {
+            uint32_t t = min(m1, key);
+            m2 = max(m2, t);
+        }
+        m1 = max(m1, key);
+    }
+}
+
+template <int WARPS, bool TREE, int ARGMAX, bool GUARD>
+__global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
+    const int lane = lane_id(), wid = warp_id();
+    if (threadIdx.x < 32) {
+        const double th = 6.283185307179586476925286766559 * threadIdx.x / 32.0;
+        sm.cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
+    }
+    __syncthreads();
+    float2 *wb = sm.wbuf[wid];
+    const int v = lane;
+    const uint32_t lrank = TREE ? bitrev5(lane) : lane;
+    // canonical half of each mirror pair (lower tie rank), bit u of this lane's column
+    uint32_t canon = 0;
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        int t = u * 32 + v, mt = ((32 - u) & 31) * 32 + ((32 - v) & 31);
+        canon |= (uint32_t)(tie_rank(t, TREE) <= tie_rank(mt, TREE)) << u;
+    }
+    // folded frequency prior of this column: wf[u][v] == wf[32-u][v] (weights.py:40-56)
+    float wfr[17];
+#pragma unroll
+    for (int u = 0; u <= 16; ++u) wfr[u] = a.wf[u * 32 + v];
+
+    const int64_t total_warps = (int64_t)gridDim.x * WARPS;
+    for (int64_t i = (int64_t)blockIdx.x * WARPS + wid; i < a.nblocks; i += total_warps) {
+        const int64_t bid = a.first + i;
+        const int64_t brow = bid / a.bcols, bcol = bid - brow * a.bcols;
+        const int64_t r0 = brow * a.B, c0 = bcol * a.B;
+        const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
+        const bool xin = x >= 0 && x < a.W;
+        cpx<float> R[32];
+        float energy = 0.f;
+        // ---- gather: lane = window column; row k coalesced across lanes
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int64_t y = wr0 + k;
+            float f = 0.f, w = 0.f;
+            if (xin && y >= 0 && y < a.H) {
+                if (a.mask[y * a.mask_pitch + x]) {
+                    f = a.px[y * a.px_pitch + x];
+                    w = a.decay[k * 32 + lane];
+                }
+            }
+            R[k] = {f * w, w};
+            energy = fmaf(f * f, w, energy);
+        }
+        // ---- 2-D FFT of z: transpose (lane = row k), FFT over l, transpose, FFT over k
+        float2 *tile = wb;  // padded [32][33]
+#pragma unroll
+        for (int k = 0; k < 32; ++k) tile[k * W32_TILE_STRIDE + lane] = make_float2(R[k].re, R[k].im);
+        __syncwarp();
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            float2 z = tile[lane * W32_TILE_STRIDE + l];
+            R[l] = {z.x, z.y};
+        }
+        __syncwarp();
+        fft32(R);  // lane k: Y[k][v], register v
+#pragma unroll
+        for (int q = 0; q < 32; ++q) tile[lane * W32_TILE_STRIDE + q] = make_float2(R[q].re, R[q].im);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            float2 z = tile[k * W32_TILE_STRIDE + lane];
+            R[k] = {z.x, z.y};
+        }
+        __syncwarp();
+        fft32(R);  // lane v: Z[u][v], register u
+        // ---- split Z into R and W via the conjugate mirror Z[-u][-v]:
+        // Z -> upper half of wb (stride 32), W -> lower half, then duplicate rows.
+        float2 *zt = wb + 32 * W32_WROW;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = make_float2(R[u].re, R[u].im);
+        __syncwarp();
+        const int mv = (32 - lane) & 31;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const float2 zm = zt[((32 - u) & 31) * W32_WROW + mv];
+            const float zr = R[u].re, zi = R[u].im;
+            R[u] = {(zr + zm.x) * 0.5f, (zi - zm.y) * 0.5f};
+            wb[u * W32_WROW + lane] = make_float2((zi + zm.y) * 0.5f, (zm.x - zr) * 0.5f);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = wb[u * W32_WROW + lane];
+        __syncwarp();
+        const float w00 = wb[0].x;
+        int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
+            if (lane == 0) {
+                unsigned slot = atomicAdd(a.empty_count, 1u);
+                a.empty_list[slot] = (int32_t)bid;
+                if (a.done) a.done[bid] = 0;
+            }
+            if (sel_b)
+                for (int it = lane; it < a.iterations; it += 32) sel_b[it] = -1;
+            __syncwarp();
+            continue;
+        }
+        // early stop threshold: 1e-12 * sum f^2 w (reconstruction.py:262-266)
+        float thr = 0.f;
+        if (a.early_stop) {
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
+            thr = 1e-12f * energy;
+        }
+        const float ginv = a.gamma / w00;
+        // target pixel of this lane (p < B*B): window coordinates (L + m, L + n)
+        const int B = a.B;
+        const int pm = a.L + lane / B, pn = a.L + lane % B;
+        const bool has_pix = lane < B * B;
+        float acc = 0.f;
+        bool herm = true;
+        bool flagged = false;
+        float gr = 0.f, gi = 0.f;
+        int pu = 0, pv = 0;
+        int done = 0;
+        for (int it = 0; it < a.iterations; ++it) {
+            uint32_t m1, m2;
+            const float2 *wrow = wb + (32 - pu) * W32_WROW + ((v - pv) & 31);
+            if (it == 0) {
+                pass32<TREE, GUARD, true, false>(R, wfr, wrow, gr, gi, canon, m1, m2);
+            } else if (herm) {
+                pass32<TREE, GUARD, true, true>(R, wfr, wrow, gr, gi, canon, m1, m2);
+            } else {
+                pass32<TREE, GUARD, false, true>(R, wfr, wrow, gr, gi, canon, m1, m2);
+            }
+            uint32_t key = m1, rank = lrank;
+            cross_lane_best<ARGMAX>(key, rank, sm.red_key[wid], sm.red_rank[wid]);
+            const uint32_t urank = 31u - (key & 31u);
+            const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
+            const int bv = TREE ? (int)bitrev5(rank) : (int)rank;
+            if (GUARD) {
+                const uint32_t c2 = (lane == bv) ? m2 : m1;
+                const uint32_t k2 = warp_max_u32(c2);
+                const float b1 = __uint_as_float(key & ~31u), b2 = __uint_as_float(k2 & ~31u);
+                flagged |= b1 > 0.f && b2 >= b1 * (1.f - a.tau);
+                // a stop decision within tau of the threshold is also ambiguous
+                flagged |= thr > 0.f && fabsf(b1 - thr) <= a.tau * thr;
+            }
+            if (sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
+            if (thr > 0.f && __uint_as_float(key & ~31u) < thr) break;
+            float2 c = pick32(R, bu);
+            c.x = __shfl_sync(0xffffffffu, c.x, bv);
+            c.y = __shfl_sync(0xffffffffu, c.y, bv);
+            gr = c.x * ginv;
+            gi = c.y * ginv;
+            pu = bu;
+            pv = bv;
+            // a non-self-mirror selection breaks the exact Hermitian symmetry
+            herm = herm && (((32 - bu) & 31) == bu) && (((32 - bv) & 31) == bv);
+            if (has_pix) {
+                const float2 e = sm.cs[(bu * pm + bv * pn) & 31];
+                acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            }
+            done = it + 1;
+        }
+        if (sel_b)
+            for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
+        if (lane == 0) {
+            if (a.done) a.done[bid] = done;
+            if (GUARD && flagged) {
+                unsigned slot = atomicAdd(a.rerun_count, 1u);
+                a.rerun_list[slot] = (int32_t)bid;
+            }
+        }
+        // merge + stitch
+        if (has_pix) {
+            const int m = lane / B, n = lane % B;
+            const int64_t y = r0 + m, xx = c0 + n;
+            if (y < a.H && xx < a.W)
+                a.out[y * a.out_pitch + xx] =
+                    a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace fsr

@@ -22,7 +22,7 @@ def load_golden(name):
 
 def golden_image(name):
     """Load an image fixture; regenerate large inputs from their recipe."""
-    from oracle import oracle
+    from oracle import port as oracle
 
     d = load_golden(f"image_{name}.npz")
     if "recipe_kind" in d:

@@ -35,7 +35,7 @@ from fsrkit.weights import _decay_grid, build_weight_set, frequency_weight  # no
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle.oracle import make_natural_image  # noqa: E402  (restated fixture; checked below)
+from oracle.port import make_natural_image  # noqa: E402  (restated fixture; checked below)
 
 
 def ref_natural(size, seed):

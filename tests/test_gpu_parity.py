@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the reference.
+
+Anchors, all produced by the reference itself (tests/golden/make_golden.py)
+or by the oracle port pinned to it (tests/test_oracle.py):
+  * loop operator: bitwise equal to _kernels.reconstruct_iterations
+    (objectives, selections, ties, residual, model), both reducers;
+  * traced per-block path: identical selection sequences;
+  * image path, fp64 validation: per-block sequences equal modulo the
+    conjugate mirror, output within 1e-9 (0..1 scale), PSNR equal;
+  * image path, fp32 production: max |d| <= 1e-3 (0..1 scale), |dPSNR| <= 0.01 dB.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_image, load_golden
+from oracle import port as oracle
+
+pytestmark = pytest.mark.gpu
+
+fsr = pytest.importorskip("paper_2202_13926_b200")
+
+FP64_TOL = 1e-9 * 255.0   # validation mode, 0..255 scale
+FP32_TOL = 1e-3 * 255.0   # production mode
+PSNR_TOL = 0.01
+
+
+def _loop_cases():
+    d = load_golden("loop_cases.npz")
+    return d, [str(c) for c in d["cases"]]
+
+
+@pytest.mark.parametrize("case", _loop_cases()[1])
+def test_loop_operator_bitwise(case):
+    d, _ = _loop_cases()
+    R = d[case + "_R0"].copy()[None]
+    G = np.zeros_like(R)
+    W = d[case + "_W"][None]
+    iters = int(d[case + "_iters"])
+    gamma = float(d.get(case + "_gamma", 0.5))
+    thr = np.array([float(d.get(case + "_thr", 0.0))])
+    sel, obj, ties, done = fsr.reconstruct_batch(R, G, W, d[case + "_wf"], gamma, iters, 32,
+                                                 case.endswith("_tree"), thr, trace=True)
+    n = int(done[0])
+    assert n == int(d[case + "_done"])
+    assert np.array_equal(sel[0, :n], d[case + "_sel"])
+    assert np.array_equal(obj[0, :n], d[case + "_obj"])
+    assert np.array_equal(ties[0, :n], d[case + "_ties"])
+    assert np.array_equal(R[0], d[case + "_R"])
+    assert np.array_equal(G[0], d[case + "_G"])
+
+
+def test_loop_operator_batch_and_skip(rng):
+    """Many blocks in one launch, including an empty-support block that must be skipped."""
+    s, count, iters = 16, 64, 50
+    R, W, _, masks = oracle.block_spectra(oracle.synthetic_frame(64, 64, 5),
+                                          oracle.quarter_sample_mask((64, 64), 2), 4, 6, 0.7)
+    R, W = R[:count].copy(), W[:count].copy()
+    W[3] = 0.0  # empty support
+    wf = oracle.frequency_weight(s)
+    Rg, Gg = R.copy(), np.zeros_like(R)
+    Ro, Go = R.copy(), np.zeros_like(R)
+    fsr.reconstruct_batch(Rg, Gg, W, wf, 0.5, iters, 32, True, None)
+    oracle.reconstruct_batch(Ro, Go, W, wf, 0.5, iters, True)
+    assert np.array_equal(Rg, Ro) and np.array_equal(Gg, Go)
+    assert np.all(Gg[3] == 0)
+
+
+@pytest.mark.parametrize("name", ["odd_37x53_s16", "odd_37x53_s8_b2", "odd_29x31_s12_b6"])
+def test_traced_block_path_sequences(name):
+    d = golden_image(name)
+    params = fsr.FsrParams(block=int(d["block"]), border=int(d["border"]),
+                           iterations=int(d["iterations"]))
+    sampled = fsr.SampledImage(fsr.GrayImage(d["sampled"]), d["mask"])
+    descs = fsr.block_partition(*sampled.shape, params)
+    for red in ("tree", "linear"):
+        if "sel_" + red not in d:
+            continue
+        for i, desc in enumerate(descs):
+            blk = fsr.extract_support_block(sampled, desc, params.support)
+            ws = fsr.build_weight_set(params.support, 0.7, blk.mask)
+            r = fsr.reconstruct_block_full(blk, ws, params, red)
+            assert np.array_equal(r.selections.astype(np.int16),
+                                  d["sel_" + red][i, :r.iterations_run]), (name, red, i)
+
+
+IMAGES = ["odd_37x53_s16", "odd_37x53_s8_b2", "odd_29x31_s12_b6", "early_48x40_s16",
+          "emptysupport_40x64_s8", "c1_natural", "c1_uniform"]
+
+
+def _run(d, red, precision, **kw):
+    B, L, I = int(d["block"]), int(d["border"]), int(d["iterations"])
+    return fsr.reconstruct(d["sampled"], d["mask"], B, B + 2 * L, I, reducer=red,
+                           early_stop=bool(d["early_stop"]), precision=precision,
+                           return_trace=True, **kw)
+
+
+@pytest.mark.parametrize("name", IMAGES)
+def test_image_fp64_validation(name):
+    d = golden_image(name)
+    s = int(d["block"]) + 2 * int(d["border"])
+    for red in ("tree", "linear"):
+        if "out_" + red not in d:
+            continue
+        out, tr = _run(d, red, "fp64")
+        ref = d["out_" + red]
+        err = float(np.abs(out - ref).max())
+        assert err <= FP64_TOL, f"{name}/{red}: max|d| {err:.3e}"
+        assert abs(oracle.psnr(d["original"], out) - float(d["psnr_" + red])) <= 1e-6
+        if "sel_" + red in d:
+            I = int(d["iterations"])
+            counts, div = oracle.compare_sequences(tr.selections[:, :I].astype(np.int64),
+                                                   d["sel_" + red].astype(np.int64), s)
+            assert counts["diverged"] == 0, f"{name}/{red}: {counts}"
+        # known pixels are copied bitwise
+        assert np.array_equal(out[d["mask"]], d["sampled"][d["mask"]])
+
+
+@pytest.mark.parametrize("name", IMAGES)
+@pytest.mark.parametrize("argmax", ["shfl", "redux", "smem"])
+def test_image_fp32_production(name, argmax):
+    d = golden_image(name)
+    for red in ("tree", "linear"):
+        if "out_" + red not in d:
+            continue
+        out, tr = _run(d, red, "fp32", argmax=argmax)
+        assert out.dtype == np.float32
+        o = out.astype(np.float64)
+        ref = d["out_" + red]
+        err = float(np.abs(o - ref).max())
+        dpsnr = abs(oracle.psnr(d["original"], o) - float(d["psnr_" + red]))
+        assert err <= FP32_TOL, f"{name}/{red}/{argmax}: max|d| {err:.4f} stats {tr.stats}"
+        assert dpsnr <= PSNR_TOL, f"{name}/{red}/{argmax}: dPSNR {dpsnr:.4f}"
+        known = d["mask"]
+        assert np.array_equal(o[known], d["sampled"][known].astype(np.float32).astype(np.float64))
+
+
+def test_argmax_variants_identical():
+    d = golden_image("c1_natural")
+    outs = [_run(d, "tree", "fp32", argmax=a)[0] for a in ("shfl", "redux", "smem")]
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_strip_partition_determinism():
+    """Bitwise identical output for any strip split (SURVEY §8e determinism);
+    two strips on the same device exercise the halo logic on a 1-GPU box."""
+    d = golden_image("c1_natural")
+    one = fsr.reconstruct(d["sampled"], d["mask"], 4, 32, 100, devices=[0])
+    for devs in ([0, 0], [0, 0, 0], [0] * 8):
+        many = fsr.reconstruct(d["sampled"], d["mask"], 4, 32, 100, devices=devs)
+        assert np.array_equal(one, many), devs
+    again = fsr.reconstruct(d["sampled"], d["mask"], 4, 32, 100, devices=[0])
+    assert np.array_equal(one, again)
+
+
+def test_reconstruct_image_dropin_api():
+    d = golden_image("odd_37x53_s16")
+    sampled = fsr.SampledImage(fsr.GrayImage(d["sampled"]), d["mask"])
+    params = fsr.FsrParams(block=4, border=6, iterations=60, threads=8)
+    got = fsr.reconstruct_image(sampled, params, precision="fp64")
+    assert isinstance(got, fsr.GrayImage)
+    assert np.abs(got.pixels - d["out_tree"]).max() <= FP64_TOL
+    with pytest.raises(ValueError, match="unknown argmax strategy"):
+        fsr.reconstruct_image(sampled, params, reducer="bogus")
+
+
+def test_no_known_samples_raises():
+    img = np.zeros((20, 24))
+    with pytest.raises(ValueError, match="no known samples"):
+        fsr.reconstruct(img, np.zeros((20, 24), bool), 4, 8, 10)
+
+
+def test_other_supports_match_oracle():
+    """Generic (non-N=32) kernels: N = 6, 10, 20 and the N=64 linear extension."""
+    img = oracle.synthetic_frame(40, 44, 9)
+    sampled, mask = oracle.quarter_sample(img, 4)
+    for B, N, I, red in ((2, 6, 20, "tree"), (4, 10, 30, "linear"), (4, 20, 40, "tree")):
+        ref = oracle.reconstruct_image(sampled, mask, B, (N - B) // 2, I, 0.7, 0.5, red)
+        out64 = fsr.reconstruct(sampled, mask, B, N, I, reducer=red, precision="fp64")
+        assert np.abs(out64 - ref).max() <= FP64_TOL, (B, N)
+        out32 = fsr.reconstruct(sampled, mask, B, N, I, reducer=red, precision="fp32")
+        assert np.abs(out32 - ref).max() <= FP32_TOL, (B, N)
+    # N = 64 (outside the reference's FsrParams cap): linear reducer only
+    ref = oracle.reconstruct_image(sampled, mask, 4, 30, 20, 0.7, 0.5, "linear")
+    out = fsr.reconstruct(sampled, mask, 4, 64, 20, reducer="linear", precision="fp64")
+    assert np.abs(out - ref).max() <= FP64_TOL
+    with pytest.raises(ValueError):
+        fsr.reconstruct(sampled, mask, 4, 64, 20, reducer="tree")
+
+
+def test_device_api_matches_host_api():
+    torch = pytest.importorskip("torch")
+    d = golden_image("c1_natural")
+    px = torch.tensor(d["sampled"], dtype=torch.float32, device="cuda")
+    mk = torch.tensor(d["mask"].astype(np.uint8), device="cuda")
+    out = torch.empty_like(px)
+    from paper_2202_13926_b200 import _lib
+    eng = _lib.default_engine([0])
+    p = _lib.make_params(4, 14, 100)
+    H, W = px.shape
+    eng.reconstruct_device(px.data_ptr(), W, mk.data_ptr(), W, H, W, 0, (H + 3) // 4,
+                           out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    host = fsr.reconstruct(d["sampled"], d["mask"], 4, 32, 100)
+    assert np.array_equal(out.cpu().numpy(), host)

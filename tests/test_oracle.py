@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import golden_image, load_golden
-from oracle import oracle
+from oracle import port as oracle
 
 
 def reference_splitmix64(seed, count):
