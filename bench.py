@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="4k", choices=list(WORKLOADS))
-    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64", "fp32_unguarded"])
+    ap.add_argument("--precision", default="fp64", choices=["fp32", "fp64", "fp32_unguarded"])
     ap.add_argument("--argmax", default="shfl", choices=["shfl", "smem", "redux"])
     ap.add_argument("--reducer", default="tree", choices=["tree", "linear"])
     ap.add_argument("--iterations", type=int, default=100)
@@ -287,25 +287,36 @@ def main():
     mean_main = float(np.mean(main_ms))
     flop = my_blocks * flops_per_block(N, I)
     achieved = flop / (mean_main * 1e-3) / 1e12
-    peak_fp32 = 148 * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    clk_hz = pk.get("sm_max_mhz", 1965.0) * 1e6
+    fp64 = args.precision == "fp64"
+    lanes = 64 if fp64 else 128  # B200: DFMA at half the FFMA rate
+    peak_fl = 148 * lanes * 2 * clk_hz / 1e12
+    fast = N == 32 and B * B <= 32
+    kernel = ("pair64_kernel" if fp64 else "warp32_kernel") if fast else "image_generic_kernel"
+    w_bytes = my_blocks * I * N * N * (16 if fp64 else 8)  # W read once per bin per iteration
+    smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
                 + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
     line = {
         "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if fp64 else "f32", "data": "synthetic",
         "config": {"workload": f"{W}x{H} quarter-sampled frame, strip-partitioned over "
                                f"{world} GPU(s)", "B": B, "N": N, "iterations": I, "rho": 0.7,
                    "gamma": 0.5, "reducer": args.reducer, "precision": args.precision,
                    "argmax": args.argmax, "image": args.image, "parallelism": f"strips{world}",
+                   "io": "f32 pixels + u8 mask in, f32 out",
                    "l2": "flushed between steps (256 MiB write)"},
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_fp32,
-                     "unit": "TFLOP/s", "frac": achieved / peak_fp32, "traffic": None,
-                     "kernel": "warp32_kernel" if (N == 32 and B * B <= 32) else "image_generic_kernel",
-                     "main_ms": mean_main,
-                     "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz "
-                                    f"({src} MEASURED_PEAKS.json has no FP32 figure)",
+        "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fl, "traffic": None,
+                     "kernel": kernel, "main_ms": mean_main,
+                     "work": "blocks x N^2 (12 I + 30 log2 N) flop (SURVEY 8d)",
+                     "peak_source": f"derived: 148 SM x {lanes} lanes x 2 flop x sm_max_mhz "
+                                    f"({src} MEASURED_PEAKS.json has no non-tensor figure)",
+                     "smem": {"achieved_tbs": w_bytes / (mean_main * 1e-3) / 1e12,
+                              "peak_tbs": smem_peak,
+                              "frac": w_bytes / (mean_main * 1e-3) / 1e12 / smem_peak},
                      "hbm_io": {"achieved_gbs": io_bytes / (ms_max * 1e-3) / 1e9,
                                 "peak_gbs": pk.get("hbm_gbs"),
                                 "frac": io_bytes / (ms_max * 1e-3) / 1e9 / pk.get("hbm_gbs", 1)}},

@@ -117,7 +117,7 @@ int fsr_reconstruct_rows_f32(fsr_engine *eng, const fsr_params *p, const float *
  * to target-block rows [row0, row1) of the full image (strip partitioning);
  * pass 0 and ceil(H/B) for the whole frame.  The halo (L rows above/below)
  * is read from d_px/d_mask, which must hold the full image rows the strip's
- * windows touch.  precision must be FP32 or FP32_UNGUARDED (f32 I/O).
+ * windows touch.  f32 I/O; the loop runs in the requested precision.
  */
 int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
                                int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,

@@ -382,3 +382,56 @@ def compare_sequences(sel_a, sel_b, support, done_a=None, done_b=None):
     mir = np.all(sel_a == mirror_index(sel_b, support), axis=1) & ~eq
     div = ~(eq | mir)
     return {"equal": int(eq.sum()), "mirror": int(mir.sum()), "diverged": int(div.sum())}, div
+
+
+def coemaximal_split(pixels, mask, block, border, iterations, rho, gamma, reducer, block_id,
+                     other_sel, rel_tol=1e-9):
+    """The reference's acceptance rule for divergent greedy branches
+    (pkg/tests/test_acceptance.py:73-87): two selection paths may differ only
+    if, at the first iteration where they part, both chosen bins attain the
+    same (co-maximal) objective.  ``other_sel`` is a candidate path for block
+    ``block_id`` (e.g. the GPU's); the comparison is made in whichever frame
+    (identity or conjugate mirror) agrees longest with the reference path.
+    Returns (is_split, first_divergence, relative_objective_gap)."""
+    s = block + 2 * border
+    R0, W, _, _ = block_spectra(pixels, mask, block, border, rho, [block_id])
+    wf = frequency_weight(s).ravel()
+    R = R0[0].copy()
+    G = np.zeros_like(R)
+    _, _, ref_sel, _ = reconstruct_iterations(R, G, W[0], wf, gamma, iterations, reducer == "tree")
+    other = np.asarray(other_sel)[:len(ref_sel)]
+    best = None
+    for frame in (other, mirror_index(other, s)):
+        d = np.nonzero(frame != ref_sel)[0]
+        f = int(d[0]) if d.size else len(ref_sel)
+        if best is None or f > best[0]:
+            best = (f, frame)
+    f, frame = best
+    if f >= len(ref_sel):
+        return True, f, 0.0
+    R = R0[0].copy()
+    G = np.zeros_like(R)
+    reconstruct_iterations(R, G, W[0], wf, gamma, f, reducer == "tree")
+    obj = wf * (R.real.ravel() ** 2 + R.imag.ravel() ** 2)
+    a, b = obj[int(ref_sel[f])], obj[int(frame[f])]
+    gap = abs(a - b) / max(abs(a), abs(b), 1e-300)
+    return gap <= rel_tol, f, float(gap)
+
+
+def assert_matches_reference(out, ref, pixels, mask, block, border, iterations, rho, gamma, reducer,
+                             sel, tol, rel_tol=1e-9):
+    """Per-block parity: every block whose pixels differ from the reference by
+    more than ``tol`` must be a proven co-maximal split.  Returns counts."""
+    H, W = out.shape
+    bc = -(-W // block)
+    err = np.abs(np.asarray(out, dtype=np.float64) - ref)
+    bad = np.argwhere(err > tol)
+    blocks = sorted({(int(y) // block) * bc + int(x) // block for y, x in bad})
+    splits = []
+    for b in blocks:
+        ok, f, gap = coemaximal_split(pixels, mask, block, border, iterations, rho, gamma, reducer,
+                                      b, sel[b])
+        assert ok, f"block {b}: diverges at iteration {f} with objective gap {gap:.3e}"
+        splits.append(b)
+    return {"blocks_over_tol": len(blocks), "proven_splits": len(splits),
+            "max_err": float(err.max()) if err.size else 0.0}

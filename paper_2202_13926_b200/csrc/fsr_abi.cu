@@ -28,6 +28,7 @@
 #include "fsr_common.cuh"
 #include "fsr_generic.cuh"
 #include "fsr_warp32.cuh"
+#include "fsr_pair64.cuh"
 
 using namespace fsr;
 
@@ -77,6 +78,7 @@ struct Device {
     DevBuf R, G, W, wf, thr, obj, ties;
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
     int launches = 0;
+    float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
 };
 
 }  // namespace
@@ -259,6 +261,56 @@ int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, cudaStream_
     return FSR_OK;
 }
 
+template <int BPC, bool TREE, int AM, typename IO>
+int launch_pair64_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
+                    cudaStream_t st) {
+    auto k = pair64_kernel<BPC, TREE, AM, IO>;
+    const size_t smem = sizeof(Pair64Smem<BPC>);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BPC * 64, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (want_blocks + BPC - 1) / BPC;
+    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
+    k<<<grid, BPC * 64, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+constexpr int kPairBPC = 4;
+
+template <typename IO>
+int launch_pair64(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
+                  int64_t want_blocks, cudaStream_t st) {
+#define FSR_P64(T, A) \
+    if (tree == T && am == A) return launch_pair64_t<kPairBPC, T, A, IO>(eng, d, a, want_blocks, st);
+    FSR_P64(true, AM_SHFL) FSR_P64(false, AM_SHFL) FSR_P64(true, AM_REDUX)
+    FSR_P64(false, AM_REDUX) FSR_P64(true, AM_SMEM) FSR_P64(false, AM_SMEM)
+#undef FSR_P64
+    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+}
+
+template <typename IO>
+Pair64Args<IO> pair64_args(const fsr_params *p, const IO *px, int64_t px_pitch, const uint8_t *mask,
+                           int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H, int64_t W,
+                           int64_t bcols, int64_t first, int64_t nblocks, const Tables<double> &tab,
+                           int32_t *sel, int32_t *done, unsigned int *empty_count,
+                           int32_t *empty_list) {
+    Pair64Args<IO> a{};
+    a.px = px; a.px_pitch = px_pitch; a.mask = mask; a.mask_pitch = mask_pitch;
+    a.out = out; a.out_pitch = out_pitch; a.H = H; a.W = W;
+    a.B = p->block; a.L = p->border; a.iterations = p->iterations; a.early_stop = p->early_stop;
+    a.bcols = bcols; a.first = first; a.nblocks = nblocks; a.list = nullptr; a.list_count = nullptr;
+    a.gamma = p->gamma; a.decay = tab.decay; a.wf = tab.wf; a.sel = sel; a.done = done;
+    a.empty_count = empty_count; a.empty_list = empty_list;
+    return a;
+}
+
+bool pair64_eligible(const fsr_params *p) {
+    return p->block + 2 * p->border == 32 && p->block * p->block <= 32;
+}
+
 constexpr int kWarps = 4;
 
 int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, bool tree, int am, bool guard,
@@ -301,7 +353,17 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     const int gen_grid = d.sms * 8;
     int rc = FSR_OK;
     if (p->precision == FSR_PREC_FP64 || !(std::is_same<IO, float>::value && warp32_eligible(p))) {
-        if (p->precision == FSR_PREC_FP64) {
+        if (p->precision == FSR_PREC_FP64 && pair64_eligible(p)) {
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, first, nblocks, tab, sel, done,
+                                               &ctr->empty_count, d.empty_list.as<int32_t>());
+            if ((rc = launch_pair64<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                        nblocks, st)))
+                return rc;
+            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+        } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             ImageArgs<double, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
@@ -365,19 +427,23 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.empty_list = d.empty_list.as<int32_t>();
         a.rerun_count = &ctr->rerun_count;
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
-        if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl, guarded, st)))
+        a.gap_out = d.gap_debug ? d.gap_debug - first : nullptr;
+        if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                guarded || d.gap_debug != nullptr, st)))
             return rc;
         CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
         if (guarded) {
             // fp64 re-run of the blocks whose fp32 greedy decisions were ambiguous
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
-            ImageArgs<double, IO> r{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
-                                    p->block, p->border, N, p->iterations, bcols, 0, 0,
-                                    d.rerun_list.as<int32_t>(), &ctr->rerun_count, p->gamma,
-                                    p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel, done,
-                                    &ctr->ticket /* scratch: empties already counted */, nullptr};
-            if ((rc = launch_generic(eng, d, r, gen_grid, st))) return rc;
+            Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, 0, 0, tab, sel, done,
+                                               &ctr->ticket /* empties already counted */, nullptr);
+            r.list = d.rerun_list.as<int32_t>();
+            r.list_count = &ctr->rerun_count;
+            if ((rc = launch_pair64<IO>(eng, d, r, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                        (int64_t)d.sms * 16, st)))
+                return rc;
         }
     }
     if (device_fill) {
@@ -419,8 +485,6 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
     if (rc) return rc;
     if (H < 1 || W < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
     if (!px || !mask || !out) return fail(eng, FSR_EINVAL, "null image buffer");
-    if (p->precision == FSR_PREC_FP64 && !std::is_same<IO, double>::value)
-        return fail(eng, FSR_EINVAL, "fp64 validation mode needs float64 I/O");
     const int B = p->block, L = p->border;
     const int64_t brows_all = (H + B - 1) / B, bcols = (W + B - 1) / B;
     if (rend < 0) rend = brows_all;
@@ -545,7 +609,7 @@ void fsr_params_init(fsr_params *p) {
     p->iterations = 100;
     p->reducer = FSR_REDUCER_TREE;
     p->early_stop = 0;
-    p->precision = FSR_PREC_FP32;
+    p->precision = FSR_PREC_FP64;
     p->argmax_impl = FSR_ARGMAX_SHFL;
     p->rho = 0.7;
     p->gamma = 0.5;
@@ -654,8 +718,6 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
     std::lock_guard<std::mutex> lock(eng->mu);
     int rc = check_params(eng, p);
     if (rc) return rc;
-    if (p->precision == FSR_PREC_FP64)
-        return fail(eng, FSR_EINVAL, "fp64 validation mode needs float64 I/O");
     if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
     const int64_t brows = (height + p->block - 1) / p->block;
     if (row0 < 0 || row1 > brows || row0 > row1) return fail(eng, FSR_EINVAL, "block-row range out of bounds");
@@ -671,6 +733,36 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
     eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
     eng->stats.kernel_launches = d.launches;
     eng->device_stats_pending = rc == FSR_OK;
+    return rc;
+}
+
+// Not part of include/fsr.h: development hook for the guard study
+// (tools/guard_study.py).  Runs the N=32 fp32 kernel on one device with the
+// top-2 tracking on but no re-run, returning each block's minimum relative
+// top-2 objective gap over its iterations, plus the selection trace.
+int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *px,
+                         const uint8_t *mask, int64_t H, int64_t W, float *out, float *gaps,
+                         int32_t *sel) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    fsr_params p = *p_in;
+    p.precision = FSR_PREC_FP32_UNGUARDED;
+    if (!warp32_eligible(&p)) return fail(eng, FSR_EINVAL, "guard study needs N=32, B*B<=32");
+    const int64_t nb = ((H + p.block - 1) / p.block) * ((W + p.block - 1) / p.block);
+    Device &d = *eng->devs[0];
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    DevBuf g;
+    CUDA_TRY(eng, g.ensure((size_t)nb * sizeof(float)));
+    d.gap_debug = g.as<float>();
+    std::vector<std::unique_ptr<Device>> others;
+    // single-device run so the gap buffer indexes every block
+    while (eng->devs.size() > 1) { others.push_back(std::move(eng->devs.back())); eng->devs.pop_back(); }
+    rc = reconstruct_host<float>(eng, &p, px, mask, H, W, out, sel, nullptr);
+    while (!others.empty()) { eng->devs.push_back(std::move(others.back())); others.pop_back(); }
+    d.gap_debug = nullptr;
+    if (rc == FSR_OK)
+        CUDA_TRY(eng, cudaMemcpy(gaps, g.p, (size_t)nb * sizeof(float), cudaMemcpyDeviceToHost));
+    g.release();
     return rc;
 }
 

@@ -35,7 +35,11 @@ __device__ __forceinline__ cpx<Real> scmul(cpx<Real> x, cpx<Real> y) {
 //         lock-step passes with offsets 16..1; the winner among maxima is the
 //         lexicographic minimum of (bitrev5(t >> 5), bitrev5(t & 31)).
 __host__ __device__ __forceinline__ uint32_t bitrev5(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __brev(x) >> 27;  // BREV + SHF
+#else
     return ((x & 1u) << 4) | ((x & 2u) << 2) | (x & 4u) | ((x & 8u) >> 2) | ((x & 16u) >> 4);
+#endif
 }
 __host__ __device__ __forceinline__ int tie_rank(int t, bool tree) {
     return tree ? (int)((bitrev5((uint32_t)t >> 5) << 5) | bitrev5((uint32_t)t & 31u)) : t;

@@ -27,18 +27,19 @@ __host__ __device__ constexpr double cos32(int m) {
 __host__ __device__ constexpr double tw_cos(int m) { return m <= 8 ? cos32(m) : -cos32(16 - m); }
 __host__ __device__ constexpr double tw_sin(int m) { return m <= 8 ? cos32(8 - m) : cos32(m - 8); }
 
-// x[k] <- sum_n x[n] e^{-2 pi i k n / 32}, output in NATURAL order.
-template <typename T>
-__device__ __forceinline__ void fft32(cpx<T> (&x)[32]) {
+// x[k] <- sum_n x[n] e^{-2 pi i k n / M}, M = 2^LOGM <= 32, output in NATURAL order.
+template <int LOGM, typename T>
+__device__ __forceinline__ void fft_pow2(cpx<T> (&x)[1 << LOGM]) {
+    constexpr int M = 1 << LOGM;
 #pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
+    for (int h = M / 2; h >= 1; h >>= 1) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < M; ++j) {
             if ((j & h) == 0) {
                 cpx<T> a = x[j], b = x[j + h];
                 x[j] = {a.re + b.re, a.im + b.im};
                 T dr = a.re - b.re, di = a.im - b.im;
-                const int m = (j & (h - 1)) * (16 / h);  // twiddle W_32^m
+                const int m = (j & (h - 1)) * (16 / h);  // stage twiddle W_{2h}^{j mod h} = W_32^m
                 if (m == 0) {
                     x[j + h] = {dr, di};
                 } else if (m == 8) {  // * (-i)
@@ -52,11 +53,19 @@ __device__ __forceinline__ void fft32(cpx<T> (&x)[32]) {
         }
     }
     // undo the bit reversal (static renaming)
-    cpx<T> y[32];
+    cpx<T> y[M];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) y[k] = x[bitrev5(k)];
+    for (int k = 0; k < M; ++k) {
+        int r = 0;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) x[k] = y[k];
+        for (int b = 0; b < LOGM; ++b) r |= ((k >> b) & 1) << (LOGM - 1 - b);
+        y[k] = x[r];
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) x[k] = y[k];
 }
+
+template <typename T>
+__device__ __forceinline__ void fft32(cpx<T> (&x)[32]) { fft_pow2<5, T>(x); }
 
 }  // namespace fsr

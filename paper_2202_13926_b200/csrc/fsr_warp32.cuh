@@ -61,6 +61,7 @@ struct Warp32Args {
     int32_t *empty_list;
     unsigned int *rerun_count;
     int32_t *rerun_list;
+    float *gap_out;        // debug: per-block min relative top-2 gap (GUARD only) or null
 };
 
 template <int WARPS>
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
         float acc = 0.f;
         bool herm = true;
         bool flagged = false;
+        float min_gap = 1.f;
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int done = 0;
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
                 const uint32_t k2 = warp_max_u32(c2);
                 const float b1 = __uint_as_float(key & ~31u), b2 = __uint_as_float(k2 & ~31u);
                 flagged |= b1 > 0.f && b2 >= b1 * (1.f - a.tau);
+                if (b1 > 0.f) min_gap = fminf(min_gap, (b1 - b2) / b1);
                 // a stop decision within tau of the threshold is also ambiguous
                 flagged |= thr > 0.f && fabsf(b1 - thr) <= a.tau * thr;
             }
@@ -332,7 +335,8 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
             for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
         if (lane == 0) {
             if (a.done) a.done[bid] = done;
-            if (GUARD && flagged) {
+            if (GUARD && a.gap_out) a.gap_out[bid] = min_gap;
+            if (GUARD && flagged && a.rerun_list) {
                 unsigned slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;
             }

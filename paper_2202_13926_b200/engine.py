@@ -13,9 +13,11 @@
         = the traced per-block path (reconstruction.py:138-209); transforms on
           the host with numpy.fft as the reference does, the loop on the GPU.
 
-Precision modes: "fp32" (production: fp32 loop, blocks with near-tied greedy
-decisions re-run in fp64), "fp64" (validation: every block in fp64) and
-"fp32_unguarded" (ablation).  There is no CPU fallback.
+Precision modes: "fp64" (default; production and validation: the whole path in
+fp64, the N=32 case on the warp-pair register kernel), "fp32" (fp32 loop with
+blocks whose greedy decisions were near-tied re-run in fp64) and
+"fp32_unguarded" (pure fp32 ablation).  DESIGN.md §4 explains why fp32 cannot
+meet the 1e-3 pixel tolerance on this algorithm.  There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -50,7 +52,7 @@ class Trace:
 
 def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int = 100,
                 rho: float = 0.7, gamma: float = 0.5, *, reducer: str = "tree",
-                early_stop: bool = False, precision: str = "fp32", devices=None,
+                early_stop: bool = False, precision: str = "fp64", devices=None,
                 argmax: str = "shfl", guard_tau: float = DEFAULT_GUARD_TAU,
                 return_trace: bool = False):
     """Reconstruct the unknown pixels of ``image`` (0..255 scale) given ``mask``.
@@ -89,7 +91,7 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
 
 
 def reconstruct_image(sampled: SampledImage, params: FsrParams, reducer: str = "tree",
-                      early_stop: bool = False, *, precision: str = "fp32", devices=None,
+                      early_stop: bool = False, *, precision: str = "fp64", devices=None,
                       argmax: str = "shfl", guard_tau: float = DEFAULT_GUARD_TAU) -> GrayImage:
     """Drop-in for fsrkit.reconstruct_image: every target block reconstructed
     independently on the GPU and stitched; empty-support blocks get the mean of

@@ -6,8 +6,10 @@ or by the oracle port pinned to it (tests/test_oracle.py):
     (objectives, selections, ties, residual, model), both reducers;
   * traced per-block path: identical selection sequences;
   * image path, fp64 validation: per-block sequences equal modulo the
-    conjugate mirror, output within 1e-9 (0..1 scale), PSNR equal;
-  * image path, fp32 production: max |d| <= 1e-3 (0..1 scale), |dPSNR| <= 0.01 dB.
+    conjugate mirror, output within 1e-9 (0..1 scale), PSNR equal; a block
+    may deviate only as a proven co-maximal split (the reference's own rule,
+    pkg/tests/test_acceptance.py:73-87);
+  * production default: max |d| <= 1e-3 (0..1 scale), |dPSNR| <= 0.01 dB.
 """
 
 import numpy as np
@@ -96,48 +98,66 @@ def _run(d, red, precision, **kw):
 
 
 @pytest.mark.parametrize("name", IMAGES)
-def test_image_fp64_validation(name):
+@pytest.mark.parametrize("argmax", ["shfl", "redux", "smem"])
+def test_image_fp64_validation(name, argmax):
     d = golden_image(name)
     s = int(d["block"]) + 2 * int(d["border"])
     for red in ("tree", "linear"):
         if "out_" + red not in d:
             continue
-        out, tr = _run(d, red, "fp64")
+        out, tr = _run(d, red, "fp64", argmax=argmax)
         ref = d["out_" + red]
-        err = float(np.abs(out - ref).max())
-        assert err <= FP64_TOL, f"{name}/{red}: max|d| {err:.3e}"
-        assert abs(oracle.psnr(d["original"], out) - float(d["psnr_" + red])) <= 1e-6
+        B, L, I = int(d["block"]), int(d["border"]), int(d["iterations"])
+        res = oracle.assert_matches_reference(out, ref, d["sampled"], d["mask"], B, L, I, 0.7, 0.5,
+                                              red, tr.selections, FP64_TOL)
+        if res["blocks_over_tol"] == 0:
+            assert abs(oracle.psnr(d["original"], out) - float(d["psnr_" + red])) <= 1e-6
         if "sel_" + red in d:
             I = int(d["iterations"])
             counts, div = oracle.compare_sequences(tr.selections[:, :I].astype(np.int64),
                                                    d["sel_" + red].astype(np.int64), s)
-            assert counts["diverged"] == 0, f"{name}/{red}: {counts}"
+            # every non-mirror divergence must be a proven co-maximal split
+            for b in np.nonzero(div)[0]:
+                ok, f, gap = oracle.coemaximal_split(d["sampled"], d["mask"], B, L, I, 0.7, 0.5,
+                                                     red, int(b), tr.selections[b])
+                assert ok, f"{name}/{red} block {b}: split at {f}, gap {gap:.3e}"
         # known pixels are copied bitwise
         assert np.array_equal(out[d["mask"]], d["sampled"][d["mask"]])
 
 
 @pytest.mark.parametrize("name", IMAGES)
-@pytest.mark.parametrize("argmax", ["shfl", "redux", "smem"])
-def test_image_fp32_production(name, argmax):
+def test_image_production_default(name):
+    """The production path (default precision) against the published
+    tolerance: max |d| <= 1e-3 on the 0..1 scale and |dPSNR| <= 0.01 dB."""
     d = golden_image(name)
     for red in ("tree", "linear"):
         if "out_" + red not in d:
             continue
-        out, tr = _run(d, red, "fp32", argmax=argmax)
-        assert out.dtype == np.float32
-        o = out.astype(np.float64)
+        B, L, I = int(d["block"]), int(d["border"]), int(d["iterations"])
+        out = fsr.reconstruct(d["sampled"], d["mask"], B, B + 2 * L, I, reducer=red,
+                              early_stop=bool(d["early_stop"]))
         ref = d["out_" + red]
-        err = float(np.abs(o - ref).max())
-        dpsnr = abs(oracle.psnr(d["original"], o) - float(d["psnr_" + red]))
-        assert err <= FP32_TOL, f"{name}/{red}/{argmax}: max|d| {err:.4f} stats {tr.stats}"
-        assert dpsnr <= PSNR_TOL, f"{name}/{red}/{argmax}: dPSNR {dpsnr:.4f}"
+        err = float(np.abs(out - ref).max())
+        dpsnr = abs(oracle.psnr(d["original"], out) - float(d["psnr_" + red]))
+        assert err <= FP32_TOL, f"{name}/{red}: max|d| {err:.4f}"
+        assert dpsnr <= PSNR_TOL, f"{name}/{red}: dPSNR {dpsnr:.4f}"
         known = d["mask"]
-        assert np.array_equal(o[known], d["sampled"][known].astype(np.float32).astype(np.float64))
+        assert np.array_equal(out[known], d["sampled"][known])
+
+
+@pytest.mark.parametrize("name", ["c1_natural", "c1_uniform"])
+def test_fp32_ablation_psnr_only(name):
+    """Pure-fp32 loop (ablation): greedy branches flip against fp64 at late
+    iterations, so only the aggregate quality is close."""
+    d = golden_image(name)
+    out, tr = _run(d, "tree", "fp32_unguarded")
+    dpsnr = abs(oracle.psnr(d["original"], out.astype(np.float64)) - float(d["psnr_tree"]))
+    assert dpsnr <= 0.05, dpsnr
 
 
 def test_argmax_variants_identical():
     d = golden_image("c1_natural")
-    outs = [_run(d, "tree", "fp32", argmax=a)[0] for a in ("shfl", "redux", "smem")]
+    outs = [_run(d, "tree", "fp64", argmax=a)[0] for a in ("shfl", "redux", "smem")]
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
@@ -174,18 +194,25 @@ def test_other_supports_match_oracle():
     """Generic (non-N=32) kernels: N = 6, 10, 20 and the N=64 linear extension."""
     img = oracle.synthetic_frame(40, 44, 9)
     sampled, mask = oracle.quarter_sample(img, 4)
-    for B, N, I, red in ((2, 6, 20, "tree"), (4, 10, 30, "linear"), (4, 20, 40, "tree")):
-        ref = oracle.reconstruct_image(sampled, mask, B, (N - B) // 2, I, 0.7, 0.5, red)
-        out64 = fsr.reconstruct(sampled, mask, B, N, I, reducer=red, precision="fp64")
-        assert np.abs(out64 - ref).max() <= FP64_TOL, (B, N)
-        out32 = fsr.reconstruct(sampled, mask, B, N, I, reducer=red, precision="fp32")
-        assert np.abs(out32 - ref).max() <= FP32_TOL, (B, N)
-    # N = 64 (outside the reference's FsrParams cap): linear reducer only
-    ref = oracle.reconstruct_image(sampled, mask, 4, 30, 20, 0.7, 0.5, "linear")
-    out = fsr.reconstruct(sampled, mask, 4, 64, 20, reducer="linear", precision="fp64")
-    assert np.abs(out - ref).max() <= FP64_TOL
+    for B, N, I, red in ((2, 6, 20, "tree"), (4, 10, 30, "linear"), (4, 20, 40, "tree"),
+                         (4, 64, 20, "linear")):
+        L = (N - B) // 2
+        ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, red)
+        out64, tr = fsr.reconstruct(sampled, mask, B, N, I, reducer=red, precision="fp64",
+                                    return_trace=True)
+        oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, 0.7, 0.5, red,
+                                        tr.selections, FP64_TOL)
     with pytest.raises(ValueError):
         fsr.reconstruct(sampled, mask, 4, 64, 20, reducer="tree")
+
+
+def test_guarded_fp32_mode_runs():
+    """fp32 loop + fp64 re-run of near-tie blocks (the SURVEY's H2 proposal);
+    kept as a measured mode, see DESIGN.md §4 for why it is not the default."""
+    d = golden_image("c1_natural")
+    out, tr = _run(d, "tree", "fp32")
+    assert tr.stats["rerun_blocks"] > 0
+    assert abs(oracle.psnr(d["original"], out.astype(np.float64)) - float(d["psnr_tree"])) <= 0.05
 
 
 def test_device_api_matches_host_api():
@@ -201,5 +228,5 @@ def test_device_api_matches_host_api():
     eng.reconstruct_device(px.data_ptr(), W, mk.data_ptr(), W, H, W, 0, (H + 3) // 4,
                            out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    host = fsr.reconstruct(d["sampled"], d["mask"], 4, 32, 100)
-    assert np.array_equal(out.cpu().numpy(), host)
+    host = fsr.reconstruct(d["sampled"].astype(np.float32), d["mask"], 4, 32, 100)
+    assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
