@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--precision", default="fp64", choices=["fp32", "fp64", "fp32_unguarded"])
     ap.add_argument("--argmax", default="shfl", choices=["shfl", "smem", "redux"])
     ap.add_argument("--reducer", default="tree", choices=["tree", "linear"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "warp", "pair"])
     ap.add_argument("--iterations", type=int, default=100)
     ap.add_argument("--support", type=int, default=32)
     ap.add_argument("--block", type=int, default=4)
@@ -214,7 +215,8 @@ def main():
     my_blocks = (row1 - row0) * bcols
 
     eng = _lib.Engine([local])
-    params = _lib.make_params(B, L, I, 0.7, 0.5, args.reducer, False, args.precision, args.argmax)
+    params = _lib.make_params(B, L, I, 0.7, 0.5, args.reducer, False, args.precision, args.argmax,
+                              kernel=args.kernel)
     dev = torch.device("cuda", local)
     d_px = torch.from_numpy(px32).to(dev)
     d_mask = torch.from_numpy(m8).to(dev)
@@ -292,7 +294,8 @@ def main():
     lanes = 64 if fp64 else 128  # B200: DFMA at half the FFMA rate
     peak_fl = 148 * lanes * 2 * clk_hz / 1e12
     fast = N == 32 and B * B <= 32
-    kernel = ("pair64_kernel" if fp64 else "warp32_kernel") if fast else "image_generic_kernel"
+    kernel = (("pair64_kernel" if args.kernel == "pair" else "warp64_kernel") if fp64
+              else "warp32_kernel") if fast else "image_generic_kernel"
     w_bytes = my_blocks * I * N * N * (16 if fp64 else 8)  # W read once per bin per iteration
     smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
@@ -305,7 +308,7 @@ def main():
         "config": {"workload": f"{W}x{H} quarter-sampled frame, strip-partitioned over "
                                f"{world} GPU(s)", "B": B, "N": N, "iterations": I, "rho": 0.7,
                    "gamma": 0.5, "reducer": args.reducer, "precision": args.precision,
-                   "argmax": args.argmax, "image": args.image, "parallelism": f"strips{world}",
+                   "argmax": args.argmax, "kernel": args.kernel, "image": args.image, "parallelism": f"strips{world}",
                    "io": "f32 pixels + u8 mask in, f32 out",
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,

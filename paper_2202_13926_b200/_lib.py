@@ -14,12 +14,14 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsr.so")
+# FSR_LIBFSR overrides the library path (used to A/B kernel build variants)
+LIB_PATH = os.environ.get("FSR_LIBFSR") or os.path.join(_HERE, "libfsr.so")
 
 FSR_OK, FSR_EINVAL, FSR_ENOSAMPLES, FSR_ECUDA, FSR_EUNSUPPORTED = 0, 1, 2, 3, 4
 REDUCER = {"tree": 0, "linear": 1}
 PRECISION = {"fp64": 0, "fp32": 1, "fp32_unguarded": 2}
 ARGMAX = {"shfl": 0, "smem": 1, "redux": 2}
+KERNEL = {"auto": 0, "warp": 1, "pair": 2}
 
 
 class FsrParamsC(ctypes.Structure):
@@ -31,7 +33,7 @@ class FsrParamsC(ctypes.Structure):
         ("early_stop", ctypes.c_int32),
         ("precision", ctypes.c_int32),
         ("argmax_impl", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("kernel", ctypes.c_int32),
         ("rho", ctypes.c_double),
         ("gamma", ctypes.c_double),
         ("guard_tau", ctypes.c_double),
@@ -113,7 +115,8 @@ def _ptr(a):
 
 
 def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer="tree",
-                early_stop=False, precision="fp64", argmax="shfl", guard_tau=1e-4) -> FsrParamsC:
+                early_stop=False, precision="fp64", argmax="shfl", guard_tau=1e-4,
+                kernel="auto") -> FsrParamsC:
     p = FsrParamsC()
     load().fsr_params_init(ctypes.byref(p))
     if reducer not in REDUCER:
@@ -125,7 +128,10 @@ def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer=
     p.block, p.border, p.iterations = int(block), int(border), int(iterations)
     p.rho, p.gamma = float(rho), float(gamma)
     p.reducer, p.early_stop = REDUCER[reducer], 1 if early_stop else 0
+    if kernel not in KERNEL:
+        raise ValueError(f"unknown kernel variant {kernel!r}, expected one of {tuple(KERNEL)}")
     p.precision, p.argmax_impl, p.guard_tau = PRECISION[precision], ARGMAX[argmax], float(guard_tau)
+    p.kernel = KERNEL[kernel]
     return p
 
 

@@ -29,6 +29,7 @@
 #include "fsr_generic.cuh"
 #include "fsr_warp32.cuh"
 #include "fsr_pair64.cuh"
+#include "fsr_warp64.cuh"
 
 using namespace fsr;
 
@@ -221,6 +222,7 @@ int validate(const fsr_params *p, char *msg, int len) {
         return FSR_EINVAL;
     }
     if (!(p->guard_tau >= 0.0 && p->guard_tau < 1.0)) return set("guard_tau must lie in [0, 1)");
+    if (p->kernel < 0 || p->kernel > 2) return set("unknown kernel variant");
     return FSR_OK;
 }
 
@@ -288,6 +290,39 @@ int launch_pair64(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree
     FSR_P64(true, AM_SHFL) FSR_P64(false, AM_SHFL) FSR_P64(true, AM_REDUX)
     FSR_P64(false, AM_REDUX) FSR_P64(true, AM_SMEM) FSR_P64(false, AM_SMEM)
 #undef FSR_P64
+    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+}
+
+template <int WARPS, bool TREE, int AM, typename IO>
+int launch_warp64_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
+                    cudaStream_t st) {
+    auto k = warp64_kernel<WARPS, TREE, AM, IO>;
+    const size_t smem = sizeof(Warp64Smem<WARPS>);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (want_blocks + WARPS - 1) / WARPS;
+    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
+    k<<<grid, WARPS * 32, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+constexpr int kWarp64Warps = 5;
+
+template <typename IO>
+int launch_fp64_n32(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, const fsr_params *p,
+                    int64_t want_blocks, cudaStream_t st) {
+    const bool tree = p->reducer == FSR_REDUCER_TREE;
+    const int am = p->argmax_impl;
+    if (p->kernel == 2) return launch_pair64<IO>(eng, d, a, tree, am, want_blocks, st);
+#define FSR_W64(T, A) \
+    if (tree == T && am == A) return launch_warp64_t<kWarp64Warps, T, A, IO>(eng, d, a, want_blocks, st);
+    FSR_W64(true, AM_SHFL) FSR_W64(false, AM_SHFL) FSR_W64(true, AM_REDUX)
+    FSR_W64(false, AM_REDUX) FSR_W64(true, AM_SMEM) FSR_W64(false, AM_SMEM)
+#undef FSR_W64
     return fail(eng, FSR_EINVAL, "unknown argmax implementation");
 }
 
@@ -359,9 +394,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
                                                &ctr->empty_count, d.empty_list.as<int32_t>());
-            if ((rc = launch_pair64<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
-                                        nblocks, st)))
-                return rc;
+            if ((rc = launch_fp64_n32<IO>(eng, d, a, p, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
         } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
@@ -441,9 +474,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                &ctr->ticket /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &ctr->rerun_count;
-            if ((rc = launch_pair64<IO>(eng, d, r, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
-                                        (int64_t)d.sms * 16, st)))
-                return rc;
+            if ((rc = launch_fp64_n32<IO>(eng, d, r, p, (int64_t)d.sms * 16, st))) return rc;
         }
     }
     if (device_fill) {

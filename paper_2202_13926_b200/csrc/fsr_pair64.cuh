@@ -64,6 +64,13 @@ struct __align__(16) PairSlot {
     double pad2;
 };
 
+// One greedy selection, kept for the deferred synthesis of the target pixels.
+struct __align__(16) SelEntry {
+    double gr, gi;  // gamma * c / W00
+    int u, v;       // selected bin
+    int pad[2];
+};
+
 template <int BPC>
 struct Pair64Smem {
     double2 buf[BPC][32 * 32];    // 16 KiB per block; the kernel aligns &buf to 16 KiB
@@ -71,8 +78,23 @@ struct Pair64Smem {
     PairSlot slot[BPC][2][2];     // [block][parity][half]
     unsigned int red_hi[BPC][2][32];
     unsigned int red_lo[BPC][2][32];
+    SelEntry hist[BPC][2][16];    // per half: every other selection, flushed every 32
+    double acc_x[BPC][32];        // half 1's partial pixel sums
     double2 cs[32];               // (cos, sin)(2 pi j / 32)
 };
+
+// Deferred synthesis: acc += sum_j Re(gp_j e^{2 pi i (u_j m + v_j n)/32}) over n entries.
+template <int BPC>
+__device__ __forceinline__ double p64_flush(const Pair64Smem<BPC> &sm, const SelEntry *h, int n,
+                                            int pm, int pn, double acc) {
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+        const SelEntry e = h[j];
+        const double2 cs = sm.cs[(e.u * pm + e.v * pn) & 31];
+        acc = fma(e.gr, cs.x, fma(-e.gi, cs.y, acc));
+    }
+    return acc;
+}
 
 // rows owned by half H, slot i = 0..15 (closed under u -> -u mod 32)
 __host__ __device__ constexpr int p64_row(int H, int i) {
@@ -344,42 +366,53 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
         const double ginv = a.gamma / w00;
         const int B = a.B;
         const int pm = a.L + lane / B, pn = a.L + lane % B;
-        const bool has_pix = H == 0 && lane < B * B;
+        const bool has_pix = lane < B * B;
         double acc = 0.0;
         double gr = 0.0, gi = 0.0;
         uint32_t P = 0, ycv = wb;
         const uint32_t cmask = 0x3FFu;
+        SelEntry *hist = sm.hist[pair][H];
         int done = 0;
         for (int it = 0; it < a.iterations; ++it) {
             unsigned long long kb = it == 0
                 ? p64_pass<H, TREE, false>(R, wfr, P, ycv, gr, gi, cmask)
                 : p64_pass<H, TREE, true>(R, wfr, P, ycv, gr, gi, cmask);
-            kb ^= lrank;  // lane-rank bits: 31 - lrank
-            const unsigned long long key = p64_warp_max<ARGMAX>(kb, sm.red_hi[pair][H],
-                                                                sm.red_lo[pair][H]);
-            const uint32_t klo = (uint32_t)key;
-            const uint32_t rr = 31u - ((klo >> 5) & 31u), lr = 31u - (klo & 31u);
-            const int bu = TREE ? (int)bitrev5(rr) : (int)rr;
-            const int bv = TREE ? (int)bitrev5(lr) : (int)lr;
-            double2 c = pick16(R, p64_slot(H, bu) & 15);
-            c.x = __shfl_sync(0xffffffffu, c.x, bv);
-            c.y = __shfl_sync(0xffffffffu, c.y, bv);
+            kb ^= lrank;  // lane-rank bits: 31 - lrank; every key is unique
+            // warp argmax -> the winning lane of this half (warp-uniform)
+            int wl;
+            if (ARGMAX == AM_REDUX) {
+                // one redux on the high words; the low words only break exact ties there
+                const uint32_t hi = (uint32_t)(kb >> 32);
+                const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+                uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
+                if (__popc(cand) > 1) {
+                    const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? (uint32_t)kb : 0u);
+                    cand = __ballot_sync(0xffffffffu, hi == mh && (uint32_t)kb == ml);
+                }
+                wl = __ffs(cand) - 1;
+            } else {
+                const unsigned long long key = p64_warp_max<ARGMAX>(kb, sm.red_hi[pair][H],
+                                                                    sm.red_lo[pair][H]);
+                wl = __ffs(__ballot_sync(0xffffffffu, kb == key)) - 1;
+            }
             PairSlot *ps = &sm.slot[pair][parity][0];
-            if (lane == 0) {
-                ps[H].key = __longlong_as_double((long long)key);
+            if (lane == wl) {
+                // only the winning lane extracts its coefficient R[u*][v] and publishes it
+                const uint32_t rr = 31u - (((uint32_t)kb >> 5) & 31u);
+                const int bu = TREE ? (int)bitrev5(rr) : (int)rr;
+                const double2 c = pick16(R, p64_slot(H, bu) & 15);
+                ps[H].key = __longlong_as_double((long long)kb);
                 ps[H].cre = c.x;
                 ps[H].cim = c.y;
             }
             bar_pair(bar_id);
             // combine the halves: the larger key wins (keys are unique)
-            const unsigned long long ko =
-                (unsigned long long)__double_as_longlong(ps[1 - H].key);
-            unsigned long long wkey = key;
-            if (ko > key) {
-                wkey = ko;
-                c.x = ps[1 - H].cre;
-                c.y = ps[1 - H].cim;
-            }
+            const unsigned long long k0 = (unsigned long long)__double_as_longlong(ps[0].key);
+            const unsigned long long k1 = (unsigned long long)__double_as_longlong(ps[1].key);
+            const double c0r = ps[0].cre, c0i = ps[0].cim, c1r = ps[1].cre, c1i = ps[1].cim;
+            const bool other = k1 > k0;
+            const unsigned long long wkey = other ? k1 : k0;
+            double2 c = make_double2(other ? c1r : c0r, other ? c1i : c0i);
             parity ^= 1;
             const uint32_t wlo = (uint32_t)wkey;
             const uint32_t wrr = 31u - ((wlo >> 5) & 31u), wlr = 31u - (wlo & 31u);
@@ -391,17 +424,30 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
             gi = c.y * ginv;
             P = (uint32_t)((32 - wu) & 31) << 9;
             ycv = wb | ((uint32_t)((lane - wv) & 31) << 4);
-            if (has_pix) {
-                const double2 e = sm.cs[(wu * pm + wv * pn) & 31];
-                acc = fma(gr, e.x, fma(-gi, e.y, acc));
+            // record every other selection per half; both halves flush together every 32
+            if ((it & 1) == H && lane == 0) hist[(it >> 1) & 15] = SelEntry{gr, gi, wu, wv, {0, 0}};
+            if ((it & 31) == 31) {
+                __syncwarp();
+                acc = p64_flush(sm, hist, 16, pm, pn, acc);
+                __syncwarp();
             }
             done = it + 1;
         }
+        {
+            // flush the selections recorded since the last full flush
+            const int rem = done & 31;
+            const int mine = (rem + 1 - H) >> 1;  // entries of this half among the last rem
+            __syncwarp();
+            acc = p64_flush(sm, hist, mine, pm, pn, acc);
+        }
+        if (H == 1 && has_pix) sm.acc_x[pair][lane] = acc;
+        bar_pair(bar_id);
         if (H == 0) {
             if (sel_b)
                 for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
             if (lane == 0 && a.done) a.done[bid] = done;
             if (has_pix) {
+                acc += sm.acc_x[pair][lane];
                 const int m = lane / B, n = lane % B;
                 const int64_t y = r0 + m, xx = c0 + n;
                 if (y < a.H && xx < a.W)
@@ -413,8 +459,11 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
     }
 }
 
+#ifndef FSR_P64_MAXREG
+#define FSR_P64_MAXREG 128
+#endif
 template <int BPC, bool TREE, int ARGMAX, typename IO>
-__global__ void __launch_bounds__(BPC * 64, 8 / BPC) pair64_kernel(Pair64Args<IO> a) {
+__global__ void __maxnreg__(FSR_P64_MAXREG) pair64_kernel(Pair64Args<IO> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Pair64Smem<BPC> &sm = *reinterpret_cast<Pair64Smem<BPC> *>(smem_raw);
     if (threadIdx.x < 32) {
