@@ -434,7 +434,10 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     } else {
         Tables<float> tf;
         if ((rc = get_tables<float>(eng, d, N, p->rho, tf))) return rc;
+        Tables<double> td;
+        if ((rc = get_tables<double>(eng, d, N, p->rho, td))) return rc;
         Warp32Args a{};
+        a.decay64 = td.decay;
         a.px = (const float *)px;
         a.px_pitch = px_pitch;
         a.mask = mask;
@@ -460,7 +463,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.empty_list = d.empty_list.as<int32_t>();
         a.rerun_count = &ctr->rerun_count;
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
-        a.gap_out = d.gap_debug ? d.gap_debug - first : nullptr;
+        a.gap_out = d.gap_debug ? d.gap_debug - 2 * first : nullptr;
+        a.guard_mode = 0;
         if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                 guarded || d.gap_debug != nullptr, st)))
             return rc;
@@ -644,7 +648,7 @@ void fsr_params_init(fsr_params *p) {
     p->argmax_impl = FSR_ARGMAX_SHFL;
     p->rho = 0.7;
     p->gamma = 0.5;
-    p->guard_tau = 1e-4;
+    p->guard_tau = 5e-5;
 }
 
 int fsr_params_validate(const fsr_params *p, char *msg, int msg_len) {
@@ -783,7 +787,7 @@ int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *p
     int rc = select_device(eng, d);
     if (rc) return rc;
     DevBuf g;
-    CUDA_TRY(eng, g.ensure((size_t)nb * sizeof(float)));
+    CUDA_TRY(eng, g.ensure((size_t)nb * 2 * sizeof(float)));
     d.gap_debug = g.as<float>();
     std::vector<std::unique_ptr<Device>> others;
     // single-device run so the gap buffer indexes every block
@@ -792,7 +796,7 @@ int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *p
     while (!others.empty()) { eng->devs.push_back(std::move(others.back())); others.pop_back(); }
     d.gap_debug = nullptr;
     if (rc == FSR_OK)
-        CUDA_TRY(eng, cudaMemcpy(gaps, g.p, (size_t)nb * sizeof(float), cudaMemcpyDeviceToHost));
+        CUDA_TRY(eng, cudaMemcpy(gaps, g.p, (size_t)nb * 2 * sizeof(float), cudaMemcpyDeviceToHost));
     g.release();
     return rc;
 }

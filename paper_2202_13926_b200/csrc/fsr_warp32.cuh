@@ -54,6 +54,7 @@ struct Warp32Args {
     float gamma;
     float tau;             // guard: relative gap threshold
     const float *decay;    // [32*32]
+    const double *decay64; // [32*32] (fp64 prologue)
     const float *wf;       // [32*32]
     int32_t *sel;          // [total blocks, iterations] or null
     int32_t *done;         // [total blocks] or null
@@ -61,7 +62,8 @@ struct Warp32Args {
     int32_t *empty_list;
     unsigned int *rerun_count;
     int32_t *rerun_list;
-    float *gap_out;        // debug: per-block min relative top-2 gap (GUARD only) or null
+    float *gap_out;        // debug: per-block [2] min top-2 gaps (relative, scaled) or null
+    int guard_mode;        // 0: relative gap (b1-b2)/b1; 1: cancellation-scaled (b1-b2)/sqrt(b1*B0)
 };
 
 template <int WARPS>
@@ -170,8 +172,103 @@ __device__ __forceinline__ void pass32(cpx<float> (&R)[32], const float (&wfr)[1
     }
 }
 
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD>
-__global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
+__device__ __forceinline__ int w32_tidx(int r, int c) { return r * 32 + (c ^ r); }
+
+// fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
+// precision, then R (registers) and W (duplicated-row shared layout) rounded
+// to fp32 once.  Halves the initial spectral error of the fp32 loop (whose late
+// iterations compare objectives of a residual 10^2-10^3 below R0), which cuts
+// the guard's fp64 re-runs.  Returns the early-stop energy sum f^2 w.
+__device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float2 *wb, cpx<float> (&R)[32],
+                                                   int64_t wr0, int64_t x, bool xin, int lane) {
+    double2 *t = reinterpret_cast<double2 *>(wb);  // 16 KiB: XOR-swizzled 32x32 double2 tile
+    double energy = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+        const int64_t y = wr0 + k;
+        double f = 0.0, w = 0.0;
+        if (xin && y >= 0 && y < a.H && a.mask[y * a.mask_pitch + x]) {
+            f = (double)a.px[y * a.px_pitch + x];
+            w = a.decay64[k * 32 + lane];
+        }
+        t[w32_tidx(k, lane)] = make_double2(f * w, w);
+        energy = fma(f * f, w, energy);
+    }
+    __syncwarp();
+    // Each 32-point line is done as two 16-point halves (even / odd samples) with
+    // the radix-2 combine written back in place: line position 2m holds
+    // frequency m, position 2m+1 frequency m+16 (permutation s below).  Peak
+    // live data: 16 complex doubles.
+    {
+        cpx<double> xv[16];
+        // rows (lane = window row)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(lane, 2 * j)]; xv[j] = {z.x, z.y}; }
+        fft_pow2<4>(xv);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[w32_tidx(lane, 2 * j)] = make_double2(xv[j].re, xv[j].im);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(lane, 2 * j + 1)]; xv[j] = {z.x, z.y}; }
+        fft_pow2<4>(xv);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const double2 e = t[w32_tidx(lane, 2 * m)];
+            const double c = tw_cos(m), sn = tw_sin(m);
+            const double tr = xv[m].re * c + xv[m].im * sn, ti = xv[m].im * c - xv[m].re * sn;
+            t[w32_tidx(lane, 2 * m)] = make_double2(e.x + tr, e.y + ti);
+            t[w32_tidx(lane, 2 * m + 1)] = make_double2(e.x - tr, e.y - ti);
+        }
+        __syncwarp();
+        // columns (lane = frequency v, stored at line position cv)
+        const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(2 * j, cv)]; xv[j] = {z.x, z.y}; }
+        fft_pow2<4>(xv);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) t[w32_tidx(2 * j, cv)] = make_double2(xv[j].re, xv[j].im);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(2 * j + 1, cv)]; xv[j] = {z.x, z.y}; }
+        fft_pow2<4>(xv);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const double2 e = t[w32_tidx(2 * m, cv)];
+            const double c = tw_cos(m), sn = tw_sin(m);
+            const double tr = xv[m].re * c + xv[m].im * sn, ti = xv[m].im * c - xv[m].re * sn;
+            t[w32_tidx(2 * m, cv)] = make_double2(e.x + tr, e.y + ti);
+            t[w32_tidx(2 * m + 1, cv)] = make_double2(e.x - tr, e.y - ti);
+        }
+        __syncwarp();
+    }
+    // split: Z[u][v] sits at (s(u), s(v)), s(f) = f < 16 ? 2f : 2(f-16)+1.
+    // R and W are rounded to fp32 once, W kept in registers until every read is done.
+    const int mv = (32 - lane) & 31;
+    const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
+    const int cm = mv < 16 ? 2 * mv : 2 * (mv - 16) + 1;
+    float2 Wf[32];
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        const int nu = (32 - u) & 31;
+        const int su = u < 16 ? 2 * u : 2 * (u - 16) + 1;
+        const int sn = nu < 16 ? 2 * nu : 2 * (nu - 16) + 1;
+        const double2 z = t[w32_tidx(su, cv)], zm = t[w32_tidx(sn, cm)];
+        R[u] = {(float)((z.x + zm.x) * 0.5), (float)((z.y - zm.y) * 0.5)};
+        Wf[u] = make_float2((float)((z.y + zm.y) * 0.5), (float)((zm.x - z.x) * 0.5));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+        wb[u * W32_WROW + lane] = Wf[u];
+        wb[(u + 32) * W32_WROW + lane] = Wf[u];
+    }
+    __syncwarp();
+    return energy;
+}
+
+#ifndef FSR_W32_FFT64
+#define FSR_W32_FFT64 1
+#endif
+template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool FFT64 = (FSR_W32_FFT64 != 0)>
+__global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
@@ -204,60 +301,66 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
         const bool xin = x >= 0 && x < a.W;
         cpx<float> R[32];
         float energy = 0.f;
-        // ---- gather: lane = window column; row k coalesced across lanes
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            const int64_t y = wr0 + k;
-            float f = 0.f, w = 0.f;
-            if (xin && y >= 0 && y < a.H) {
-                if (a.mask[y * a.mask_pitch + x]) {
-                    f = a.px[y * a.px_pitch + x];
-                    w = a.decay[k * 32 + lane];
+        if (FFT64) {
+            energy = (float)w32_prologue_f64(a, wb, R, wr0, x, xin, lane);
+        } else {
+            // ---- gather: lane = window column; row k coalesced across lanes
+    #pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int64_t y = wr0 + k;
+                float f = 0.f, w = 0.f;
+                if (xin && y >= 0 && y < a.H) {
+                    if (a.mask[y * a.mask_pitch + x]) {
+                        f = a.px[y * a.px_pitch + x];
+                        w = a.decay[k * 32 + lane];
+                    }
                 }
+                // w scaled by 2^7 (exact) so both halves of the packed transform have
+                // comparable magnitude and W is not swamped by the rounding of F{f w}
+                R[k] = {f * w, w * 128.f};
+                energy = fmaf(f * f, w, energy);
             }
-            R[k] = {f * w, w};
-            energy = fmaf(f * f, w, energy);
+            // ---- 2-D FFT of z: transpose (lane = row k), FFT over l, transpose, FFT over k
+            float2 *tile = wb;  // padded [32][33]
+    #pragma unroll
+            for (int k = 0; k < 32; ++k) tile[k * W32_TILE_STRIDE + lane] = make_float2(R[k].re, R[k].im);
+            __syncwarp();
+    #pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                float2 z = tile[lane * W32_TILE_STRIDE + l];
+                R[l] = {z.x, z.y};
+            }
+            __syncwarp();
+            fft32(R);  // lane k: Y[k][v], register v
+    #pragma unroll
+            for (int q = 0; q < 32; ++q) tile[lane * W32_TILE_STRIDE + q] = make_float2(R[q].re, R[q].im);
+            __syncwarp();
+    #pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                float2 z = tile[k * W32_TILE_STRIDE + lane];
+                R[k] = {z.x, z.y};
+            }
+            __syncwarp();
+            fft32(R);  // lane v: Z[u][v], register u
+            // ---- split Z into R and W via the conjugate mirror Z[-u][-v]:
+            // Z -> upper half of wb (stride 32), W -> lower half, then duplicate rows.
+            float2 *zt = wb + 32 * W32_WROW;
+    #pragma unroll
+            for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = make_float2(R[u].re, R[u].im);
+            __syncwarp();
+            const int mv = (32 - lane) & 31;
+    #pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const float2 zm = zt[((32 - u) & 31) * W32_WROW + mv];
+                const float zr = R[u].re, zi = R[u].im;
+                R[u] = {(zr + zm.x) * 0.5f, (zi - zm.y) * 0.5f};
+                wb[u * W32_WROW + lane] = make_float2((zi + zm.y) * (0.5f / 128.f), (zm.x - zr) * (0.5f / 128.f));
+            }
+            __syncwarp();
+    #pragma unroll
+            for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = wb[u * W32_WROW + lane];
+            __syncwarp();
         }
-        // ---- 2-D FFT of z: transpose (lane = row k), FFT over l, transpose, FFT over k
-        float2 *tile = wb;  // padded [32][33]
-#pragma unroll
-        for (int k = 0; k < 32; ++k) tile[k * W32_TILE_STRIDE + lane] = make_float2(R[k].re, R[k].im);
-        __syncwarp();
-#pragma unroll
-        for (int l = 0; l < 32; ++l) {
-            float2 z = tile[lane * W32_TILE_STRIDE + l];
-            R[l] = {z.x, z.y};
-        }
-        __syncwarp();
-        fft32(R);  // lane k: Y[k][v], register v
-#pragma unroll
-        for (int q = 0; q < 32; ++q) tile[lane * W32_TILE_STRIDE + q] = make_float2(R[q].re, R[q].im);
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-            float2 z = tile[k * W32_TILE_STRIDE + lane];
-            R[k] = {z.x, z.y};
-        }
-        __syncwarp();
-        fft32(R);  // lane v: Z[u][v], register u
-        // ---- split Z into R and W via the conjugate mirror Z[-u][-v]:
-        // Z -> upper half of wb (stride 32), W -> lower half, then duplicate rows.
-        float2 *zt = wb + 32 * W32_WROW;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = make_float2(R[u].re, R[u].im);
-        __syncwarp();
-        const int mv = (32 - lane) & 31;
-#pragma unroll
-        for (int u = 0; u < 32; ++u) {
-            const float2 zm = zt[((32 - u) & 31) * W32_WROW + mv];
-            const float zr = R[u].re, zi = R[u].im;
-            R[u] = {(zr + zm.x) * 0.5f, (zi - zm.y) * 0.5f};
-            wb[u * W32_WROW + lane] = make_float2((zi + zm.y) * 0.5f, (zm.x - zr) * 0.5f);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = wb[u * W32_WROW + lane];
-        __syncwarp();
         const float w00 = wb[0].x;
         int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
@@ -286,7 +389,7 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
         float acc = 0.f;
         bool herm = true;
         bool flagged = false;
-        float min_gap = 1.f;
+        float min_gap = 1.f, min_gap2 = 1.f, B0 = 0.f;
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int done = 0;
@@ -309,8 +412,15 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
                 const uint32_t c2 = (lane == bv) ? m2 : m1;
                 const uint32_t k2 = warp_max_u32(c2);
                 const float b1 = __uint_as_float(key & ~31u), b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b1 > 0.f && b2 >= b1 * (1.f - a.tau);
-                if (b1 > 0.f) min_gap = fminf(min_gap, (b1 - b2) / b1);
+                // The fp32 residual carries an absolute error ~eps*|R0|, so the
+                // objective's relative error grows like sqrt(B0 / b1) as the
+                // residual shrinks; mode 1 scales the gap test accordingly.
+                if (it == 0) B0 = b1;
+                const float g1 = b1 > 0.f ? (b1 - b2) / b1 : 1.f;
+                const float g2 = b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f;
+                flagged |= b1 > 0.f && (a.guard_mode ? g2 : g1) < a.tau;
+                min_gap = fminf(min_gap, g1);
+                min_gap2 = fminf(min_gap2, g2);
                 // a stop decision within tau of the threshold is also ambiguous
                 flagged |= thr > 0.f && fabsf(b1 - thr) <= a.tau * thr;
             }
@@ -335,7 +445,10 @@ __global__ void __launch_bounds__(WARPS * 32) warp32_kernel(Warp32Args a) {
             for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
         if (lane == 0) {
             if (a.done) a.done[bid] = done;
-            if (GUARD && a.gap_out) a.gap_out[bid] = min_gap;
+            if (GUARD && a.gap_out) {
+                a.gap_out[2 * bid] = min_gap;
+                a.gap_out[2 * bid + 1] = min_gap2;
+            }
             if (GUARD && flagged && a.rerun_list) {
                 unsigned slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;

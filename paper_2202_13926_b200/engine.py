@@ -32,7 +32,7 @@ from .spectra import WeightSet
 
 REDUCERS = ("tree", "linear")
 EARLY_STOP_RELATIVE = 1e-12
-DEFAULT_GUARD_TAU = 1e-4
+DEFAULT_GUARD_TAU = 5e-5
 
 
 def _check_reducer(reducer: str) -> bool:

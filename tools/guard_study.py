@@ -36,16 +36,17 @@ def study(name, img, B=4, N=32, I=100, reducer="tree"):
     nb = frames.n_blocks(H, W, B)
     p32 = _lib.make_params(B, (N - B) // 2, I, reducer=reducer, precision="fp32_unguarded")
     out32 = np.empty((H, W), np.float32)
-    gaps = np.empty(nb, np.float32)
+    gaps2 = np.empty((nb, 2), np.float32)
     sel32 = np.empty((nb, I), np.int32)
     px32 = px.astype(np.float32)
     m8 = mask.astype(np.uint8)
     rc = L.fsr_debug_guard_gaps(eng._h, ctypes.byref(p32), _lib._ptr(px32), _lib._ptr(m8), H, W,
-                                _lib._ptr(out32), _lib._ptr(gaps), _lib._ptr(sel32))
+                                _lib._ptr(out32), _lib._ptr(gaps2), _lib._ptr(sel32))
     assert rc == 0, L.fsr_last_error(eng._h)
     p64 = _lib.make_params(B, (N - B) // 2, I, reducer=reducer, precision="fp64")
     sel64 = np.empty((nb, I), np.int32)
     out64 = eng.reconstruct(px, mask, p64, sel64, None)
+    gaps, gapsc = gaps2[:, 0], gaps2[:, 1]
     eq = np.all(sel32 == sel64, axis=1) | np.all(sel32 == mirror(sel64, N), axis=1)
     flipped = ~eq
     # per-block max error
@@ -71,6 +72,14 @@ def study(name, img, B=4, N=32, I=100, reducer="tree"):
                          "max_err_unflagged": float(left.max()) if left.size else 0.0,
                          "flipped_unflagged": int((flipped & ~flag).sum())})
     res["tau"] = tau_rows
+    rows2 = []
+    for tau in (1e-6, 2e-6, 5e-6, 1e-5, 2e-5, 5e-5, 1e-4):
+        flag = gapsc < tau
+        left = eb[~flag]
+        rows2.append({"tau": tau, "rerun_frac": float(flag.mean()),
+                      "max_err_unflagged": float(left.max()) if left.size else 0.0,
+                      "flipped_unflagged": int((flipped & ~flag).sum())})
+    res["tau_scaled"] = rows2
     print(json.dumps(res), flush=True)
     return res
 
@@ -81,6 +90,8 @@ if __name__ == "__main__":
     out.append(study("uni256", synth.frame(256, 256, 1, "uniform")))
     out.append(study("nat1080", synth.frame(1080, 1920, 7)))
     out.append(study("uni1080", synth.frame(1080, 1920, 3, "uniform")))
-    out.append(study("nat1080_linear", synth.frame(1080, 1920, 7), reducer="linear"))
+    out.append(study("nat1080_s11", synth.frame(1080, 1920, 11)))
+    out.append(study("uni1080_s5", synth.frame(1080, 1920, 5, "uniform")))
+    out.append(study("nat4k", synth.frame(2160, 3840, 7)))
     with open(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/guard_study.json", "w") as f:
         json.dump(out, f, indent=1)
