@@ -51,8 +51,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="4k", choices=list(WORKLOADS))
-    ap.add_argument("--precision", default="fp64", choices=["fp32", "fp64", "fp32_unguarded"])
-    ap.add_argument("--argmax", default="shfl", choices=["shfl", "smem", "redux"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64", "fp32_unguarded"])
+    ap.add_argument("--argmax", default="redux", choices=["shfl", "smem", "redux"])
     ap.add_argument("--reducer", default="tree", choices=["tree", "linear"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "warp", "pair"])
     ap.add_argument("--iterations", type=int, default=100)

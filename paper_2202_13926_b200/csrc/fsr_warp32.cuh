@@ -72,6 +72,7 @@ struct Warp32Smem {
     float2 cs[32];                          // cos/sin(2 pi j / 32)
     unsigned int red_key[WARPS][32];        // AM_SMEM scratch
     unsigned int red_rank[WARPS][32];
+    float4 hist[WARPS][32];                 // deferred synthesis: (gr, gi, u, v) per selection
 };
 
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
@@ -108,9 +109,13 @@ __device__ __forceinline__ void cross_lane_best(uint32_t &key, uint32_t &rank,
             rank = take ? orank : rank;
         }
     } else if (ARGMAX == AM_REDUX) {
-        uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
-        uint32_t cand = key == kmax ? rank : 0xffffffffu;
-        rank = __reduce_min_sync(0xffffffffu, cand);
+        const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
+        const uint32_t tied = __ballot_sync(0xffffffffu, key == kmax);
+        if (__popc(tied) == 1) {
+            rank = __shfl_sync(0xffffffffu, rank, __ffs(tied) - 1);
+        } else {  // exact tie on (objective, row rank): lowest lane rank wins
+            rank = __reduce_min_sync(0xffffffffu, key == kmax ? rank : 0xffffffffu);
+        }
         key = kmax;
     } else {  // AM_SMEM: classic shared-memory tree reduction
         skey[lane] = key;
@@ -390,9 +395,11 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
         bool herm = true;
         bool flagged = false;
         float min_gap = 1.f, min_gap2 = 1.f, B0 = 0.f;
+        const float one_minus_tau = 1.f - a.tau;
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int done = 0;
+        float4 *hist = sm.hist[wid];
         for (int it = 0; it < a.iterations; ++it) {
             uint32_t m1, m2;
             const float2 *wrow = wb + (32 - pu) * W32_WROW + ((v - pv) & 31);
@@ -408,24 +415,22 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
             const uint32_t urank = 31u - (key & 31u);
             const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
             const int bv = TREE ? (int)bitrev5(rank) : (int)rank;
+            const float b1 = __uint_as_float(key & ~31u);
             if (GUARD) {
-                const uint32_t c2 = (lane == bv) ? m2 : m1;
-                const uint32_t k2 = warp_max_u32(c2);
-                const float b1 = __uint_as_float(key & ~31u), b2 = __uint_as_float(k2 & ~31u);
-                // The fp32 residual carries an absolute error ~eps*|R0|, so the
-                // objective's relative error grows like sqrt(B0 / b1) as the
-                // residual shrinks; mode 1 scales the gap test accordingly.
-                if (it == 0) B0 = b1;
-                const float g1 = b1 > 0.f ? (b1 - b2) / b1 : 1.f;
-                const float g2 = b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f;
-                flagged |= b1 > 0.f && (a.guard_mode ? g2 : g1) < a.tau;
-                min_gap = fminf(min_gap, g1);
-                min_gap2 = fminf(min_gap2, g2);
+                // second-best objective: the winner lane's runner-up or any other lane's best
+                const uint32_t k2 = warp_max_u32((lane == bv) ? m2 : m1);
+                const float b2 = __uint_as_float(k2 & ~31u);
+                flagged |= b1 > 0.f && b2 >= b1 * one_minus_tau;
                 // a stop decision within tau of the threshold is also ambiguous
                 flagged |= thr > 0.f && fabsf(b1 - thr) <= a.tau * thr;
+                if (a.gap_out) {  // guard-study instrumentation (tools/guard_study.py)
+                    if (it == 0) B0 = b1;
+                    min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
+                    min_gap2 = fminf(min_gap2, b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f);
+                }
             }
             if (sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
-            if (thr > 0.f && __uint_as_float(key & ~31u) < thr) break;
+            if (thr > 0.f && b1 < thr) break;
             float2 c = pick32(R, bu);
             c.x = __shfl_sync(0xffffffffu, c.x, bv);
             c.y = __shfl_sync(0xffffffffu, c.y, bv);
@@ -435,11 +440,29 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
             pv = bv;
             // a non-self-mirror selection breaks the exact Hermitian symmetry
             herm = herm && (((32 - bu) & 31) == bu) && (((32 - bv) & 31) == bv);
-            if (has_pix) {
-                const float2 e = sm.cs[(bu * pm + bv * pn) & 31];
-                acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            // deferred synthesis of the target pixels: record, flush every 32
+            if (lane == 0) hist[it & 31] = make_float4(gr, gi, __int_as_float(bu), __int_as_float(bv));
+            if ((it & 31) == 31) {
+                __syncwarp();
+#pragma unroll 4
+                for (int j = 0; j < 32; ++j) {
+                    const float4 h = hist[j];
+                    const float2 e = sm.cs[(__float_as_int(h.z) * pm + __float_as_int(h.w) * pn) & 31];
+                    acc = fmaf(h.x, e.x, fmaf(-h.y, e.y, acc));
+                }
+                __syncwarp();
             }
             done = it + 1;
+        }
+        {
+            __syncwarp();
+            const int rem = done & 31;
+            for (int j = 0; j < rem; ++j) {
+                const float4 h = hist[j];
+                const float2 e = sm.cs[(__float_as_int(h.z) * pm + __float_as_int(h.w) * pn) & 31];
+                acc = fmaf(h.x, e.x, fmaf(-h.y, e.y, acc));
+            }
+            __syncwarp();
         }
         if (sel_b)
             for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
