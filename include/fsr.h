@@ -61,7 +61,7 @@ typedef struct {
     int32_t early_stop;  /* reconstruction.py:27, 262-266 */
     int32_t precision;   /* fsr_precision */
     int32_t argmax_impl; /* fsr_argmax_impl */
-    int32_t kernel;      /* N=32 fp64 kernel: 0 auto, 1 one warp per block, 2 warp pair */
+    int32_t kernel;      /* N=32 fp64 kernel: 0 auto (= warp pair), 1 one warp per block, 2 warp pair */
     double rho;          /* (0, 1) */
     double gamma;        /* (0, 1] */
     double guard_tau;    /* fp32 near-tie guard: relative top-2 gap that forces an fp64 re-run */

@@ -317,7 +317,7 @@ int launch_fp64_n32(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, const f
                     int64_t want_blocks, cudaStream_t st) {
     const bool tree = p->reducer == FSR_REDUCER_TREE;
     const int am = p->argmax_impl;
-    if (p->kernel == 2) return launch_pair64<IO>(eng, d, a, tree, am, want_blocks, st);
+    if (p->kernel != 1) return launch_pair64<IO>(eng, d, a, tree, am, want_blocks, st);  // auto/pair
 #define FSR_W64(T, A) \
     if (tree == T && am == A) return launch_warp64_t<kWarp64Warps, T, A, IO>(eng, d, a, want_blocks, st);
     FSR_W64(true, AM_SHFL) FSR_W64(false, AM_SHFL) FSR_W64(true, AM_REDUX)
