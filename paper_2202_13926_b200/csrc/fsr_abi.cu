@@ -246,9 +246,9 @@ int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, 
     return FSR_OK;
 }
 
-template <int WARPS, bool TREE, int AM, bool GUARD>
+template <int WARPS, bool TREE, int AM, bool GUARD, bool STUDY = false>
 int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, cudaStream_t st) {
-    auto k = warp32_kernel<WARPS, TREE, AM, GUARD>;
+    auto k = warp32_kernel<WARPS, TREE, AM, GUARD, STUDY>;
     const size_t smem = sizeof(Warp32Smem<WARPS>);
     CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -350,6 +350,11 @@ constexpr int kWarps = 4;
 
 int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, bool tree, int am, bool guard,
                   cudaStream_t st) {
+    if (a.gap_out) {  // guard study (tools/guard_study.py): redux argmax only
+        if (am != AM_REDUX) return fail(eng, FSR_EINVAL, "guard study needs argmax=redux");
+        return tree ? launch_warp32_t<kWarps, true, AM_REDUX, true, true>(eng, d, a, st)
+                    : launch_warp32_t<kWarps, false, AM_REDUX, true, true>(eng, d, a, st);
+    }
 #define FSR_W32(T, A, G) \
     if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, st);
     FSR_W32(true, AM_SHFL, true) FSR_W32(true, AM_SHFL, false)
@@ -455,7 +460,6 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.nblocks = nblocks;
         a.gamma = (float)p->gamma;
         a.tau = (float)p->guard_tau;
-        a.decay = tf.decay;
         a.wf = tf.wf;
         a.sel = sel;
         a.done = done;
@@ -464,7 +468,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.rerun_count = &ctr->rerun_count;
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
         a.gap_out = d.gap_debug ? d.gap_debug - 2 * first : nullptr;
-        a.guard_mode = 0;
+        a.key_mask = 0xffffffe0u;
         if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                 guarded || d.gap_debug != nullptr, st)))
             return rc;

@@ -2,25 +2,36 @@
 // per target block, everything register/shared-memory resident.
 //
 // Per block (reference path reconstruction.py:246-280 + _kernels.py:62-126):
-//   gather     lane l loads window column l (coalesced 128 B rows), mask-gated
-//              rho^d weights, packed z = f*w + i*w           (sampling.py:93-107,
-//                                                              weights.py:18-37)
-//   FFT        32-point in-register FFT along rows, smem transpose, FFT along
-//              columns; split Z into R = F{f w} and W = F{w}, exactly Hermitian
-//   loop       lane v owns spectral column v (R[u][v], u = 0..31, 64 regs);
-//              W lives in shared memory with duplicated rows so the circular
-//              shift W[(u-pu) mod 32][(v-pv) mod 32] is a per-lane base plus an
-//              immediate offset; the residual update of iteration it-1 is fused
-//              with the objective pass of iteration it, so R never leaves
-//              registers and W is read once per bin per iteration.
+//   gather     lane l loads window column l (coalesced 128 B rows), all 32 rows
+//              of pixels and mask issued before any is consumed; mask-gated
+//              rho^d weights, packed z = f*w + i*w        (sampling.py:93-107,
+//                                                           weights.py:18-37)
+//   FFT        fp64: 2-D FFT of z in registers + a 16 KiB XOR-swizzled tile,
+//              split into R = F{f w} and W = F{w} (exactly Hermitian), both
+//              rounded to fp32 once
+//   loop       lane v owns spectral column v.  Its 32 bins are held as 16
+//              packed row pairs (u, u+16): re2[i] = (Re R[i][v], Re R[i+16][v]),
+//              im2[i] likewise, so the residual update and the objective run
+//              on the sm_100 paired-fp32 pipe (FFMA2/FMUL2: two bins per
+//              instruction, same rounding as the scalar ops).  W lives in
+//              shared memory as row-pair float4s
+//                 U[k][c] = (Wx[k+16][c], Wx[k][c], Wy[k+16][c], Wy[k][c])
+//              (indices mod 32), so the circular shift W[(u-pu)][(v-pv)] for
+//              the lane's pair i is ONE LDS.128 at row 16 + i - (pu mod 16)
+//              (never wraps) and column (v - pv) mod 32; pu >= 16 reads the
+//              same float4 with its halves swapped (a free FFMA2 operand
+//              swizzle, selected by a warp-uniform branch).  The update of
+//              iteration it-1 is fused with the objective pass of iteration
+//              it, so R never leaves registers and W is read once per bin.
 //   argmax     per-lane running max over packed keys (objective bits with the
-//              5 low mantissa bits replaced by the row's tie rank), then a
-//              cross-lane step: __shfl_xor_sync butterfly on (key, lane rank)
-//              (the paper's register argmax), or redux.sync, or a shared-memory
-//              tree (the paper's comparison point) -- template ARGMAX.
+//              5 low mantissa bits replaced by the row's tie rank; VIMNMX3
+//              folds two bins per op), then a cross-lane step: __shfl_xor_sync
+//              butterfly on (key, lane rank) (the paper's register argmax), or
+//              redux.sync + ballot, or a shared-memory tree (the paper's
+//              comparison point) -- template ARGMAX.
 //   synthesis  lanes p < B*B accumulate g(m,n) += Re(gp e^{2 pi i(u m + v n)/32})
-//              directly (no inverse FFT, only the B x B target pixels), then
-//              merge (known pixels copied) and stitch.
+//              every iteration (no inverse FFT, only the B x B target pixels),
+//              then merge (known pixels copied) and stitch.
 //   guard      fp32 near-tie guard: per-lane top-2 keys give the best and the
 //              second-best objective of every iteration (excluding the exact
 //              conjugate mirror while the state is exactly Hermitian); a block
@@ -36,11 +47,6 @@ namespace fsr {
 
 enum ArgmaxImpl { AM_SHFL = 0, AM_SMEM = 1, AM_REDUX = 2 };
 
-constexpr int W32_N = 32;
-constexpr int W32_WROW = 32;                         // complex per W row
-constexpr int W32_WBYTES = 2 * 32 * W32_WROW * 8;    // duplicated rows: 16 KiB
-constexpr int W32_TILE_STRIDE = 33;                  // padded transpose tile row
-
 struct Warp32Args {
     const float *px;
     int64_t px_pitch;
@@ -53,8 +59,7 @@ struct Warp32Args {
     int64_t bcols, first, nblocks;
     float gamma;
     float tau;             // guard: relative gap threshold
-    const float *decay;    // [32*32]
-    const double *decay64; // [32*32] (fp64 prologue)
+    const double *decay64; // [32*32]
     const float *wf;       // [32*32]
     int32_t *sel;          // [total blocks, iterations] or null
     int32_t *done;         // [total blocks] or null
@@ -63,69 +68,71 @@ struct Warp32Args {
     unsigned int *rerun_count;
     int32_t *rerun_list;
     float *gap_out;        // debug: per-block [2] min top-2 gaps (relative, scaled) or null
-    int guard_mode;        // 0: relative gap (b1-b2)/b1; 1: cancellation-scaled (b1-b2)/sqrt(b1*B0)
+    uint32_t key_mask;     // 0xffffffe0 (see pass_x2)
 };
 
 template <int WARPS>
 struct Warp32Smem {
-    float2 wbuf[WARPS][2 * 32 * W32_WROW];  // duplicated-row W, also the transpose tile
-    float2 cs[32];                          // cos/sin(2 pi j / 32)
-    unsigned int red_key[WARPS][32];        // AM_SMEM scratch
+    float4 ubuf[WARPS][32 * 32];         // U row-pair table (16 KiB), also the fp64 FFT tile
+    float2 cs[32];                       // cos/sin(2 pi j / 32)
+    unsigned int red_key[WARPS][32];     // AM_SMEM scratch
     unsigned int red_rank[WARPS][32];
-    float4 hist[WARPS][32];                 // deferred synthesis: (gr, gi, u, v) per selection
 };
 
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ uint32_t umax3(uint32_t a, uint32_t b, uint32_t c) { return max(max(a, b), c); }
 
-// Extract R[u] for a warp-uniform dynamic u (jump table, no divergence).
-__device__ __forceinline__ float2 pick32(const cpx<float> (&R)[32], int u) {
-    float2 c;
-    switch (u) {
+// (Re, Im) of R[u][lane] for a warp-uniform dynamic u (uniform branches only).
+__device__ __forceinline__ float2 pick_pair(const float2 (&re)[16], const float2 (&im)[16], int u) {
+    float4 q;
+    switch (u & 15) {
 #define FSR_PICK(i) \
-    case i: c = make_float2(R[i].re, R[i].im); break;
+    case i: q = make_float4(re[i].x, re[i].y, im[i].x, im[i].y); break;
         FSR_PICK(0) FSR_PICK(1) FSR_PICK(2) FSR_PICK(3) FSR_PICK(4) FSR_PICK(5) FSR_PICK(6)
         FSR_PICK(7) FSR_PICK(8) FSR_PICK(9) FSR_PICK(10) FSR_PICK(11) FSR_PICK(12)
-        FSR_PICK(13) FSR_PICK(14) FSR_PICK(15) FSR_PICK(16) FSR_PICK(17) FSR_PICK(18)
-        FSR_PICK(19) FSR_PICK(20) FSR_PICK(21) FSR_PICK(22) FSR_PICK(23) FSR_PICK(24)
-        FSR_PICK(25) FSR_PICK(26) FSR_PICK(27) FSR_PICK(28) FSR_PICK(29) FSR_PICK(30)
-        default: c = make_float2(R[31].re, R[31].im); break;
+        FSR_PICK(13) FSR_PICK(14)
+        default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); break;
 #undef FSR_PICK
     }
-    return c;
+    return u < 16 ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
 }
 
-// Cross-lane argmax on (key desc, rank asc); every lane gets the winner.
-template <int ARGMAX>
-__device__ __forceinline__ void cross_lane_best(uint32_t &key, uint32_t &rank,
+// Cross-lane argmax on (key desc, lane rank asc).  Returns the winning key and
+// the winning lane (= spectral column) on every lane.
+template <int ARGMAX, bool TREE>
+__device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int &wl,
                                                 unsigned int *skey, unsigned int *srank) {
     const int lane = lane_id();
+    const uint32_t lrank = TREE ? bitrev5(lane) : (uint32_t)lane;
     if (ARGMAX == AM_SHFL) {
+        uint32_t key = m1, rank = lrank;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
-            uint32_t ok = __shfl_xor_sync(0xffffffffu, key, off);
-            uint32_t orank = __shfl_xor_sync(0xffffffffu, rank, off);
-            bool take = ok > key || (ok == key && orank < rank);
+            const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, off);
+            const uint32_t orank = __shfl_xor_sync(0xffffffffu, rank, off);
+            const bool take = ok > key || (ok == key && orank < rank);
             key = take ? ok : key;
             rank = take ? orank : rank;
         }
+        kmax = key;
+        wl = TREE ? (int)bitrev5(rank) : (int)rank;
     } else if (ARGMAX == AM_REDUX) {
-        const uint32_t kmax = __reduce_max_sync(0xffffffffu, key);
-        const uint32_t tied = __ballot_sync(0xffffffffu, key == kmax);
-        if (__popc(tied) == 1) {
-            rank = __shfl_sync(0xffffffffu, rank, __ffs(tied) - 1);
-        } else {  // exact tie on (objective, row rank): lowest lane rank wins
-            rank = __reduce_min_sync(0xffffffffu, key == kmax ? rank : 0xffffffffu);
+        kmax = __reduce_max_sync(0xffffffffu, m1);
+        const uint32_t tied = __ballot_sync(0xffffffffu, m1 == kmax);
+        if (!TREE || __popc(tied) == 1) {
+            wl = __ffs(tied) - 1;  // linear: the lowest lane is the lowest rank
+        } else {                   // tree, exact tie across lanes: lowest bitrev5(lane)
+            wl = (int)bitrev5(__reduce_min_sync(0xffffffffu, m1 == kmax ? lrank : 0xffffffffu));
         }
-        key = kmax;
     } else {  // AM_SMEM: classic shared-memory tree reduction
-        skey[lane] = key;
-        srank[lane] = rank;
+        skey[lane] = m1;
+        srank[lane] = lrank;
         __syncwarp();
 #pragma unroll
         for (int s = 16; s >= 1; s >>= 1) {
             if (lane < s) {
-                uint32_t ok = skey[lane + s], orank = srank[lane + s];
-                uint32_t mk = skey[lane], mr = srank[lane];
+                const uint32_t ok = skey[lane + s], orank = srank[lane + s];
+                const uint32_t mk = skey[lane], mr = srank[lane];
                 if (ok > mk || (ok == mk && orank < mr)) {
                     skey[lane] = ok;
                     srank[lane] = orank;
@@ -133,68 +140,105 @@ __device__ __forceinline__ void cross_lane_best(uint32_t &key, uint32_t &rank,
             }
             __syncwarp();
         }
-        key = skey[0];
-        rank = srank[0];
+        kmax = skey[0];
+        const uint32_t rank = srank[0];
+        wl = TREE ? (int)bitrev5(rank) : (int)rank;
         __syncwarp();
     }
 }
 
-__device__ __forceinline__ uint32_t warp_max_u32(uint32_t x) {
-    return __reduce_max_sync(0xffffffffu, x);
-}
-
-// One objective/update pass over the 32 rows a lane owns.
-// HERM: the state is exactly Hermitian, keys of non-canonical bins are zeroed.
-template <bool TREE, bool GUARD, bool HERM, bool UPDATE>
-__device__ __forceinline__ void pass32(cpx<float> (&R)[32], const float (&wfr)[17],
-                                       const float2 *wrow, float gr, float gi,
-                                       uint32_t canon, uint32_t &m1, uint32_t &m2) {
+// One objective/update pass over the lane's 16 row pairs (32 bins).
+//   UPDATE: apply R -= gp * W(. - pu, . - pv) first (fused residual update)
+//   SWAP:   pu >= 16, the U float4 halves are exchanged
+//   HERM:   the state is exactly Hermitian; keys of non-canonical bins are zeroed
+//   hmask:  ~31, passed in from a kernel argument so that ptxas keeps it in a
+//           register: with both constants immediate it splits the key
+//           formation (o & ~31) | c into two LOP3s
+template <bool TREE, bool GUARD, bool HERM, bool UPDATE, bool SWAP>
+__device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
+                                        const float4 *up, float gr, float gi, uint32_t canon,
+                                        uint32_t hmask, uint32_t &m1, uint32_t &m2) {
     m1 = 0;
     m2 = 0;
+    const float2 ngr = make_float2(-gr, -gr), pgi = make_float2(gi, gi), ngi = make_float2(-gi, -gi);
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-        float re = R[u].re, im = R[u].im;
+    for (int i = 0; i < 16; ++i) {
+        float2 r = re[i], m = im[i];
         if (UPDATE) {
-            const float2 w = wrow[u * W32_WROW];  // W[(u - pu) mod 32][(v - pv) mod 32]
-            re = fmaf(-gr, w.x, re);
-            re = fmaf(gi, w.y, re);
-            im = fmaf(-gr, w.y, im);
-            im = fmaf(-gi, w.x, im);
-            R[u].re = re;
-            R[u].im = im;
+            const float4 w = up[i * 32];  // U[16 + i - pu%16][(v - pv) mod 32]
+            const float2 wx = SWAP ? make_float2(w.y, w.x) : make_float2(w.x, w.y);
+            const float2 wy = SWAP ? make_float2(w.w, w.z) : make_float2(w.z, w.w);
+            // same operation order as the scalar form re = fma(-gr, wx, re); re = fma(gi, wy, re);
+            // im = fma(-gr, wy, im); im = fma(-gi, wx, im)
+            r = __ffma2_rn(wx, ngr, r);
+            r = __ffma2_rn(wy, pgi, r);
+            m = __ffma2_rn(wy, ngr, m);
+            m = __ffma2_rn(wx, ngi, m);
+            re[i] = r;
+            im[i] = m;
         }
-        const float mag = fmaf(re, re, im * im);
-        const float o = mag * wfr[u <= 16 ? u : 32 - u];
-        const uint32_t rk = TREE ? ((u & 1) << 4 | (u & 2) << 2 | (u & 4) | (u & 8) >> 2 | (u & 16) >> 4)
-                                     : (uint32_t)u;
-        uint32_t key = (f2u(o) | 31u) ^ rk;  // low 5 bits = 31 - rank(u)
-        if (HERM && GUARD) key = ((canon >> u) & 1u) ? key : 0u;
+        const float2 mag = __ffma2_rn(r, r, __fmul2_rn(m, m));  // fma(re, re, im*im)
+        const float2 o = __fmul2_rn(mag, wf2[i]);
+        const uint32_t rka = TREE ? ((i & 1) << 4 | (i & 2) << 2 | (i & 4) | (i & 8) >> 2) : (uint32_t)i;
+        const uint32_t rkb = TREE ? (rka | 1u) : (uint32_t)(i + 16);
+        // low 5 bits = 31 - rank(u)
+        uint32_t ka = (f2u(o.x) & hmask) | (31u ^ rka);
+        uint32_t kb = (f2u(o.y) & hmask) | (31u ^ rkb);
+        if (HERM && GUARD) {
+            ka = ((canon >> i) & 1u) ? ka : 0u;
+            kb = ((canon >> (i + 16)) & 1u) ? kb : 0u;
+        }
         if (GUARD) {
-            uint32_t t = min(m1, key);
-            m2 = max(m2, t);
+            const uint32_t hi = max(ka, kb), lo = min(ka, kb);
+            m2 = umax3(m2, lo, min(m1, hi));
+            m1 = max(m1, hi);
+        } else {
+            m1 = umax3(m1, ka, kb);
         }
-        m1 = max(m1, key);
     }
+}
+
+template <bool TREE, bool GUARD, bool HERM>
+__device__ __forceinline__ void pass_update(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
+                                            const float4 *up, bool swap, float gr, float gi,
+                                            uint32_t canon, uint32_t hmask, uint32_t &m1, uint32_t &m2) {
+    if (swap)
+        pass_x2<TREE, GUARD, HERM, true, true>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
+    else
+        pass_x2<TREE, GUARD, HERM, true, false>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
 }
 
 __device__ __forceinline__ int w32_tidx(int r, int c) { return r * 32 + (c ^ r); }
 
 // fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
-// precision, then R (registers) and W (duplicated-row shared layout) rounded
-// to fp32 once.  Halves the initial spectral error of the fp32 loop (whose late
-// iterations compare objectives of a residual 10^2-10^3 below R0), which cuts
-// the guard's fp64 re-runs.  Returns the early-stop energy sum f^2 w.
-__device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float2 *wb, cpx<float> (&R)[32],
-                                                   int64_t wr0, int64_t x, bool xin, int lane) {
-    double2 *t = reinterpret_cast<double2 *>(wb);  // 16 KiB: XOR-swizzled 32x32 double2 tile
+// precision, then R (registers, packed row pairs) and W (U table in shared
+// memory) rounded to fp32 once.  Returns the early-stop energy sum f^2 w.
+__device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *ub, float2 (&re)[16],
+                                                   float2 (&im)[16], int64_t wr0, int64_t x,
+                                                   bool xin, int lane) {
+    double2 *t = reinterpret_cast<double2 *>(ub);  // 16 KiB: XOR-swizzled 32x32 double2 tile
+    // ---- gather: every row's pixel and mask load is issued before any is used
+    float pf[32];
+    uint32_t pm[32];
+    {
+        const int64_t xc = xin ? x : 0;
+        const float *pp = a.px + wr0 * a.px_pitch + xc;
+        const uint8_t *mp = a.mask + wr0 * a.mask_pitch + xc;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int64_t y = wr0 + k;
+            const bool in = xin && y >= 0 && y < a.H;
+            pf[k] = in ? __ldg(pp + k * a.px_pitch) : 0.f;
+            pm[k] = in ? (uint32_t)__ldg(mp + k * a.mask_pitch) : 0u;
+        }
+    }
     double energy = 0.0;
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < 32; ++k) {
-        const int64_t y = wr0 + k;
         double f = 0.0, w = 0.0;
-        if (xin && y >= 0 && y < a.H && a.mask[y * a.mask_pitch + x]) {
-            f = (double)a.px[y * a.px_pitch + x];
-            w = a.decay64[k * 32 + lane];
+        if (pm[k]) {
+            f = (double)pf[k];
+            w = __ldg(a.decay64 + k * 32 + lane);
         }
         t[w32_tidx(k, lane)] = make_double2(f * w, w);
         energy = fma(f * f, w, energy);
@@ -256,23 +300,29 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float2 *
         const int su = u < 16 ? 2 * u : 2 * (u - 16) + 1;
         const int sn = nu < 16 ? 2 * nu : 2 * (nu - 16) + 1;
         const double2 z = t[w32_tidx(su, cv)], zm = t[w32_tidx(sn, cm)];
-        R[u] = {(float)((z.x + zm.x) * 0.5), (float)((z.y - zm.y) * 0.5)};
+        const float rr = (float)((z.x + zm.x) * 0.5), ri = (float)((z.y - zm.y) * 0.5);
+        if (u < 16) {
+            re[u].x = rr;
+            im[u].x = ri;
+        } else {
+            re[u - 16].y = rr;
+            im[u - 16].y = ri;
+        }
         Wf[u] = make_float2((float)((z.y + zm.y) * 0.5), (float)((zm.x - z.x) * 0.5));
     }
     __syncwarp();
+    // U[k][v] = (Wx[k+16], Wx[k], Wy[k+16], Wy[k]) (row indices mod 32)
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-        wb[u * W32_WROW + lane] = Wf[u];
-        wb[(u + 32) * W32_WROW + lane] = Wf[u];
+    for (int k = 0; k < 16; ++k) {
+        ub[k * 32 + lane] = make_float4(Wf[k + 16].x, Wf[k].x, Wf[k + 16].y, Wf[k].y);
+        ub[(k + 16) * 32 + lane] = make_float4(Wf[k].x, Wf[k + 16].x, Wf[k].y, Wf[k + 16].y);
     }
     __syncwarp();
     return energy;
 }
 
-#ifndef FSR_W32_FFT64
-#define FSR_W32_FFT64 1
-#endif
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool FFT64 = (FSR_W32_FFT64 != 0)>
+// STUDY: record per-block minimum top-2 gaps (tools/guard_study.py only).
+template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY>
 __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Args a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
@@ -282,9 +332,8 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
         sm.cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
     }
     __syncthreads();
-    float2 *wb = sm.wbuf[wid];
+    float4 *ub = sm.ubuf[wid];
     const int v = lane;
-    const uint32_t lrank = TREE ? bitrev5(lane) : lane;
     // canonical half of each mirror pair (lower tie rank), bit u of this lane's column
     uint32_t canon = 0;
 #pragma unroll
@@ -292,81 +341,23 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
         int t = u * 32 + v, mt = ((32 - u) & 31) * 32 + ((32 - v) & 31);
         canon |= (uint32_t)(tie_rank(t, TREE) <= tie_rank(mt, TREE)) << u;
     }
-    // folded frequency prior of this column: wf[u][v] == wf[32-u][v] (weights.py:40-56)
-    float wfr[17];
-#pragma unroll
-    for (int u = 0; u <= 16; ++u) wfr[u] = a.wf[u * 32 + v];
+    const float one_minus_tau = 1.f - a.tau;
 
     const int64_t total_warps = (int64_t)gridDim.x * WARPS;
-    for (int64_t i = (int64_t)blockIdx.x * WARPS + wid; i < a.nblocks; i += total_warps) {
-        const int64_t bid = a.first + i;
+    for (int64_t bi = (int64_t)blockIdx.x * WARPS + wid; bi < a.nblocks; bi += total_warps) {
+        const int64_t bid = a.first + bi;
         const int64_t brow = bid / a.bcols, bcol = bid - brow * a.bcols;
         const int64_t r0 = brow * a.B, c0 = bcol * a.B;
         const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
         const bool xin = x >= 0 && x < a.W;
-        cpx<float> R[32];
-        float energy = 0.f;
-        if (FFT64) {
-            energy = (float)w32_prologue_f64(a, wb, R, wr0, x, xin, lane);
-        } else {
-            // ---- gather: lane = window column; row k coalesced across lanes
-    #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int64_t y = wr0 + k;
-                float f = 0.f, w = 0.f;
-                if (xin && y >= 0 && y < a.H) {
-                    if (a.mask[y * a.mask_pitch + x]) {
-                        f = a.px[y * a.px_pitch + x];
-                        w = a.decay[k * 32 + lane];
-                    }
-                }
-                // w scaled by 2^7 (exact) so both halves of the packed transform have
-                // comparable magnitude and W is not swamped by the rounding of F{f w}
-                R[k] = {f * w, w * 128.f};
-                energy = fmaf(f * f, w, energy);
-            }
-            // ---- 2-D FFT of z: transpose (lane = row k), FFT over l, transpose, FFT over k
-            float2 *tile = wb;  // padded [32][33]
-    #pragma unroll
-            for (int k = 0; k < 32; ++k) tile[k * W32_TILE_STRIDE + lane] = make_float2(R[k].re, R[k].im);
-            __syncwarp();
-    #pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                float2 z = tile[lane * W32_TILE_STRIDE + l];
-                R[l] = {z.x, z.y};
-            }
-            __syncwarp();
-            fft32(R);  // lane k: Y[k][v], register v
-    #pragma unroll
-            for (int q = 0; q < 32; ++q) tile[lane * W32_TILE_STRIDE + q] = make_float2(R[q].re, R[q].im);
-            __syncwarp();
-    #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                float2 z = tile[k * W32_TILE_STRIDE + lane];
-                R[k] = {z.x, z.y};
-            }
-            __syncwarp();
-            fft32(R);  // lane v: Z[u][v], register u
-            // ---- split Z into R and W via the conjugate mirror Z[-u][-v]:
-            // Z -> upper half of wb (stride 32), W -> lower half, then duplicate rows.
-            float2 *zt = wb + 32 * W32_WROW;
-    #pragma unroll
-            for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = make_float2(R[u].re, R[u].im);
-            __syncwarp();
-            const int mv = (32 - lane) & 31;
-    #pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                const float2 zm = zt[((32 - u) & 31) * W32_WROW + mv];
-                const float zr = R[u].re, zi = R[u].im;
-                R[u] = {(zr + zm.x) * 0.5f, (zi - zm.y) * 0.5f};
-                wb[u * W32_WROW + lane] = make_float2((zi + zm.y) * (0.5f / 128.f), (zm.x - zr) * (0.5f / 128.f));
-            }
-            __syncwarp();
-    #pragma unroll
-            for (int u = 0; u < 32; ++u) zt[u * W32_WROW + lane] = wb[u * W32_WROW + lane];
-            __syncwarp();
-        }
-        const float w00 = wb[0].x;
+        float2 re[16], im[16];
+        const float energy = (float)w32_prologue_f64(a, ub, re, im, wr0, x, xin, lane);
+        const float w00 = ub[16 * 32].x;  // U[16][0].x = Wx[0][0] = sum of the weights
+        // frequency prior of this column for the row pairs (i, i+16) (weights.py:40-56);
+        // re-read per block (L1-resident) so it is not live across the prologue
+        float2 wf2[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) wf2[i] = make_float2(__ldg(a.wf + i * 32 + v), __ldg(a.wf + (i + 16) * 32 + v));
         int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
             if (lane == 0) {
@@ -382,93 +373,77 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
         // early stop threshold: 1e-12 * sum f^2 w (reconstruction.py:262-266)
         float thr = 0.f;
         if (a.early_stop) {
+            float e = energy;
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
-            thr = 1e-12f * energy;
+            for (int off = 16; off >= 1; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+            thr = 1e-12f * e;
         }
         const float ginv = a.gamma / w00;
-        // target pixel of this lane (p < B*B): window coordinates (L + m, L + n)
-        const int B = a.B;
-        const int pm = a.L + lane / B, pn = a.L + lane % B;
-        const bool has_pix = lane < B * B;
+        // target pixel of this lane (p < B*B) at window coordinates (L + m, L + n):
+        // g(m,n) = sum over selections of Re(gp e^{2 pi i (u m + v n) / 32}),
+        // accumulated directly (no inverse FFT, reconstruction.py:270 restated)
+        const int pm = a.L + lane / a.B, pn = a.L + lane % a.B;
         float acc = 0.f;
         bool herm = true;
         bool flagged = false;
         float min_gap = 1.f, min_gap2 = 1.f, B0 = 0.f;
-        const float one_minus_tau = 1.f - a.tau;
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
-        int done = 0;
-        float4 *hist = sm.hist[wid];
-        for (int it = 0; it < a.iterations; ++it) {
+        int it = 0;
+        for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            const float2 *wrow = wb + (32 - pu) * W32_WROW + ((v - pv) & 31);
+            const float4 *up = ub + (16 - (pu & 15)) * 32 + ((v - pv) & 31);
+            const bool swap = pu >= 16;
             if (it == 0) {
-                pass32<TREE, GUARD, true, false>(R, wfr, wrow, gr, gi, canon, m1, m2);
+                pass_x2<TREE, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
             } else if (herm) {
-                pass32<TREE, GUARD, true, true>(R, wfr, wrow, gr, gi, canon, m1, m2);
+                pass_update<TREE, GUARD, true>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             } else {
-                pass32<TREE, GUARD, false, true>(R, wfr, wrow, gr, gi, canon, m1, m2);
+                pass_update<TREE, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
-            uint32_t key = m1, rank = lrank;
-            cross_lane_best<ARGMAX>(key, rank, sm.red_key[wid], sm.red_rank[wid]);
-            const uint32_t urank = 31u - (key & 31u);
+            uint32_t kmax;
+            int bv;
+            cross_lane_best<ARGMAX, TREE>(m1, kmax, bv, sm.red_key[wid], sm.red_rank[wid]);
+            const uint32_t urank = 31u - (kmax & 31u);
             const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
-            const int bv = TREE ? (int)bitrev5(rank) : (int)rank;
-            const float b1 = __uint_as_float(key & ~31u);
-            if (GUARD) {
-                // second-best objective: the winner lane's runner-up or any other lane's best
-                const uint32_t k2 = warp_max_u32((lane == bv) ? m2 : m1);
-                const float b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b1 > 0.f && b2 >= b1 * one_minus_tau;
-                // a stop decision within tau of the threshold is also ambiguous
-                flagged |= thr > 0.f && fabsf(b1 - thr) <= a.tau * thr;
-                if (a.gap_out) {  // guard-study instrumentation (tools/guard_study.py)
-                    if (it == 0) B0 = b1;
-                    min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
-                    min_gap2 = fminf(min_gap2, b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f);
-                }
-            }
+            const float b1 = __uint_as_float(kmax & ~31u);
             if (sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
-            if (thr > 0.f && b1 < thr) break;
-            float2 c = pick32(R, bu);
+            if (b1 < thr) {  // thr == 0 unless early stop is on
+                if (GUARD && b1 >= thr * one_minus_tau) flagged = true;  // a stop decision within tau
+                break;
+            }
+            float2 c = pick_pair(re, im, bu);
             c.x = __shfl_sync(0xffffffffu, c.x, bv);
             c.y = __shfl_sync(0xffffffffu, c.y, bv);
             gr = c.x * ginv;
             gi = c.y * ginv;
             pu = bu;
             pv = bv;
-            // a non-self-mirror selection breaks the exact Hermitian symmetry
-            herm = herm && (((32 - bu) & 31) == bu) && (((32 - bv) & 31) == bv);
-            // deferred synthesis of the target pixels: record, flush every 32
-            if (lane == 0) hist[it & 31] = make_float4(gr, gi, __int_as_float(bu), __int_as_float(bv));
-            if ((it & 31) == 31) {
-                __syncwarp();
-#pragma unroll 4
-                for (int j = 0; j < 32; ++j) {
-                    const float4 h = hist[j];
-                    const float2 e = sm.cs[(__float_as_int(h.z) * pm + __float_as_int(h.w) * pn) & 31];
-                    acc = fmaf(h.x, e.x, fmaf(-h.y, e.y, acc));
+            if (GUARD) {
+                // second-best objective: the winner lane's runner-up or any other lane's best
+                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == bv) ? m2 : m1);
+                const float b2 = __uint_as_float(k2 & ~31u);
+                flagged |= b2 >= b1 * one_minus_tau;
+                // a continue decision within tau of the stop threshold is ambiguous too
+                flagged |= b1 * one_minus_tau < thr;
+                if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)
+                    if (it == 0) B0 = b1;
+                    min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
+                    min_gap2 = fminf(min_gap2, b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f);
                 }
-                __syncwarp();
             }
-            done = it + 1;
+            // a non-self-mirror selection breaks the exact Hermitian symmetry
+            if (herm) herm = ((bu & 15) == 0) && ((bv & 15) == 0);
+            // synthesis of the target pixels, Re(gp e^{+2 pi i (bu m + bv n)/32})
+            const float2 e = sm.cs[(bu * pm + bv * pn) & 31];
+            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
         }
-        {
-            __syncwarp();
-            const int rem = done & 31;
-            for (int j = 0; j < rem; ++j) {
-                const float4 h = hist[j];
-                const float2 e = sm.cs[(__float_as_int(h.z) * pm + __float_as_int(h.w) * pn) & 31];
-                acc = fmaf(h.x, e.x, fmaf(-h.y, e.y, acc));
-            }
-            __syncwarp();
-        }
+        const int done = it;
         if (sel_b)
-            for (int it = done + lane; it < a.iterations; it += 32) sel_b[it] = -1;
+            for (int j = done + lane; j < a.iterations; j += 32) sel_b[j] = -1;
         if (lane == 0) {
             if (a.done) a.done[bid] = done;
-            if (GUARD && a.gap_out) {
+            if (STUDY) {
                 a.gap_out[2 * bid] = min_gap;
                 a.gap_out[2 * bid + 1] = min_gap2;
             }
@@ -478,8 +453,8 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
             }
         }
         // merge + stitch
-        if (has_pix) {
-            const int m = lane / B, n = lane % B;
+        if (lane < a.B * a.B) {
+            const int m = lane / a.B, n = lane % a.B;
             const int64_t y = r0 + m, xx = c0 + n;
             if (y < a.H && xx < a.W)
                 a.out[y * a.out_pitch + xx] =
