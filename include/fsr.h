@@ -145,10 +145,14 @@ typedef struct {
     int64_t rerun_blocks;    /* blocks re-run in fp64 by the near-tie guard */
     int64_t empty_blocks;    /* blocks with no known sample in the window */
     int32_t kernel_launches; /* kernels launched by the call (all devices) */
-    int32_t reserved;
+    int32_t flags;           /* FSR_STATS_* bits of the first device's launch */
     double kernel_ms;        /* device time of the last call's kernels (first device) */
     double main_ms;          /* device time of the dominant kernel (first device) */
 } fsr_stats;
+/* fsr_stats.flags: the N=32 fp32 kernel gathered its windows with TMA (2-D
+ * tensor maps, zero fill outside the image).  Set FSR_NO_TMA=1 in the
+ * environment before fsr_engine_create to force the plain-load gather. */
+#define FSR_STATS_TMA_GATHER 1
 int fsr_last_stats(const fsr_engine *eng, fsr_stats *out);
 
 #ifdef __cplusplus

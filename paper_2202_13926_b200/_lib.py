@@ -46,7 +46,7 @@ class FsrStatsC(ctypes.Structure):
         ("rerun_blocks", ctypes.c_int64),
         ("empty_blocks", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
         ("kernel_ms", ctypes.c_double),
         ("main_ms", ctypes.c_double),
     ]

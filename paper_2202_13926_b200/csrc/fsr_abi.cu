@@ -10,11 +10,13 @@
 //   precision FP32, other N   -> image_generic_kernel<float>  (+ fp64 re-run)
 // No CPU fallback: without a CUDA device every entry point returns FSR_ECUDA.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -80,6 +82,8 @@ struct Device {
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
+    bool tma_enabled = true;     // warp32 window gather by TMA when the rows allow it
+    int used_tma = 0;            // last warp32 launch gathered by TMA
 };
 
 }  // namespace
@@ -247,7 +251,8 @@ int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, 
 }
 
 template <int WARPS, bool TREE, int AM, bool GUARD, bool STUDY = false>
-int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, cudaStream_t st) {
+int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
+                    cudaStream_t st) {
     auto k = warp32_kernel<WARPS, TREE, AM, GUARD, STUDY>;
     const size_t smem = sizeof(Warp32Smem<WARPS>);
     CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -257,7 +262,7 @@ int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, cudaStream_
     int64_t want = (a.nblocks + WARPS - 1) / WARPS;
     int grid = (int)std::min<int64_t>(want, (int64_t)d.sms * per_sm);
     if (grid < 1) grid = 1;
-    k<<<grid, WARPS * 32, smem, st>>>(a);
+    k<<<grid, WARPS * 32, smem, st>>>(a, maps);
     d.launches++;
     CUDA_TRY(eng, cudaGetLastError());
     return FSR_OK;
@@ -348,15 +353,54 @@ bool pair64_eligible(const fsr_params *p) {
 
 constexpr int kWarps = 4;
 
-int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, bool tree, int am, bool guard,
-                  cudaStream_t st) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// Tensor maps for the warp32 window gather: 32-row boxes widened to 16-byte
+// aligned starts (W32_BOX_PX / W32_BOX_MK columns), zero fill outside the image.  Returns false when TMA cannot address the buffers (rows not
+// 16-byte aligned); the kernel then gathers with plain loads.
+bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t mask_pitch,
+                 int64_t H, int64_t W, Warp32Maps *m) {
+    if ((reinterpret_cast<uintptr_t>(px) & 15) || ((px_pitch * 4) & 15) ||
+        (reinterpret_cast<uintptr_t>(mask) & 15) || (mask_pitch & 15) || H < 1 || W < 1 ||
+        H > (int64_t)INT32_MAX || W > (int64_t)INT32_MAX)
+        return false;
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
+    const cuuint32_t bpx[2] = {W32_BOX_PX, 32}, bmk[2] = {W32_BOX_MK, 32}, estr[2] = {1, 1};
+    const cuuint64_t spx[1] = {(cuuint64_t)px_pitch * 4}, smk[1] = {(cuuint64_t)mask_pitch};
+    if (enc(&m->px, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(px), dims, spx, bpx, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (enc(&m->mask, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(mask), dims, smk, bmk, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    return true;
+}
+
+int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps, bool tree,
+                  int am, bool guard, cudaStream_t st) {
     if (a.gap_out) {  // guard study (tools/guard_study.py): redux argmax only
         if (am != AM_REDUX) return fail(eng, FSR_EINVAL, "guard study needs argmax=redux");
-        return tree ? launch_warp32_t<kWarps, true, AM_REDUX, true, true>(eng, d, a, st)
-                    : launch_warp32_t<kWarps, false, AM_REDUX, true, true>(eng, d, a, st);
+        return tree ? launch_warp32_t<kWarps, true, AM_REDUX, true, true>(eng, d, a, maps, st)
+                    : launch_warp32_t<kWarps, false, AM_REDUX, true, true>(eng, d, a, maps, st);
     }
 #define FSR_W32(T, A, G) \
-    if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, st);
+    if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, maps, st);
     FSR_W32(true, AM_SHFL, true) FSR_W32(true, AM_SHFL, false)
     FSR_W32(false, AM_SHFL, true) FSR_W32(false, AM_SHFL, false)
     FSR_W32(true, AM_REDUX, true) FSR_W32(true, AM_REDUX, false)
@@ -469,7 +513,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
         a.gap_out = d.gap_debug ? d.gap_debug - 2 * first : nullptr;
         a.key_mask = 0xffffffe0u;
-        if ((rc = launch_warp32(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+        Warp32Maps maps;
+        std::memset(&maps, 0, sizeof(maps));
+        a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps)) ? 1 : 0;
+        d.used_tma = a.use_tma;
+        if ((rc = launch_warp32(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                 guarded || d.gap_debug != nullptr, st)))
             return rc;
         CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
@@ -595,6 +643,7 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         eng->stats.rerun_blocks += ctrs[g].rerun_count;
         eng->stats.kernel_launches += d.launches;
         if (g == 0) {
+            eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
             float ms = 0.f, mm = 0.f;
             if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
             if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
@@ -699,6 +748,8 @@ int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **ou
             return fail(nullptr, FSR_ECUDA, "device %d is sm_%d%d; libfsr is built for sm_100a",
                         id, prop.major, prop.minor);
         d->sms = prop.multiProcessorCount;
+        const char *no_tma = std::getenv("FSR_NO_TMA");  // A/B switch for the TMA window gather
+        d->tma_enabled = !(no_tma && *no_tma && *no_tma != '0');
         CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));
@@ -771,6 +822,7 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
     eng->stats = fsr_stats{};
     eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
     eng->stats.kernel_launches = d.launches;
+    eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
     eng->device_stats_pending = rc == FSR_OK;
     return rc;
 }

@@ -40,6 +40,8 @@
 //              reference within tolerance.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include "fsr_common.cuh"
 #include "fsr_fft.cuh"
 
@@ -69,14 +71,71 @@ struct Warp32Args {
     int32_t *rerun_list;
     float *gap_out;        // debug: per-block [2] min top-2 gaps (relative, scaled) or null
     uint32_t key_mask;     // 0xffffffe0 (see pass_x2)
+    int use_tma;           // gather the window with TMA (needs 16 B aligned rows)
 };
+
+// 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
+// the image: the TMA out-of-bounds rule is exactly the reference's "outside
+// the image = unknown" window rule (sampling.py:93-107).  A TMA box must start
+// on a 16-byte boundary in the innermost dimension, so the boxes are widened
+// (pixels 36 = 32 + 4 columns from x0 rounded down to a multiple of 4, mask
+// 48 = 32 + 16 from a multiple of 16) and each lane reads at its offset.
+constexpr int W32_BOX_PX = 36, W32_BOX_MK = 48;
+constexpr int W32_STAGE_MK = 32 * W32_BOX_PX * 4;                    // mask staging offset (bytes)
+constexpr int W32_STAGE_BYTES = W32_STAGE_MK + 32 * W32_BOX_MK;      // 6144
+struct alignas(64) Warp32Maps {
+    CUtensorMap px;
+    CUtensorMap mask;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+// Whole warp: one elect.sync'd lane arms `bar` with the staging bytes and
+// issues the two 2-D TMA box loads that complete on it.  (Issued from the
+// converged warp: UTMALDG is a uniform-datapath instruction.)
+__device__ __forceinline__ void tma_window(const Warp32Maps &maps, uint32_t bar, uint32_t dst_px,
+                                           uint32_t dst_mask, int x_px, int x_mk, int y0) {
+    asm volatile(
+        "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+        "@p fence.proxy.async.shared::cta;\n"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%2], [%3, {%4, %5}], [%0];\n"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%6], [%7, {%8, %5}], [%0];\n}"
+        ::"r"(bar), "r"(W32_STAGE_BYTES), "r"(dst_px), "l"(reinterpret_cast<uint64_t>(&maps.px)),
+        "r"(x_px), "r"(y0), "r"(dst_mask), "l"(reinterpret_cast<uint64_t>(&maps.mask)), "r"(x_mk)
+        : "memory");
+}
+
+// fp64 FFT tile: 32 x 32 double2 with a one-element row pad (stride 33, 528 B),
+// which makes row-wise (lane = column) and column-wise (lane = row) 16-byte
+// accesses both conflict-free (4 wavefronts per warp access) with purely
+// compile-time offsets from a per-lane base.
+constexpr int W32_TS = 33;
 
 template <int WARPS>
 struct Warp32Smem {
-    float4 ubuf[WARPS][32 * 32];         // U row-pair table (16 KiB), also the fp64 FFT tile
+    float4 ubuf[WARPS][W32_TS * 32];     // U row-pair table (16 KiB), also the fp64 FFT tile (16.5 KiB)
     float2 cs[32];                       // cos/sin(2 pi j / 32)
     unsigned int red_key[WARPS][32];     // AM_SMEM scratch
     unsigned int red_rank[WARPS][32];
+    unsigned long long bar[WARPS];       // TMA window barrier, one per warp
 };
 
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
@@ -208,30 +267,52 @@ __device__ __forceinline__ void pass_update(float2 (&re)[16], float2 (&im)[16], 
         pass_x2<TREE, GUARD, HERM, true, false>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
 }
 
-__device__ __forceinline__ int w32_tidx(int r, int c) { return r * 32 + (c ^ r); }
-
 // fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
 // precision, then R (registers, packed row pairs) and W (U table in shared
 // memory) rounded to fp32 once.  Returns the early-stop energy sum f^2 w.
-__device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *ub, float2 (&re)[16],
-                                                   float2 (&im)[16], int64_t wr0, int64_t x,
-                                                   bool xin, int lane) {
-    double2 *t = reinterpret_cast<double2 *>(ub);  // 16 KiB: XOR-swizzled 32x32 double2 tile
-    // ---- gather: every row's pixel and mask load is issued before any is used
+__device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Warp32Maps &maps,
+                                                   float4 *ub, uint32_t bar, uint32_t &phase,
+                                                   float2 (&re)[16], float2 (&im)[16], int64_t wr0,
+                                                   int64_t x, bool xin, int lane) {
+    double2 *t = reinterpret_cast<double2 *>(ub);  // 32 x 33 double2 (16.5 KiB)
+    // ---- gather: every row's pixel and mask load is issued before any is used.
+    // Window rows k in [k0, k1) lie inside the image; outside rows and columns
+    // are unknown (sampling.py:93-107).
     float pf[32];
     uint32_t pm[32];
-    {
+    if (a.use_tma) {
+        // the 32 x 32 window of pixels (4 KiB) and mask (1 KiB) lands in the
+        // tile region by TMA; lane l then reads window column l
+        const int x0 = (int)(x - lane);
+        const int xp = x0 & ~3, xm = x0 & ~15;  // floor to 16-byte boundaries
+        const float *spx = reinterpret_cast<const float *>(ub);
+        const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + W32_STAGE_MK;
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0);
+        mbar_wait(bar, phase);
+        phase ^= 1u;
+        const float *cpx = spx + (x0 - xp) + lane;
+        const uint8_t *cmk = smk + (x0 - xm) + lane;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            pf[k] = cpx[k * W32_BOX_PX];
+            pm[k] = cmk[k * W32_BOX_MK];
+        }
+        __syncwarp();
+    } else {
         const int64_t xc = xin ? x : 0;
         const float *pp = a.px + wr0 * a.px_pitch + xc;
         const uint8_t *mp = a.mask + wr0 * a.mask_pitch + xc;
+        const int k0 = wr0 < 0 ? (int)-wr0 : 0;
+        const int k1 = a.H - wr0 < 32 ? (int)(a.H - wr0) : 32;
+        const int ppitch = (int)a.px_pitch, mpitch = (int)a.mask_pitch;
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-            const int64_t y = wr0 + k;
-            const bool in = xin && y >= 0 && y < a.H;
-            pf[k] = in ? __ldg(pp + k * a.px_pitch) : 0.f;
-            pm[k] = in ? (uint32_t)__ldg(mp + k * a.mask_pitch) : 0u;
+            const bool in = xin && k >= k0 && k < k1;
+            pf[k] = in ? __ldg(pp + k * ppitch) : 0.f;
+            pm[k] = in ? (uint32_t)__ldg(mp + k * mpitch) : 0u;
         }
     }
+    double2 *tl = t + lane;  // column `lane` of the tile
     double energy = 0.0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -240,7 +321,7 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *
             f = (double)pf[k];
             w = __ldg(a.decay64 + k * 32 + lane);
         }
-        t[w32_tidx(k, lane)] = make_double2(f * w, w);
+        tl[k * W32_TS] = make_double2(f * w, w);
         energy = fma(f * f, w, energy);
     }
     __syncwarp();
@@ -248,58 +329,60 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *
     // the radix-2 combine written back in place: line position 2m holds
     // frequency m, position 2m+1 frequency m+16 (permutation s below).  Peak
     // live data: 16 complex doubles.
+    const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
     {
         cpx<double> xv[16];
         // rows (lane = window row)
+        double2 *tr_ = t + lane * W32_TS;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(lane, 2 * j)]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tr_[2 * j]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) t[w32_tidx(lane, 2 * j)] = make_double2(xv[j].re, xv[j].im);
+        for (int j = 0; j < 16; ++j) tr_[2 * j] = make_double2(xv[j].re, xv[j].im);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(lane, 2 * j + 1)]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tr_[2 * j + 1]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
-            const double2 e = t[w32_tidx(lane, 2 * m)];
+            const double2 e = tr_[2 * m];
             const double c = tw_cos(m), sn = tw_sin(m);
             const double tr = xv[m].re * c + xv[m].im * sn, ti = xv[m].im * c - xv[m].re * sn;
-            t[w32_tidx(lane, 2 * m)] = make_double2(e.x + tr, e.y + ti);
-            t[w32_tidx(lane, 2 * m + 1)] = make_double2(e.x - tr, e.y - ti);
+            tr_[2 * m] = make_double2(e.x + tr, e.y + ti);
+            tr_[2 * m + 1] = make_double2(e.x - tr, e.y - ti);
         }
         __syncwarp();
         // columns (lane = frequency v, stored at line position cv)
-        const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
+        double2 *tc = t + cv;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(2 * j, cv)]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tc[2 * j * W32_TS]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) t[w32_tidx(2 * j, cv)] = make_double2(xv[j].re, xv[j].im);
+        for (int j = 0; j < 16; ++j) tc[2 * j * W32_TS] = make_double2(xv[j].re, xv[j].im);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = t[w32_tidx(2 * j + 1, cv)]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tc[(2 * j + 1) * W32_TS]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
-            const double2 e = t[w32_tidx(2 * m, cv)];
+            const double2 e = tc[2 * m * W32_TS];
             const double c = tw_cos(m), sn = tw_sin(m);
             const double tr = xv[m].re * c + xv[m].im * sn, ti = xv[m].im * c - xv[m].re * sn;
-            t[w32_tidx(2 * m, cv)] = make_double2(e.x + tr, e.y + ti);
-            t[w32_tidx(2 * m + 1, cv)] = make_double2(e.x - tr, e.y - ti);
+            tc[2 * m * W32_TS] = make_double2(e.x + tr, e.y + ti);
+            tc[(2 * m + 1) * W32_TS] = make_double2(e.x - tr, e.y - ti);
         }
         __syncwarp();
     }
     // split: Z[u][v] sits at (s(u), s(v)), s(f) = f < 16 ? 2f : 2(f-16)+1.
     // R and W are rounded to fp32 once, W kept in registers until every read is done.
     const int mv = (32 - lane) & 31;
-    const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
     const int cm = mv < 16 ? 2 * mv : 2 * (mv - 16) + 1;
+    const double2 *tv = t + cv, *tm = t + cm;
     float2 Wf[32];
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
         const int nu = (32 - u) & 31;
         const int su = u < 16 ? 2 * u : 2 * (u - 16) + 1;
         const int sn = nu < 16 ? 2 * nu : 2 * (nu - 16) + 1;
-        const double2 z = t[w32_tidx(su, cv)], zm = t[w32_tidx(sn, cm)];
+        const double2 z = tv[su * W32_TS], zm = tm[sn * W32_TS];
         const float rr = (float)((z.x + zm.x) * 0.5), ri = (float)((z.y - zm.y) * 0.5);
         if (u < 16) {
             re[u].x = rr;
@@ -312,10 +395,11 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *
     }
     __syncwarp();
     // U[k][v] = (Wx[k+16], Wx[k], Wy[k+16], Wy[k]) (row indices mod 32)
+    float4 *ul = ub + lane;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        ub[k * 32 + lane] = make_float4(Wf[k + 16].x, Wf[k].x, Wf[k + 16].y, Wf[k].y);
-        ub[(k + 16) * 32 + lane] = make_float4(Wf[k].x, Wf[k + 16].x, Wf[k].y, Wf[k + 16].y);
+        ul[k * 32] = make_float4(Wf[k + 16].x, Wf[k].x, Wf[k + 16].y, Wf[k].y);
+        ul[(k + 16) * 32] = make_float4(Wf[k].x, Wf[k + 16].x, Wf[k].y, Wf[k + 16].y);
     }
     __syncwarp();
     return energy;
@@ -323,15 +407,20 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, float4 *
 
 // STUDY: record per-block minimum top-2 gaps (tools/guard_study.py only).
 template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY>
-__global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Args a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
+    warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
     if (threadIdx.x < 32) {
         const double th = 6.283185307179586476925286766559 * threadIdx.x / 32.0;
         sm.cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
     }
+    const uint32_t bar = smem_u32(&sm.bar[wid]);
+    if (lane == 0) mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
+    uint32_t phase = 0;
     float4 *ub = sm.ubuf[wid];
     const int v = lane;
     // canonical half of each mirror pair (lower tie rank), bit u of this lane's column
@@ -351,7 +440,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS) warp32_kernel(Warp32Ar
         const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
         const bool xin = x >= 0 && x < a.W;
         float2 re[16], im[16];
-        const float energy = (float)w32_prologue_f64(a, ub, re, im, wr0, x, xin, lane);
+        const float energy = (float)w32_prologue_f64(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane);
         const float w00 = ub[16 * 32].x;  // U[16][0].x = Wx[0][0] = sum of the weights
         // frequency prior of this column for the row pairs (i, i+16) (weights.py:40-56);
         // re-read per block (L1-resident) so it is not live across the prologue

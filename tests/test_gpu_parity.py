@@ -234,3 +234,30 @@ def test_device_api_matches_host_api():
     torch.cuda.synchronize()
     host = fsr.reconstruct(d["sampled"].astype(np.float32), d["mask"], 4, 32, 100)
     assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
+
+
+@pytest.mark.parametrize("shape", [(96, 128), (1080 // 8, 1920 // 8)])
+def test_tma_gather_matches_plain_loads(monkeypatch, shape):
+    """The N=32 fp32 kernel gathers each 32x32 window with 2-D TMA (zero fill
+    outside the image = the reference's outside-is-unknown rule,
+    sampling.py:93-107).  It must give bitwise the same image as the
+    plain-load gather, on frames whose windows cross all four edges."""
+    from paper_2202_13926_b200 import _lib
+    H, W = shape
+    img = oracle.synthetic_frame(H, W, 11)
+    sampled, mask = oracle.quarter_sample(img, 5)
+    px, m8 = sampled.astype(np.float32), mask.astype(np.uint8)
+    outs = {}
+    for no_tma in ("0", "1"):
+        monkeypatch.setenv("FSR_NO_TMA", no_tma)
+        eng = _lib.Engine([0])
+        for precision in ("fp32", "fp32_unguarded"):
+            p = _lib.make_params(4, 14, 100, precision=precision, argmax="redux")
+            out = np.zeros_like(px)
+            eng.reconstruct_rows(px, m8, p, 0, (H + 3) // 4, out)
+            outs[no_tma, precision] = (out, eng.last_stats()["flags"])
+        eng.close()
+    for precision in ("fp32", "fp32_unguarded"):
+        assert outs["0", precision][1] & 1, "TMA gather not used"
+        assert not outs["1", precision][1] & 1
+        assert np.array_equal(outs["0", precision][0], outs["1", precision][0]), precision

@@ -87,13 +87,36 @@ KERNEL_BEGIN(k_imnmx, unsigned)
 unsigned m = 12345u + threadIdx.x;
 KERNEL_LOOP x[j] = max(x[j] + 0, m + j) ;
 KERNEL_END
-// FFMA2 + LOP3 interleaved (fma pipe + alu pipe)
+// FFMA2 + VIMNMX interleaved (fma pipe + alu pipe); both results live
+#define KERNEL_END_K                                                            \
+    } }                                                                         \
+    float s = 0;                                                                \
+    _Pragma("unroll") for (int j = 0; j < 8; ++j) s += sum(x[j]) + (float)k[j]; \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;                             \
+    if (blockIdx.x == 0 && threadIdx.x == 0) { g_clk[1] = clock64(); g_ns[1] = gtimer(); } \
+    }
 KERNEL_BEGIN(k_mix, float2)
 unsigned k[8];
 _Pragma("unroll") for (int j = 0; j < 8; ++j) k[j] = threadIdx.x + j;
 float2 y = make_float2(b * 0.5f + threadIdx.x, b), z = make_float2(a, a * 0.5f);
-unsigned m = 0xffffffe0u + (threadIdx.x >> 10);
-KERNEL_LOOP x[j] = __ffma2_rn(x[j], y, z); k[j] = (k[j] & m) | (unsigned)(j + 1 + i);
+unsigned m = 12345u + threadIdx.x;
+KERNEL_LOOP x[j] = __ffma2_rn(x[j], y, z); k[j] = max(k[j], m + j);
+KERNEL_END_K
+// FFMA + VIMNMX interleaved
+KERNEL_BEGIN(k_mix1, float)
+unsigned k[8];
+_Pragma("unroll") for (int j = 0; j < 8; ++j) k[j] = threadIdx.x + j;
+float y = b * 0.5f + threadIdx.x, z = a;
+unsigned m = 12345u + threadIdx.x;
+KERNEL_LOOP x[j] = fmaf(x[j], y, z); k[j] = max(k[j], m + j);
+KERNEL_END_K
+// VIMNMX two chains per element (alu only, 16 per iteration)
+KERNEL_BEGIN(k_alu2, float)
+unsigned k[8], q[8];
+_Pragma("unroll") for (int j = 0; j < 8; ++j) { k[j] = threadIdx.x + j; q[j] = threadIdx.x * 3 + j; }
+unsigned m = 12345u + threadIdx.x;
+KERNEL_LOOP k[j] = max(k[j], m + j); q[j] = min(q[j], m - j);
+_Pragma("unroll") for (int j = 0; j < 8; ++j) x[j] = (float)(k[j] ^ q[j]);
 KERNEL_END
 
 int main() {
@@ -117,7 +140,9 @@ int main() {
               {"FADD", k_fadd, 8},
               {"LOP3", k_lop3, 8},
               {"IMNMX", k_imnmx, 8},
-              {"FFMA2+LOP3 (count both)", k_mix, 16}};
+              {"FFMA2+VIMNMX (count both)", k_mix, 16},
+              {"FFMA+VIMNMX (count both)", k_mix1, 16},
+              {"VIMNMX+VIMNMX (count both)", k_alu2, 16}};
     for (int w = 0; w < 200; ++w) k_ffma_rr<<<grid, block>>>(out, 1.0f, 0.999f);  // clock ramp
     cudaDeviceSynchronize();
     for (int rep = 0; rep < 2; ++rep)
