@@ -131,7 +131,8 @@ constexpr int W32_TS = 33;
 
 template <int WARPS>
 struct Warp32Smem {
-    float4 ubuf[WARPS][W32_TS * 32];     // U row-pair table (16 KiB), also the fp64 FFT tile (16.5 KiB)
+    float4 ubuf[WARPS][W32_TS * 32];     // U row-pair table (16 KiB, columns by ucol), also the
+                                         // fp64 FFT tile (16.5 KiB) and the TMA staging area
     float2 cs[32];                       // cos/sin(2 pi j / 32)
     unsigned int red_key[WARPS][32];     // AM_SMEM scratch
     unsigned int red_rank[WARPS][32];
@@ -139,6 +140,16 @@ struct Warp32Smem {
 };
 
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+
+// Physical column of U-table column c.  With the tree reducer lane l owns
+// column bitrev5(l), so the 8 lanes of one LDS.128 phase read columns
+// 4a + b (a = 0..7, b fixed); storing column c at (c & 3) * 8 + (c >> 2) puts
+// them in 8 different 16-byte bank groups (conflict-free).  Linear lanes read
+// consecutive columns and keep the identity layout.
+template <bool TREE>
+__device__ __forceinline__ int ucol(int c) {
+    return TREE ? (((c & 3) << 3) | (c >> 2)) : c;
+}
 __device__ __forceinline__ uint32_t umax3(uint32_t a, uint32_t b, uint32_t c) { return max(max(a, b), c); }
 
 // (Re, Im) of R[u][lane] for a warp-uniform dynamic u (uniform branches only).
@@ -156,15 +167,16 @@ __device__ __forceinline__ float2 pick_pair(const float2 (&re)[16], const float2
     return u < 16 ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
 }
 
-// Cross-lane argmax on (key desc, lane rank asc).  Returns the winning key and
-// the winning lane (= spectral column) on every lane.
-template <int ARGMAX, bool TREE>
+// Cross-lane argmax on (key desc, lane asc).  Lanes hold spectral columns in
+// tie-rank order (lane l owns column bitrev5(l) for the tree reducer, l for
+// linear), so the reference's tie rule across columns is "lowest lane".
+// Returns the winning key and the winning lane on every lane.
+template <int ARGMAX>
 __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int &wl,
                                                 unsigned int *skey, unsigned int *srank) {
     const int lane = lane_id();
-    const uint32_t lrank = TREE ? bitrev5(lane) : (uint32_t)lane;
     if (ARGMAX == AM_SHFL) {
-        uint32_t key = m1, rank = lrank;
+        uint32_t key = m1, rank = (uint32_t)lane;
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) {
             const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, off);
@@ -174,18 +186,13 @@ __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int
             rank = take ? orank : rank;
         }
         kmax = key;
-        wl = TREE ? (int)bitrev5(rank) : (int)rank;
+        wl = (int)rank;
     } else if (ARGMAX == AM_REDUX) {
         kmax = __reduce_max_sync(0xffffffffu, m1);
-        const uint32_t tied = __ballot_sync(0xffffffffu, m1 == kmax);
-        if (!TREE || __popc(tied) == 1) {
-            wl = __ffs(tied) - 1;  // linear: the lowest lane is the lowest rank
-        } else {                   // tree, exact tie across lanes: lowest bitrev5(lane)
-            wl = (int)bitrev5(__reduce_min_sync(0xffffffffu, m1 == kmax ? lrank : 0xffffffffu));
-        }
+        wl = __ffs(__ballot_sync(0xffffffffu, m1 == kmax)) - 1;
     } else {  // AM_SMEM: classic shared-memory tree reduction
         skey[lane] = m1;
-        srank[lane] = lrank;
+        srank[lane] = (uint32_t)lane;
         __syncwarp();
 #pragma unroll
         for (int s = 16; s >= 1; s >>= 1) {
@@ -200,8 +207,7 @@ __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int
             __syncwarp();
         }
         kmax = skey[0];
-        const uint32_t rank = srank[0];
-        wl = TREE ? (int)bitrev5(rank) : (int)rank;
+        wl = (int)srank[0];
         __syncwarp();
     }
 }
@@ -270,10 +276,11 @@ __device__ __forceinline__ void pass_update(float2 (&re)[16], float2 (&im)[16], 
 // fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
 // precision, then R (registers, packed row pairs) and W (U table in shared
 // memory) rounded to fp32 once.  Returns the early-stop energy sum f^2 w.
+template <bool TREE>
 __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Warp32Maps &maps,
                                                    float4 *ub, uint32_t bar, uint32_t &phase,
                                                    float2 (&re)[16], float2 (&im)[16], int64_t wr0,
-                                                   int64_t x, bool xin, int lane) {
+                                                   int64_t x, bool xin, int lane, int v) {
     double2 *t = reinterpret_cast<double2 *>(ub);  // 32 x 33 double2 (16.5 KiB)
     // ---- gather: every row's pixel and mask load is issued before any is used.
     // Window rows k in [k0, k1) lie inside the image; outside rows and columns
@@ -371,11 +378,13 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
         }
         __syncwarp();
     }
-    // split: Z[u][v] sits at (s(u), s(v)), s(f) = f < 16 ? 2f : 2(f-16)+1.
+    // split: Z[u][v] sits at (s(u), s(v)), s(f) = f < 16 ? 2f : 2(f-16)+1.  This
+    // lane keeps spectral column v (its tie-rank order column, see the kernel).
     // R and W are rounded to fp32 once, W kept in registers until every read is done.
-    const int mv = (32 - lane) & 31;
+    const int sv = v < 16 ? 2 * v : 2 * (v - 16) + 1;
+    const int mv = (32 - v) & 31;
     const int cm = mv < 16 ? 2 * mv : 2 * (mv - 16) + 1;
-    const double2 *tv = t + cv, *tm = t + cm;
+    const double2 *tv = t + sv, *tm = t + cm;
     float2 Wf[32];
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
@@ -395,7 +404,7 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
     }
     __syncwarp();
     // U[k][v] = (Wx[k+16], Wx[k], Wy[k+16], Wy[k]) (row indices mod 32)
-    float4 *ul = ub + lane;
+    float4 *ul = ub + ucol<TREE>(v);
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         ul[k * 32] = make_float4(Wf[k + 16].x, Wf[k].x, Wf[k + 16].y, Wf[k].y);
@@ -422,7 +431,10 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
     __syncthreads();
     uint32_t phase = 0;
     float4 *ub = sm.ubuf[wid];
-    const int v = lane;
+    // spectral column of this lane, in tie-rank order: the tree reducer's rank
+    // of column v is bitrev5(v) (_kernels.py:12-49), so lane l owns column
+    // bitrev5(l) and "lowest lane" is the reference's column tie-break
+    const int v = TREE ? (int)bitrev5(lane) : lane;
     // canonical half of each mirror pair (lower tie rank), bit u of this lane's column
     uint32_t canon = 0;
 #pragma unroll
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
         const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
         const bool xin = x >= 0 && x < a.W;
         float2 re[16], im[16];
-        const float energy = (float)w32_prologue_f64(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane);
+        const float energy = (float)w32_prologue_f64<TREE>(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane, v);
         const float w00 = ub[16 * 32].x;  // U[16][0].x = Wx[0][0] = sum of the weights
         // frequency prior of this column for the row pairs (i, i+16) (weights.py:40-56);
         // re-read per block (L1-resident) so it is not live across the prologue
@@ -481,7 +493,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
         int it = 0;
         for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            const float4 *up = ub + (16 - (pu & 15)) * 32 + ((v - pv) & 31);
+            const float4 *up = ub + (16 - (pu & 15)) * 32 + ucol<TREE>((v - pv) & 31);
             const bool swap = pu >= 16;
             if (it == 0) {
                 pass_x2<TREE, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
@@ -491,8 +503,9 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
                 pass_update<TREE, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
             uint32_t kmax;
-            int bv;
-            cross_lane_best<ARGMAX, TREE>(m1, kmax, bv, sm.red_key[wid], sm.red_rank[wid]);
+            int wl;
+            cross_lane_best<ARGMAX>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
+            const int bv = TREE ? (int)bitrev5((uint32_t)wl) : wl;
             const uint32_t urank = 31u - (kmax & 31u);
             const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
             const float b1 = __uint_as_float(kmax & ~31u);
@@ -502,15 +515,15 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
                 break;
             }
             float2 c = pick_pair(re, im, bu);
-            c.x = __shfl_sync(0xffffffffu, c.x, bv);
-            c.y = __shfl_sync(0xffffffffu, c.y, bv);
+            c.x = __shfl_sync(0xffffffffu, c.x, wl);
+            c.y = __shfl_sync(0xffffffffu, c.y, wl);
             gr = c.x * ginv;
             gi = c.y * ginv;
             pu = bu;
             pv = bv;
             if (GUARD) {
                 // second-best objective: the winner lane's runner-up or any other lane's best
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == bv) ? m2 : m1);
+                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 flagged |= b2 >= b1 * one_minus_tau;
                 // a continue decision within tau of the stop threshold is ambiguous too
