@@ -73,6 +73,21 @@ def make_frame(H, W, kind):
     return np.where(mask, img, 0.0), mask, img
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (tools/ncu_summary.py), for the workload it was taken on."""
+    path = os.path.join(ROOT, "profiles", "r01", "warp32_ncu.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except OSError:
+        return None
+    for ln in d.get("launches", []):
+        if ln["kernel"].startswith(kernel_prefix):
+            return ln["dram_bytes_per_launch"]
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -300,6 +315,13 @@ def main():
     smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
                 + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
+    traffic, traffic_src = None, None
+    if (kernel == "warp32_kernel" and args.workload == "4k" and world == 1
+            and args.precision == "fp32" and args.reducer == "tree" and args.argmax == "redux"):
+        traffic = ncu_traffic("void warp32_kernel<4, 1, 2, 1, 0>")
+        if traffic is not None:
+            traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
+                           "(profiles/r01/warp32_ncu.json); algorithmic I/O bytes " + str(io_bytes))
     line = {
         "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -312,7 +334,8 @@ def main():
                    "io": "f32 pixels + u8 mask in, f32 out",
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,
-                     "unit": "TFLOP/s", "frac": achieved / peak_fl, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak_fl, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": kernel, "main_ms": mean_main,
                      "work": "blocks x N^2 (12 I + 30 log2 N) flop (SURVEY 8d)",
                      "peak_source": f"derived: 148 SM x {lanes} lanes x 2 flop x sm_max_mhz "
