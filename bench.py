@@ -5,7 +5,14 @@ Default workload (BASELINE.json configs[2], the north-star target): one
 (B=4, N=32, I=100, rho=0.7, gamma=0.5), strip-partitioned over the ranks
 (block rows split into contiguous strips, halo L=(N-B)/2 rows read on both
 sides; no collective on the data path -> "scaling": "strong").
-``--workload 1080p`` gives configs[1].
+``--workload 1080p`` gives configs[1]; ``--workload stream64`` configs[3]:
+64 synthetic 1080p frames (image seed i, mask seed 42+i) dealt round-robin
+over the ranks ("scaling": "strong", total work fixed), value = frames/s of
+the whole stream, e2e = the same stream through the pipelined FrameStream
+(H2D / kernels / D2H overlapped on three CUDA streams, pinned host frames).
+With N > 1 on the frame workloads the strips are also assembled on every rank
+once after the timed region (one NCCL all_gather, shard.gather_strips) and
+its time reported as "gather_ms".
 
 One JSON line on rank 0:
   value   fps with inputs resident in HBM, device time (CUDA events on the
@@ -37,7 +44,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FSR fps & Mpixel/s at 1080p/4K at 1/2/4/8 B200; PSNR delta vs CPU reference"
-WORKLOADS = {"4k": (2160, 3840), "1080p": (1080, 1920)}
+WORKLOADS = {"4k": (2160, 3840), "1080p": (1080, 1920), "stream64": (1080, 1920)}
+STREAM_FRAMES = 64  # BASELINE configs[3]: 64 synthetic 1080p frames, round-robin over the ranks
 
 
 def flops_per_block(N: int, I: int) -> float:
@@ -202,10 +210,115 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_stream(args):
+    """BASELINE configs[3]: 64 synthetic 1080p frames dealt round-robin over the ranks."""
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2202_13926_b200 import _lib, frames, shard, synth
+    from paper_2202_13926_b200.stream import FrameStream
+
+    H, W = WORKLOADS["stream64"]
+    B, N, I = args.block, args.support, args.iterations
+    L = (N - B) // 2
+    mine = shard.frame_shard(STREAM_FRAMES, rank, world)
+    dev = torch.device("cuda", local)
+    host, d_px, d_mk = [], [], []
+    for i in mine:
+        img = synth.frame(H, W, i, args.image)
+        m = frames.quarter_sample_mask(H, W, 42 + i)
+        px = torch.from_numpy(np.where(m, img, 0.0).astype(np.float32)).pin_memory()
+        mk = torch.from_numpy(m.astype(np.uint8)).pin_memory()
+        host.append((px, mk))
+        d_px.append(px.to(dev))
+        d_mk.append(mk.to(dev))
+    d_out = torch.empty((H, W), dtype=torch.float32, device=dev)
+    eng = _lib.Engine([local])
+    params = _lib.make_params(B, L, I, 0.7, 0.5, args.reducer, False, args.precision, args.argmax,
+                              kernel=args.kernel)
+    stream = torch.cuda.current_stream()
+    brows = -(-H // B)
+
+    def step():
+        for j in range(len(mine)):
+            eng.reconstruct_device(d_px[j].data_ptr(), W, d_mk[j].data_ptr(), W, H, W, 0, brows,
+                                   d_out.data_ptr(), W, params, stream.cuda_stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        barrier()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    launches_per_frame = eng.last_stats()["kernel_launches"]
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    fps = STREAM_FRAMES / (ms_max * 1e-3)
+    e2e = None
+    if not args.no_e2e:
+        fs = FrameStream(H, W, params, device=local, engine=eng)
+        fs.run_timed(host[:2])
+        tt = []
+        for _ in range(args.steps):
+            barrier()
+            tt.append(fs.run_timed(host))
+        e = torch.tensor([float(np.mean(tt))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        e2e = {"value": STREAM_FRAMES / float(e.item()), "unit": "fps",
+               "h2d_bytes_per_step": int(len(mine) * H * W * 5),
+               "d2h_bytes_per_step": int(len(mine) * H * W * 4),
+               "ms_per_step": float(e.item()) * 1e3,
+               "pipeline": "FrameStream: H2D / kernels / D2H on three CUDA streams, double-buffered"}
+    line = {
+        "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if args.precision == "fp64" else "f32", "data": "synthetic",
+        "config": {"workload": f"stream of {STREAM_FRAMES} {W}x{H} quarter-sampled frames, "
+                               f"round-robin over {world} GPU(s) (BASELINE configs[3])",
+                   "B": B, "N": N, "iterations": I, "rho": 0.7, "gamma": 0.5,
+                   "reducer": args.reducer, "precision": args.precision, "argmax": args.argmax,
+                   "image": args.image, "parallelism": f"frames{world}",
+                   "l2": "flushed between steps (256 MiB write); frames > L2 at N=1"},
+        "gpu_launches": launches_per_frame * len(mine) * args.steps, "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "stream64":
+        run_stream(args)
         return
     import torch
     import torch.distributed as dist
@@ -225,8 +338,10 @@ def main():
     sampled, mask, original = make_frame(H, W, args.image)
     px32 = sampled.astype(np.float32)
     m8 = mask.astype(np.uint8)
+    from paper_2202_13926_b200 import shard
+
     brows, bcols = -(-H // B), -(-W // B)
-    row0, row1 = brows * rank // world, brows * (rank + 1) // world
+    row0, row1 = shard.strip_rows(brows, rank, world)
     my_blocks = (row1 - row0) * bcols
 
     eng = _lib.Engine([local])
@@ -299,6 +414,21 @@ def main():
                "ms_per_step": float(e.item()) * 1e3}
         # quality of this run against the original frame (rank 0 holds its strip only)
         out_full = ho.numpy()
+    # ---- N > 1: assemble the frame from the strips once (the only collective)
+    gather = None
+    if world > 1:
+        try:
+            ya, yb, oa, ob = shard.strip_io_rows(row0, row1, B, L, H)
+            barrier()
+            g0 = time.perf_counter()
+            full = shard.gather_strips(d_out[oa:ob], row0, row1, B, H, W, world)
+            torch.cuda.synchronize()
+            gms = (time.perf_counter() - g0) * 1e3
+            ok = bool(torch.equal(full[oa:ob], d_out[oa:ob]))
+            gather = {"ms": gms, "bytes": int(H * W * 4), "collective": "all_gather_into_tensor (NCCL)",
+                      "own_strip_intact": ok}
+        except Exception as exc:  # report, never lose the timing line
+            gather = {"error": repr(exc)[:200]}
     # ---- roofline for the dominant kernel
     pk, src = peaks()
     mean_main = float(np.mean(main_ms))
@@ -352,6 +482,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if gather is not None:
+        line["gather"] = gather
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
         t, nb, k = cpu_port_sample(sampled, mask, B, N, I, args.reducer, args.cpu_seconds, threads)

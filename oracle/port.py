@@ -276,11 +276,14 @@ def block_origins(height: int, width: int, block: int):
 
 
 def reconstruct_image(pixels, mask, block=4, border=14, iterations=100, rho=0.7, gamma=0.5,
-                      reducer="tree", early_stop=False, threads=0, trace=False):
+                      reducer="tree", early_stop=False, threads=0, trace=False, block_rows=None):
     """reconstruction.py:216-290 restated: spans of 128 blocks, numpy FFTs,
     the C loop, inverse FFT, merge and stitch.  With ``trace`` the per-block
     selections/objectives/ties/done are returned as well (they are the
-    reference's reconstruct_block_full traces, reconstruction.py:159-203)."""
+    reference's reconstruct_block_full traces, reconstruction.py:159-203).
+    ``block_rows=(r0, r1)`` restricts the work to target-block rows [r0, r1)
+    (a strip; other pixels keep the sampled values) -- the per-block result is
+    independent of which other blocks are processed (reconstruction.py:220-226)."""
     if reducer not in REDUCERS:
         raise ValueError(f"unknown argmax strategy {reducer!r}, expected one of {REDUCERS}")
     use_tree = reducer == "tree"
@@ -288,6 +291,9 @@ def reconstruct_image(pixels, mask, block=4, border=14, iterations=100, rho=0.7,
     mask = np.ascontiguousarray(mask, dtype=bool)
     height, width = pixels.shape
     rows, cols = block_origins(height, width, block)
+    if block_rows is not None:
+        keep = (rows >= block_rows[0] * block) & (rows < block_rows[1] * block)
+        rows, cols = rows[keep], cols[keep]
     s = block + 2 * border
     wf_flat = np.ascontiguousarray(frequency_weight(s)).ravel()
     decay = decay_grid(s, rho)

@@ -261,3 +261,24 @@ def test_tma_gather_matches_plain_loads(monkeypatch, shape):
         assert outs["0", precision][1] & 1, "TMA gather not used"
         assert not outs["1", precision][1] & 1
         assert np.array_equal(outs["0", precision][0], outs["1", precision][0]), precision
+
+
+def test_frame_stream_matches_single_frames():
+    """The pipelined frame stream (H2D / kernels / D2H on three streams,
+    double-buffered) returns exactly the per-frame results."""
+    from paper_2202_13926_b200 import _lib
+    from paper_2202_13926_b200.stream import FrameStream
+    H, W = 72, 96
+    frames = []
+    for i in range(5):
+        img = oracle.synthetic_frame(H, W, i)
+        s, m = oracle.quarter_sample(img, 42 + i)
+        frames.append((s.astype(np.float32), m.astype(np.uint8)))
+    p = _lib.make_params(4, 14, 60, precision="fp32", argmax="redux")
+    fs = FrameStream(H, W, p)
+    got = list(fs.run(frames))
+    eng = _lib.Engine([0])
+    for (px, mk), out in zip(frames, got):
+        ref = np.zeros_like(px)
+        eng.reconstruct_rows(px, mk, p, 0, (H + 3) // 4, ref)
+        assert np.array_equal(out, ref)
