@@ -159,10 +159,13 @@ def cpu_port_sample(sampled, mask, B, N, I, reducer, target_s, threads):
     L = (N - B) // 2
     bcols = -(-W // B)
 
+    out = [None]
+
     def run(k):
         h = min(H, k * B)
         t0 = time.perf_counter()
-        port.reconstruct_image(sampled[:h], mask[:h], B, L, I, 0.7, 0.5, reducer, threads=threads)
+        out[0] = port.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, reducer, threads=threads,
+                                        block_rows=(0, k))
         return time.perf_counter() - t0, -(-h // B) * bcols
 
     port.lib()
@@ -172,7 +175,20 @@ def cpu_port_sample(sampled, mask, B, N, I, reducer, target_s, threads):
     k = max(2, int(target_s / (per_block * bcols)))
     k = min(k, -(-H // B))
     t, nb = run(k)
-    return t, nb, k
+    return t, nb, k, out[0][:min(H, k * B)]
+
+
+def quality_vs_cpu(original, gpu_rows, cpu_rows):
+    """PSNR delta and max |error| of the GPU rows against the CPU reference
+    restatement on the same rows (the metric's "PSNR delta vs CPU reference")."""
+    from oracle import port
+    h = cpu_rows.shape[0]
+    ref = original[:h]
+    p_gpu = port.psnr(ref, gpu_rows.astype(np.float64))
+    p_cpu = port.psnr(ref, cpu_rows)
+    return {"psnr_gpu_db": p_gpu, "psnr_cpu_db": p_cpu, "psnr_delta_db": p_gpu - p_cpu,
+            "max_abs_err_0_1": float(np.abs(gpu_rows.astype(np.float64) - cpu_rows).max()) / 255.0,
+            "rows": int(h), "tolerance": "max |d| <= 1e-3 (0..1), |dPSNR| <= 0.01 dB (north_star)"}
 
 
 def run_reference(args):
@@ -187,7 +203,7 @@ def run_reference(args):
     per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     times = []
     for i in range(args.warmup + args.steps):
-        t, nb, k = cpu_port_sample(sampled, mask, B, N, I, args.reducer, per_step_s, threads)
+        t, nb, k, _ = cpu_port_sample(sampled, mask, B, N, I, args.reducer, per_step_s, threads)
         if i >= args.warmup:
             times.append(t * total / nb)  # seconds per full frame
     s_per_frame = float(np.mean(times))
@@ -486,7 +502,10 @@ def main():
         line["gather"] = gather
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        t, nb, k = cpu_port_sample(sampled, mask, B, N, I, args.reducer, args.cpu_seconds, threads)
+        t, nb, k, cpu_rows = cpu_port_sample(sampled, mask, B, N, I, args.reducer, args.cpu_seconds,
+                                             threads)
+        gpu_rows = d_out[:cpu_rows.shape[0]].cpu().numpy()
+        line["quality"] = quality_vs_cpu(original, gpu_rows, cpu_rows)
         total = brows * bcols
         cfps = nb / t / total
         line["cpu_baseline"] = {"value": cfps, "unit": "fps", "cores": threads, "kind": "port",
