@@ -7,6 +7,7 @@
 // kernel dispatch:
 //   precision FP64            -> image_generic_kernel<double>  (validation)
 //   precision FP32, N=32,B<=5 -> warp32_kernel (+ fp64 re-run of guarded blocks)
+//   precision FP32, N=16,B<=5 -> warp16_kernel (+ fp64 generic re-run of guarded blocks)
 //   precision FP32, other N   -> image_generic_kernel<float>  (+ fp64 re-run)
 // No CPU fallback: without a CUDA device every entry point returns FSR_ECUDA.
 #include <cuda_runtime.h>
@@ -30,6 +31,7 @@
 #include "fsr_common.cuh"
 #include "fsr_generic.cuh"
 #include "fsr_warp32.cuh"
+#include "fsr_warp16.cuh"
 #include "fsr_pair64.cuh"
 #include "fsr_warp64.cuh"
 
@@ -371,7 +373,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // aligned starts (W32_BOX_PX / W32_BOX_MK columns), zero fill outside the image.  Returns false when TMA cannot address the buffers (rows not
 // 16-byte aligned); the kernel then gathers with plain loads.
 bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t mask_pitch,
-                 int64_t H, int64_t W, Warp32Maps *m) {
+                 int64_t H, int64_t W, Warp32Maps *m, int box_px = W32_BOX_PX, int box_mk = W32_BOX_MK,
+                 int box_rows = 32) {
     if ((reinterpret_cast<uintptr_t>(px) & 15) || ((px_pitch * 4) & 15) ||
         (reinterpret_cast<uintptr_t>(mask) & 15) || (mask_pitch & 15) || H < 1 || W < 1 ||
         H > (int64_t)INT32_MAX || W > (int64_t)INT32_MAX)
@@ -379,7 +382,8 @@ bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t
     auto enc = tensor_map_encoder();
     if (!enc) return false;
     const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
-    const cuuint32_t bpx[2] = {W32_BOX_PX, 32}, bmk[2] = {W32_BOX_MK, 32}, estr[2] = {1, 1};
+    const cuuint32_t bpx[2] = {(cuuint32_t)box_px, (cuuint32_t)box_rows},
+                     bmk[2] = {(cuuint32_t)box_mk, (cuuint32_t)box_rows}, estr[2] = {1, 1};
     const cuuint64_t spx[1] = {(cuuint64_t)px_pitch * 4}, smk[1] = {(cuuint64_t)mask_pitch};
     if (enc(&m->px, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(px), dims, spx, bpx, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -411,6 +415,75 @@ int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32M
     return fail(eng, FSR_EINVAL, "unknown argmax implementation");
 }
 
+template <int WARPS, bool TREE, int AM, bool GUARD>
+int launch_warp16_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
+                    cudaStream_t st) {
+    auto k = warp16_kernel<WARPS, TREE, AM, GUARD>;
+    const size_t smem = sizeof(Warp16Smem<WARPS>);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (a.nblocks + WARPS - 1) / WARPS;
+    int grid = (int)std::min<int64_t>(want, (int64_t)d.sms * per_sm);
+    if (grid < 1) grid = 1;
+    k<<<grid, WARPS * 32, smem, st>>>(a, maps);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+int launch_warp16(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps, bool tree,
+                  int am, bool guard, cudaStream_t st) {
+#define FSR_W16(T, A, G) \
+    if (tree == T && am == A && guard == G) return launch_warp16_t<kWarps, T, A, G>(eng, d, a, maps, st);
+    FSR_W16(true, AM_SHFL, true) FSR_W16(true, AM_SHFL, false)
+    FSR_W16(false, AM_SHFL, true) FSR_W16(false, AM_SHFL, false)
+    FSR_W16(true, AM_REDUX, true) FSR_W16(true, AM_REDUX, false)
+    FSR_W16(false, AM_REDUX, true) FSR_W16(false, AM_REDUX, false)
+    FSR_W16(true, AM_SMEM, true) FSR_W16(true, AM_SMEM, false)
+    FSR_W16(false, AM_SMEM, true) FSR_W16(false, AM_SMEM, false)
+#undef FSR_W16
+    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+}
+
+template <int WARPS, bool TREE, int AM, typename IO>
+int launch_warp16d_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
+                     cudaStream_t st) {
+    auto k = warp16d_kernel<WARPS, TREE, AM, IO>;
+    const size_t smem = sizeof(Warp16dSmem<WARPS>);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t want = (want_blocks + WARPS - 1) / WARPS;
+    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
+    k<<<grid, WARPS * 32, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+template <typename IO>
+int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
+                   int64_t want_blocks, cudaStream_t st) {
+#define FSR_W16D(T, A) \
+    if (tree == T && am == A) return launch_warp16d_t<kWarps, T, A, IO>(eng, d, a, want_blocks, st);
+    FSR_W16D(true, AM_SHFL) FSR_W16D(false, AM_SHFL) FSR_W16D(true, AM_REDUX)
+    FSR_W16D(false, AM_REDUX) FSR_W16D(true, AM_SMEM) FSR_W16D(false, AM_SMEM)
+#undef FSR_W16D
+    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+}
+
+bool warp16d_eligible(const fsr_params *p) {
+    return p->block + 2 * p->border == 16 && p->block * p->block <= 32;
+}
+
+bool warp16_eligible(const fsr_params *p) {
+    const int N = p->block + 2 * p->border;
+    return N == 16 && p->block * p->block <= 32 && p->precision != FSR_PREC_FP64;
+}
+
 bool warp32_eligible(const fsr_params *p) {
     const int N = p->block + 2 * p->border;
     return N == 32 && p->block * p->block <= 32 && p->precision != FSR_PREC_FP64;
@@ -436,7 +509,9 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
     const int gen_grid = d.sms * 8;
     int rc = FSR_OK;
-    if (p->precision == FSR_PREC_FP64 || !(std::is_same<IO, float>::value && warp32_eligible(p))) {
+    const bool fast32 = std::is_same<IO, float>::value && warp32_eligible(p);
+    const bool fast16 = std::is_same<IO, float>::value && warp16_eligible(p);
+    if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16)) {
         if (p->precision == FSR_PREC_FP64 && pair64_eligible(p)) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
@@ -444,6 +519,16 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                W, bcols, first, nblocks, tab, sel, done,
                                                &ctr->empty_count, d.empty_list.as<int32_t>());
             if ((rc = launch_fp64_n32<IO>(eng, d, a, p, nblocks, st))) return rc;
+            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+        } else if (p->precision == FSR_PREC_FP64 && warp16d_eligible(p)) {
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, first, nblocks, tab, sel, done,
+                                               &ctr->empty_count, d.empty_list.as<int32_t>());
+            if ((rc = launch_warp16d<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                         nblocks, st)))
+                return rc;
             CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
         } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
@@ -515,13 +600,34 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.key_mask = 0xffffffe0u;
         Warp32Maps maps;
         std::memset(&maps, 0, sizeof(maps));
-        a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps)) ? 1 : 0;
-        d.used_tma = a.use_tma;
-        if ((rc = launch_warp32(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
-                                guarded || d.gap_debug != nullptr, st)))
-            return rc;
+        if (fast16) {
+            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps,
+                                                      W16_BOX_PX, W16_BOX_MK, 16)) ? 1 : 0;
+            d.used_tma = a.use_tma;
+            if ((rc = launch_warp16(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                    guarded, st)))
+                return rc;
+        } else {
+            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps)) ? 1 : 0;
+            d.used_tma = a.use_tma;
+            if ((rc = launch_warp32(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                    guarded || d.gap_debug != nullptr, st)))
+                return rc;
+        }
         CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
-        if (guarded) {
+        if (guarded && fast16) {
+            // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, 0, 0, tab, sel, done,
+                                               &ctr->ticket /* empties already counted */, nullptr);
+            r.list = d.rerun_list.as<int32_t>();
+            r.list_count = &ctr->rerun_count;
+            if ((rc = launch_warp16d<IO>(eng, d, r, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
+                                         (int64_t)d.sms * 16, st)))
+                return rc;
+        } else if (guarded) {
             // fp64 re-run of the blocks whose fp32 greedy decisions were ambiguous
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;

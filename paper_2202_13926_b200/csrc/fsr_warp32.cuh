@@ -109,7 +109,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // issues the two 2-D TMA box loads that complete on it.  (Issued from the
 // converged warp: UTMALDG is a uniform-datapath instruction.)
 __device__ __forceinline__ void tma_window(const Warp32Maps &maps, uint32_t bar, uint32_t dst_px,
-                                           uint32_t dst_mask, int x_px, int x_mk, int y0) {
+                                           uint32_t dst_mask, int x_px, int x_mk, int y0,
+                                           uint32_t bytes = W32_STAGE_BYTES) {
     asm volatile(
         "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
         "@p fence.proxy.async.shared::cta;\n"
@@ -118,7 +119,7 @@ __device__ __forceinline__ void tma_window(const Warp32Maps &maps, uint32_t bar,
         " [%2], [%3, {%4, %5}], [%0];\n"
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%6], [%7, {%8, %5}], [%0];\n}"
-        ::"r"(bar), "r"(W32_STAGE_BYTES), "r"(dst_px), "l"(reinterpret_cast<uint64_t>(&maps.px)),
+        ::"r"(bar), "r"(bytes), "r"(dst_px), "l"(reinterpret_cast<uint64_t>(&maps.px)),
         "r"(x_px), "r"(y0), "r"(dst_mask), "l"(reinterpret_cast<uint64_t>(&maps.mask)), "r"(x_mk)
         : "memory");
 }

@@ -236,8 +236,9 @@ def test_device_api_matches_host_api():
     assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
 
 
+@pytest.mark.parametrize("support", [32, 16])
 @pytest.mark.parametrize("shape", [(96, 128), (1080 // 8, 1920 // 8)])
-def test_tma_gather_matches_plain_loads(monkeypatch, shape):
+def test_tma_gather_matches_plain_loads(monkeypatch, shape, support):
     """The N=32 fp32 kernel gathers each 32x32 window with 2-D TMA (zero fill
     outside the image = the reference's outside-is-unknown rule,
     sampling.py:93-107).  It must give bitwise the same image as the
@@ -252,7 +253,7 @@ def test_tma_gather_matches_plain_loads(monkeypatch, shape):
         monkeypatch.setenv("FSR_NO_TMA", no_tma)
         eng = _lib.Engine([0])
         for precision in ("fp32", "fp32_unguarded"):
-            p = _lib.make_params(4, 14, 100, precision=precision, argmax="redux")
+            p = _lib.make_params(4, (support - 4) // 2, 100, precision=precision, argmax="redux")
             out = np.zeros_like(px)
             eng.reconstruct_rows(px, m8, p, 0, (H + 3) // 4, out)
             outs[no_tma, precision] = (out, eng.last_stats()["flags"])
@@ -282,3 +283,27 @@ def test_frame_stream_matches_single_frames():
         ref = np.zeros_like(px)
         eng.reconstruct_rows(px, mk, p, 0, (H + 3) // 4, ref)
         assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("reducer", ["tree", "linear"])
+@pytest.mark.parametrize("argmax", ["redux", "shfl", "smem"])
+def test_support16_fp32_kernel_matches_oracle(reducer, argmax):
+    """The N=16 register kernel (warp16, the paper's S=16): guarded fp32 within
+    the production tolerance of the reference restatement; unguarded fp32 on
+    the same kernel as an ablation (PSNR only)."""
+    img = oracle.synthetic_frame(96, 128, 21)
+    sampled, mask = oracle.quarter_sample(img, 8)
+    ref = oracle.reconstruct_image(sampled, mask, 4, 6, 100, 0.7, 0.5, reducer)
+    out, tr = fsr.reconstruct(sampled.astype(np.float32), mask, 4, 16, 100, reducer=reducer,
+                              precision="fp32", argmax=argmax, return_trace=True)
+    out = out.astype(np.float64)
+    assert float(np.abs(out - ref).max()) <= FP32_TOL
+    assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
+    assert np.array_equal(out[mask], sampled[mask].astype(np.float32).astype(np.float64))
+    # every non-guarded block's selection sequence equals the fp64 engine's
+    # modulo the conjugate mirror except where the guard re-ran it in fp64
+    _, tr64 = fsr.reconstruct(sampled, mask, 4, 16, 100, reducer=reducer, precision="fp64",
+                              return_trace=True)
+    counts, div = oracle.compare_sequences(tr.selections.astype(np.int64),
+                                           tr64.selections.astype(np.int64), 16)
+    assert div.mean() <= 0.05, div.mean()

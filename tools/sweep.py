@@ -76,8 +76,9 @@ def main():
                         "frame_ms": frame_ms, "fps": 1e3 / frame_ms,
                         "mpixel_per_s": H * W / (frame_ms * 1e-3) / 1e6,
                         "rerun_fraction": stats["rerun_blocks"] / max(1, rows * bcols),
-                        "kernel": "warp32" if N == 32 and args.precision != "fp64" else
-                                  ("pair64" if N == 32 else "generic")}
+                        "kernel": {(32, False): "warp32 (+pair64 re-runs)", (32, True): "pair64",
+                                   (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d"}
+                                  .get((N, args.precision == "fp64"), "generic")}
                 print(json.dumps(line), flush=True)
 
 
