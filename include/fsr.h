@@ -139,6 +139,27 @@ int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int
                         const double *thr, int32_t *sel, double *obj, uint8_t *ties,
                         int32_t *done);
 
+/*
+ * The callers either side of the loop, on the engine's first device,
+ * asynchronous on `stream` (device pointers, pitches in elements):
+ *
+ * fsr_quarter_sample_device: quarter sampling of a frame exactly as
+ * fsrkit.sampling.quarter_sample (pkg/src/fsrkit/sampling.py:18-29 SplitMix64,
+ * 53-80): one known pixel per 2x2 cell (edge cells of odd frames shrink);
+ * writes the mask (1 = known) and the sampled frame (unknown pixels 0).
+ *
+ * fsr_sq_error_device: *d_sse = sum over pixels of (clamp(test,0,255) - ref)^2
+ * in fp64 (fsrkit.metrics.psnr, metrics.py:35-48: PSNR = 10 log10(255^2 /
+ * (sse / (height*width)))); deterministic summation order.
+ */
+int fsr_quarter_sample_device(fsr_engine *eng, const float *d_img, int64_t img_pitch,
+                              int64_t height, int64_t width, uint64_t seed, float *d_sampled,
+                              int64_t sampled_pitch, uint8_t *d_mask, int64_t mask_pitch,
+                              void *stream);
+int fsr_sq_error_device(fsr_engine *eng, const float *d_ref, int64_t ref_pitch, const float *d_test,
+                        int64_t test_pitch, int64_t height, int64_t width, double *d_sse,
+                        void *stream);
+
 /* Statistics of the last image call on the first device. */
 typedef struct {
     int64_t blocks;          /* target blocks processed */

@@ -94,6 +94,10 @@ def load():
         L.fsr_reconstruct_device_f32.restype = ctypes.c_int
         L.fsr_iterate_spectra.argtypes = [P, pp, i64, i32, P, P, P, P, P, P, P, P, P]
         L.fsr_iterate_spectra.restype = ctypes.c_int
+        L.fsr_quarter_sample_device.argtypes = [P, P, i64, i64, i64, ctypes.c_uint64, P, i64, P, i64, P]
+        L.fsr_quarter_sample_device.restype = ctypes.c_int
+        L.fsr_sq_error_device.argtypes = [P, P, i64, P, i64, i64, i64, P, P]
+        L.fsr_sq_error_device.restype = ctypes.c_int
         L.fsr_last_stats.argtypes = [P, ctypes.POINTER(FsrStatsC)]
         L.fsr_last_stats.restype = ctypes.c_int
         _lib = L
@@ -103,7 +107,7 @@ def load():
 EXPORTED = ["fsr_params_init", "fsr_params_validate", "fsr_engine_create", "fsr_engine_destroy",
             "fsr_last_error", "fsr_status_string", "fsr_abi_version", "fsr_reconstruct_f64",
             "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_device_f32", "fsr_iterate_spectra",
-            "fsr_last_stats"]
+            "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats"]
 
 
 def _ptr(a):
@@ -215,6 +219,20 @@ class Engine:
         self._check(self._L.fsr_iterate_spectra(
             self._h, ctypes.byref(params), count, n, _ptr(R), _ptr(G), _ptr(W), _ptr(wf),
             _ptr(thr), _ptr(sel), _ptr(obj), _ptr(ties), _ptr(done)))
+
+    def quarter_sample_device(self, d_img, img_pitch, height, width, seed, d_sampled, sampled_pitch,
+                              d_mask, mask_pitch, stream=0):
+        """On-device quarter sampling (sampling.py:53-80), asynchronous on ``stream``."""
+        self._check(self._L.fsr_quarter_sample_device(
+            self._h, ctypes.c_void_p(d_img), img_pitch, height, width, ctypes.c_uint64(seed & (2**64 - 1)),
+            ctypes.c_void_p(d_sampled), sampled_pitch, ctypes.c_void_p(d_mask), mask_pitch,
+            ctypes.c_void_p(stream)))
+
+    def sq_error_device(self, d_ref, ref_pitch, d_test, test_pitch, height, width, d_sse, stream=0):
+        """*d_sse = sum (clamp(test, 0, 255) - ref)^2 in fp64 (metrics.py:35-48), asynchronous."""
+        self._check(self._L.fsr_sq_error_device(
+            self._h, ctypes.c_void_p(d_ref), ref_pitch, ctypes.c_void_p(d_test), test_pitch, height,
+            width, ctypes.c_void_p(d_sse), ctypes.c_void_p(stream)))
 
     def last_stats(self) -> dict:
         s = FsrStatsC()

@@ -33,6 +33,7 @@
 #include "fsr_warp32.cuh"
 #include "fsr_warp16.cuh"
 #include "fsr_pair64.cuh"
+#include "fsr_aux.cuh"
 #include "fsr_warp64.cuh"
 
 using namespace fsr;
@@ -80,7 +81,7 @@ struct Device {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     DevBuf px, mask, out, sel, done, empty_list, rerun_list, counters;
-    DevBuf R, G, W, wf, thr, obj, ties;
+    DevBuf R, G, W, wf, thr, obj, ties, partials;
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
@@ -1056,3 +1057,45 @@ int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Callers either side of the loop, on the device.
+
+int fsr_quarter_sample_device(fsr_engine *eng, const float *d_img, int64_t img_pitch,
+                              int64_t height, int64_t width, uint64_t seed, float *d_sampled,
+                              int64_t sampled_pitch, uint8_t *d_mask, int64_t mask_pitch,
+                              void *stream) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
+    Device &d = *eng->devs[0];
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    const int64_t cells = ((height + 1) / 2) * ((width + 1) / 2);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((cells + 255) / 256, (int64_t)d.sms * 16));
+    quarter_sample_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(d_img, img_pitch, height, width, seed,
+                                                                  d_sampled, sampled_pitch, d_mask,
+                                                                  mask_pitch);
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+int fsr_sq_error_device(fsr_engine *eng, const float *d_ref, int64_t ref_pitch, const float *d_test,
+                        int64_t test_pitch, int64_t height, int64_t width, double *d_sse,
+                        void *stream) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
+    Device &d = *eng->devs[0];
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    const int grid = d.sms * 4;  // fixed grid: the fixed-order final sum is deterministic
+    CUDA_TRY(eng, d.partials.ensure((size_t)grid * sizeof(double)));
+    cudaStream_t st = (cudaStream_t)stream;
+    sq_err_partial_kernel<<<grid, 256, 0, st>>>(d_ref, ref_pitch, d_test, test_pitch, height, width,
+                                                d.partials.as<double>());
+    CUDA_TRY(eng, cudaGetLastError());
+    sq_err_final_kernel<<<1, 32, 0, st>>>(d.partials.as<double>(), grid, d_sse);
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}

@@ -211,3 +211,22 @@ def extract_support_block(sampled: SampledImage, desc: BlockDescriptor, support:
         sig[ya - y0:yb - y0, xa - x0:xb - x0] = sampled.image.pixels[ya:yb, xa:xb]
         m[ya - y0:yb - y0, xa - x0:xb - x0] = sampled.mask[ya:yb, xa:xb]
     return SampledBlock(signal=sig, mask=m)
+
+
+def quarter_sample_device(image, seed: int, engine=None, stream=None):
+    """``quarter_sample`` on the GPU (sampling.py:53-80, bit-exact): ``image`` is
+    a float32 CUDA tensor [H, W]; returns (sampled, mask) CUDA tensors (float32,
+    uint8) produced by libfsr's fsr_quarter_sample_device."""
+    import torch
+
+    from . import _lib
+
+    img = image.contiguous()
+    h, w = img.shape
+    eng = engine or _lib.default_engine([img.device.index or 0])
+    sampled = torch.empty_like(img)
+    mask = torch.empty((h, w), dtype=torch.uint8, device=img.device)
+    st = stream or torch.cuda.current_stream(img.device)
+    eng.quarter_sample_device(img.data_ptr(), w, h, w, seed, sampled.data_ptr(), w, mask.data_ptr(), w,
+                              st.cuda_stream)
+    return sampled, mask

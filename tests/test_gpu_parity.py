@@ -307,3 +307,30 @@ def test_support16_fp32_kernel_matches_oracle(reducer, argmax):
     counts, div = oracle.compare_sequences(tr.selections.astype(np.int64),
                                            tr64.selections.astype(np.int64), 16)
     assert div.mean() <= 0.05, div.mean()
+
+
+@pytest.mark.parametrize("shape,seed", [((37, 53), 42), ((1080, 1920), 7), ((2, 1), 3), ((1, 5), 2**63 + 11)])
+def test_quarter_sample_device_bitexact(shape, seed):
+    """On-device quarter sampling == the reference's SplitMix64 quarter_sample
+    (sampling.py:18-80; the oracle is pinned to the reference KATs)."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200.frames import quarter_sample_device
+    img = oracle.synthetic_frame(*shape, 5) if min(shape) > 2 else np.arange(shape[0] * shape[1],
+                                                                               dtype=np.float64).reshape(shape)
+    ref_s, ref_m = oracle.quarter_sample(img.astype(np.float32).astype(np.float64), seed)
+    s, m = quarter_sample_device(torch.tensor(img, dtype=torch.float32, device="cuda"), seed)
+    assert np.array_equal(m.cpu().numpy().astype(bool), ref_m)
+    assert np.array_equal(s.cpu().numpy().astype(np.float64), ref_s)
+
+
+def test_psnr_device_matches_reference():
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200.quality import psnr_device
+    d = golden_image("c1_natural")
+    out = fsr.reconstruct(d["sampled"].astype(np.float32), d["mask"], 4, 32, 100, precision="fp32")
+    ref32 = d["original"].astype(np.float32)
+    r = psnr_device(torch.tensor(ref32, device="cuda"), torch.tensor(out, device="cuda"))
+    want = oracle.psnr(ref32.astype(np.float64), out.astype(np.float64))
+    assert abs(r.psnr_db - want) <= 1e-9 * abs(want)
+    same = psnr_device(torch.tensor(ref32, device="cuda"), torch.tensor(ref32, device="cuda"))
+    assert same.identical and same.psnr_db == float("inf")
