@@ -253,10 +253,10 @@ int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, 
     return FSR_OK;
 }
 
-template <int WARPS, bool TREE, int AM, bool GUARD, bool STUDY = false>
+template <int WARPS, bool TREE, int AM, bool GUARD, bool STUDY = false, int OPTS = W32_ALL>
 int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
                     cudaStream_t st) {
-    auto k = warp32_kernel<WARPS, TREE, AM, GUARD, STUDY>;
+    auto k = warp32_kernel<WARPS, TREE, AM, GUARD, STUDY, OPTS>;
     const size_t smem = sizeof(Warp32Smem<WARPS>);
     CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -404,6 +404,15 @@ int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32M
         return tree ? launch_warp32_t<kWarps, true, AM_REDUX, true, true>(eng, d, a, maps, st)
                     : launch_warp32_t<kWarps, false, AM_REDUX, true, true>(eng, d, a, maps, st);
     }
+    // production argmax: variants without the trace / early-stop checks
+    const int opts = (a.sel ? W32_TRACE : 0) | (a.early_stop ? W32_EARLY : 0);
+#define FSR_W32R(T, G, O) \
+    if (am == AM_REDUX && tree == T && guard == G && opts == O) \
+        return launch_warp32_t<kWarps, T, AM_REDUX, G, false, O>(eng, d, a, maps, st);
+    FSR_W32R(true, true, 0) FSR_W32R(true, false, 0) FSR_W32R(false, true, 0) FSR_W32R(false, false, 0)
+    FSR_W32R(true, true, 1) FSR_W32R(true, false, 1) FSR_W32R(false, true, 1) FSR_W32R(false, false, 1)
+    FSR_W32R(true, true, 2) FSR_W32R(true, false, 2) FSR_W32R(false, true, 2) FSR_W32R(false, false, 2)
+#undef FSR_W32R
 #define FSR_W32(T, A, G) \
     if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, maps, st);
     FSR_W32(true, AM_SHFL, true) FSR_W32(true, AM_SHFL, false)

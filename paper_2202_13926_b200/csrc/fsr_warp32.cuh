@@ -416,9 +416,14 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 }
 
 // STUDY: record per-block minimum top-2 gaps (tools/guard_study.py only).
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY>
+// OPTS: W32_TRACE compiles the selection trace in, W32_EARLY the early stop;
+// production launches without them carry no per-iteration checks for either.
+constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_ALL = 3;
+
+template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY, int OPTS = W32_ALL>
 __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
+    constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
@@ -460,7 +465,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
         float2 wf2[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) wf2[i] = make_float2(__ldg(a.wf + i * 32 + v), __ldg(a.wf + (i + 16) * 32 + v));
-        int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        int32_t *sel_b = (TRACE && a.sel) ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
             if (lane == 0) {
                 unsigned slot = atomicAdd(a.empty_count, 1u);
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
         }
         // early stop threshold: 1e-12 * sum f^2 w (reconstruction.py:262-266)
         float thr = 0.f;
-        if (a.early_stop) {
+        if (EARLY && a.early_stop) {
             float e = energy;
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
@@ -510,8 +515,8 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
             const uint32_t urank = 31u - (kmax & 31u);
             const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
             const float b1 = __uint_as_float(kmax & ~31u);
-            if (sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
-            if (b1 < thr) {  // thr == 0 unless early stop is on
+            if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
+            if (EARLY && b1 < thr) {  // thr == 0 unless early stop is on
                 if (GUARD && b1 >= thr * one_minus_tau) flagged = true;  // a stop decision within tau
                 break;
             }
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
                 const float b2 = __uint_as_float(k2 & ~31u);
                 flagged |= b2 >= b1 * one_minus_tau;
                 // a continue decision within tau of the stop threshold is ambiguous too
-                flagged |= b1 * one_minus_tau < thr;
+                if (EARLY) flagged |= b1 * one_minus_tau < thr;
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)
                     if (it == 0) B0 = b1;
                     min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
