@@ -7,7 +7,8 @@
 // kernel dispatch:
 //   precision FP64            -> image_generic_kernel<double>  (validation)
 //   precision FP32, N=32,B<=5 -> warp32_kernel (+ fp64 re-run of guarded blocks)
-//   precision FP32, N=16,B<=5 -> warp16_kernel (+ fp64 generic re-run of guarded blocks)
+//   precision FP32, N=16,B<=5 -> warp16_kernel (+ warp16d fp64 re-run of guarded blocks)
+//   precision FP32, N=64       -> cta64_kernel (+ generic fp64 re-run of guarded blocks)
 //   precision FP32, other N   -> image_generic_kernel<float>  (+ fp64 re-run)
 // No CPU fallback: without a CUDA device every entry point returns FSR_ECUDA.
 #include <cuda_runtime.h>
@@ -32,6 +33,7 @@
 #include "fsr_generic.cuh"
 #include "fsr_warp32.cuh"
 #include "fsr_warp16.cuh"
+#include "fsr_cta64.cuh"
 #include "fsr_pair64.cuh"
 #include "fsr_aux.cuh"
 #include "fsr_warp64.cuh"
@@ -485,6 +487,27 @@ int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tre
     return fail(eng, FSR_EINVAL, "unknown argmax implementation");
 }
 
+template <bool GUARD>
+int launch_cta64_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
+                   cudaStream_t st) {
+    auto k = cta64_kernel<GUARD>;
+    const size_t smem = sizeof(C64Smem);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C64_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nblocks, (int64_t)d.sms * per_sm));
+    k<<<grid, C64_THREADS, smem, st>>>(a, maps);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
+bool cta64_eligible(const fsr_params *p) {
+    return p->block + 2 * p->border == 64 && p->block * p->block <= C64_THREADS &&
+           p->reducer == FSR_REDUCER_LINEAR && p->precision != FSR_PREC_FP64;
+}
+
 bool warp16d_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 16 && p->block * p->block <= 32;
 }
@@ -521,7 +544,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     int rc = FSR_OK;
     const bool fast32 = std::is_same<IO, float>::value && warp32_eligible(p);
     const bool fast16 = std::is_same<IO, float>::value && warp16_eligible(p);
-    if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16)) {
+    const bool fast64 = std::is_same<IO, float>::value && cta64_eligible(p);
+    if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16 || fast64)) {
         if (p->precision == FSR_PREC_FP64 && pair64_eligible(p)) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
@@ -610,7 +634,14 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.key_mask = 0xffffffe0u;
         Warp32Maps maps;
         std::memset(&maps, 0, sizeof(maps));
-        if (fast16) {
+        if (fast64) {
+            a.key_mask = 0xffffffc0u;  // 6 rank bits (row u of 64)
+            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps,
+                                                      C64_BOX_PX, C64_BOX_MK, 64)) ? 1 : 0;
+            d.used_tma = a.use_tma;
+            rc = guarded ? launch_cta64_t<true>(eng, d, a, maps, st) : launch_cta64_t<false>(eng, d, a, maps, st);
+            if (rc) return rc;
+        } else if (fast16) {
             a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps,
                                                       W16_BOX_PX, W16_BOX_MK, 16)) ? 1 : 0;
             d.used_tma = a.use_tma;
@@ -625,7 +656,17 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                 return rc;
         }
         CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
-        if (guarded && fast16) {
+        if (guarded && fast64) {
+            // fp64 re-run of ambiguous blocks on the exact generic kernel (list mode)
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            ImageArgs<double, IO> r{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
+                                    p->block, p->border, N, p->iterations, bcols, 0, 0,
+                                    d.rerun_list.as<int32_t>(), &ctr->rerun_count, p->gamma,
+                                    p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel, done,
+                                    &ctr->ticket /* empties already counted */, nullptr};
+            if ((rc = launch_generic(eng, d, r, d.sms * 8, st))) return rc;
+        } else if (guarded && fast16) {
             // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;

@@ -1,0 +1,381 @@
+// fsr_cta64.cuh -- FSR kernel for support N = 64 (BASELINE configs[4]; beyond the
+// reference's S^2 <= 1024 cap, so the linear reducer only: core.py:76-80,
+// SURVEY §8c), fp32 loop with the near-tie guard, one 4-warp CTA per block.
+//
+// Per block (4096 bins):
+//   threads    tid = h * 64 + v owns spectral column v and the 16 row pairs
+//              (u, u + 32), u = 16h + i (i = 0..15): 32 bins, 64 registers, as
+//              in fsr_warp32.cuh.  Threads with equal row u share h, so among
+//              equal keys the lowest tid is the lowest column: the linear
+//              reducer's tie order (_kernels.py:52-59) is "max key, then
+//              lowest tid", and keys carry 63 - u in their 6 low bits.
+//   W          row-pair table U64[k][c] = (W[k+32][c], W[k][c]) (x then y),
+//              64 x 64 float4 = 64 KiB; pair i of thread (v, h) reads row
+//              32 + 16h + i - (pu mod 32) (never wraps), halves swapped when
+//              pu >= 32; lanes read consecutive columns (conflict-free).
+//   argmax     per warp: redux + ballot (the warp's best key, its winning
+//              lane's coefficient and its runner-up for the guard) into a
+//              double-buffered slot; one __syncthreads; every thread then
+//              reduces the 4 slots -- the paper's two-phase (in-warp, then
+//              cross-warp) argmax with the coefficient carried along.
+//   prologue   2-D TMA gather (68-column f32 and 80-column u8 boxes from
+//              16-byte aligned starts), fp64 2-D FFT on a 64 x 65 double2
+//              tile: each 64-point line as four 16-point register FFTs
+//              (samples 4m + r) and a radix-4 combine with twiddles from a
+//              shared table, frequency f landing at position
+//              4 (f mod 16) + f div 16; Hermitian split, R and W rounded to
+//              fp32 once.
+//   re-runs    flagged blocks: the exact generic fp64 kernel in list mode.
+#pragma once
+
+#include "fsr_warp32.cuh"
+
+namespace fsr {
+
+constexpr int C64_THREADS = 128;
+constexpr int C64_TS = 65;  // fp64 tile row stride (double2)
+constexpr int C64_BOX_PX = 68, C64_BOX_MK = 80;
+constexpr int C64_STAGE_MK = 64 * C64_BOX_PX * 4;                 // 17408
+constexpr int C64_STAGE_BYTES = C64_STAGE_MK + 64 * C64_BOX_MK;   // 22528
+constexpr int C64_REGION = 64 * C64_TS * 16;                      // 66560 >= 64 KiB U table
+
+struct __align__(16) C64Slot {
+    uint32_t k1, k2;  // warp best key, warp runner-up key
+    float cre, cim;   // coefficient R[u*][v*] of the warp's best bin
+    int32_t lane;
+    int32_t pad[3];
+};
+
+struct C64Smem {
+    unsigned char region[C64_REGION];  // TMA staging -> fp64 tile -> U64 table
+    double2 tw[64];                    // e^{-2 pi i j / 64}
+    float2 cs[64];                     // (cos, sin)(2 pi j / 64)
+    C64Slot slot[2][4];
+    unsigned int red_key[4][32], red_rank[4][32];
+    double esum[4];
+    unsigned long long bar;
+};
+
+__device__ __forceinline__ int c64_pos(int f) { return ((f & 15) << 2) | (f >> 4); }
+
+// One 64-point forward DFT line of the tile, shared by 2 threads per line
+// (phase A: sub-FFTs r and r + 2; phase B: 8 combines each), all 64 lines.
+// Line `ln` element `e` is at t[ln * ls + e * es].
+__device__ __forceinline__ void c64_fft_lines(double2 *t, int ls, int es, const double2 *tw, int tid) {
+    const int ln = tid & 63, r0 = tid >> 6;  // r0 in {0, 1}
+    double2 *line = t + ln * ls;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {  // phase A: 16-point FFTs of samples 4m + r, in place at 4k + r
+        const int r = r0 + 2 * q;
+        cpx<double> xv[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) { const double2 z = line[(4 * m + r) * es]; xv[m] = {z.x, z.y}; }
+        fft_pow2<4>(xv);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) line[(4 * k + r) * es] = make_double2(xv[k].re, xv[k].im);
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int jj = 0; jj < 8; ++jj) {  // phase B: radix-4 combine of bin k
+        const int k = r0 + 2 * jj;
+        double2 a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double2 f = line[(4 * k + r) * es];
+            if (r == 0) {
+                a[0] = f;
+            } else {
+                const double2 w = tw[(r * k) & 63];
+                a[r] = make_double2(f.x * w.x - f.y * w.y, f.x * w.y + f.y * w.x);
+            }
+        }
+        const double2 s02 = make_double2(a[0].x + a[2].x, a[0].y + a[2].y);
+        const double2 d02 = make_double2(a[0].x - a[2].x, a[0].y - a[2].y);
+        const double2 s13 = make_double2(a[1].x + a[3].x, a[1].y + a[3].y);
+        const double2 d13 = make_double2(a[1].x - a[3].x, a[1].y - a[3].y);
+        // y_q = sum_r a_r (-i)^{rq}
+        line[(4 * k + 0) * es] = make_double2(s02.x + s13.x, s02.y + s13.y);
+        line[(4 * k + 1) * es] = make_double2(d02.x + d13.y, d02.y - d13.x);
+        line[(4 * k + 2) * es] = make_double2(s02.x - s13.x, s02.y - s13.y);
+        line[(4 * k + 3) * es] = make_double2(d02.x - d13.y, d02.y + d13.x);
+    }
+    __syncthreads();
+}
+
+template <bool GUARD, bool HERM, bool UPDATE, bool SWAP>
+__device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
+                                       const float4 *up, float gr, float gi, uint32_t canon,
+                                       int h, uint32_t hmask, uint32_t &m1, uint32_t &m2) {
+    m1 = 0;
+    m2 = 0;
+    const float2 ngr = make_float2(-gr, -gr), pgi = make_float2(gi, gi), ngi = make_float2(-gi, -gi);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float2 r = re[i], m = im[i];
+        if (UPDATE) {
+            const float4 w = up[i * 64];
+            const float2 wx = SWAP ? make_float2(w.y, w.x) : make_float2(w.x, w.y);
+            const float2 wy = SWAP ? make_float2(w.w, w.z) : make_float2(w.z, w.w);
+            r = __ffma2_rn(wx, ngr, r);
+            r = __ffma2_rn(wy, pgi, r);
+            m = __ffma2_rn(wy, ngr, m);
+            m = __ffma2_rn(wx, ngi, m);
+            re[i] = r;
+            im[i] = m;
+        }
+        const float2 mag = __ffma2_rn(r, r, __fmul2_rn(m, m));
+        const float2 o = __fmul2_rn(mag, wf2[i]);
+        const uint32_t u = (uint32_t)(16 * h + i);  // h is uniform per warp
+        uint32_t ka = (f2u(o.x) & hmask) | (63u - u);
+        uint32_t kb = (f2u(o.y) & hmask) | (31u - u);  // row u + 32: 63 - (u + 32)
+        if (HERM && GUARD) {
+            ka = ((canon >> i) & 1u) ? ka : 0u;
+            kb = ((canon >> (i + 16)) & 1u) ? kb : 0u;
+        }
+        if (GUARD) {
+            const uint32_t hi = max(ka, kb), lo = min(ka, kb);
+            m2 = umax3(m2, lo, min(m1, hi));
+            m1 = max(m1, hi);
+        } else {
+            m1 = umax3(m1, ka, kb);
+        }
+    }
+}
+
+template <bool GUARD>
+__global__ void __launch_bounds__(C64_THREADS, 3)
+    cta64_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    C64Smem &sm = *reinterpret_cast<C64Smem *>(smem_raw);
+    const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    const int h = tid >> 6, v = tid & 63;
+    if (tid < 64) {
+        const double th = 6.283185307179586476925286766559 * tid / 64.0;
+        sm.tw[tid] = make_double2(cos(th), -sin(th));
+        sm.cs[tid] = make_float2((float)cos(th), (float)sin(th));
+    }
+    const uint32_t bar = smem_u32(&sm.bar);
+    if (tid == 0) mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    uint32_t phase = 0;
+    double2 *t = reinterpret_cast<double2 *>(sm.region);
+    float4 *ub = reinterpret_cast<float4 *>(sm.region);
+    // canonical half of each mirror pair (linear rank = flat index): bit i row 16h+i, bit i+16 row +32
+    uint32_t canon = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int u = 16 * h + i + 32 * hh;
+            const int tt = u * 64 + v, mt = ((64 - u) & 63) * 64 + ((64 - v) & 63);
+            canon |= (uint32_t)(tt <= mt) << (i + 16 * hh);
+        }
+    }
+    const float one_minus_tau = 1.f - a.tau;
+
+    for (int64_t bi = blockIdx.x; bi < a.nblocks; bi += gridDim.x) {
+        const int64_t bid = a.first + bi;
+        const int64_t brow = bid / a.bcols, bcol = bid - brow * a.bcols;
+        const int64_t r0 = brow * a.B, c0 = bcol * a.B;
+        const int64_t wr0 = r0 - a.L, wc0 = c0 - a.L;
+        // ---- gather: thread owns window column v, rows 32h .. 32h + 31
+        float pf[32];
+        uint32_t pm[32];
+        if (a.use_tma) {
+            const int x0 = (int)wc0, xp = x0 & ~3, xm = x0 & ~15;
+            const float *spx = reinterpret_cast<const float *>(sm.region);
+            const uint8_t *smk = sm.region + C64_STAGE_MK;
+            if (wid == 0)
+                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0, C64_STAGE_BYTES);
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+            const float *cpx = spx + 32 * h * C64_BOX_PX + (x0 - xp) + v;
+            const uint8_t *cmk = smk + 32 * h * C64_BOX_MK + (x0 - xm) + v;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                pf[k] = cpx[k * C64_BOX_PX];
+                pm[k] = cmk[k * C64_BOX_MK];
+            }
+        } else {
+            const int64_t x = wc0 + v;
+            const bool xin = x >= 0 && x < a.W;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                const int64_t y = wr0 + 32 * h + k;
+                const bool in = xin && y >= 0 && y < a.H;
+                pf[k] = in ? __ldg(a.px + y * a.px_pitch + x) : 0.f;
+                pm[k] = in ? (uint32_t)__ldg(a.mask + y * a.mask_pitch + x) : 0u;
+            }
+        }
+        __syncthreads();  // staging fully read before the tile overwrites it
+        double energy = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const int r = 32 * h + k;
+            double f = 0.0, w = 0.0;
+            if (pm[k]) {
+                f = (double)pf[k];
+                w = __ldg(a.decay64 + r * 64 + v);
+            }
+            t[r * C64_TS + v] = make_double2(f * w, w);
+            energy = fma(f * f, w, energy);
+        }
+        __syncthreads();
+        c64_fft_lines(t, C64_TS, 1, sm.tw, tid);  // rows
+        c64_fft_lines(t, 1, C64_TS, sm.tw, tid);  // columns
+        // ---- split (thread (v, h): rows 16h + i and + 32 of column v)
+        float2 re[16], im[16], Wl[16], Wh[16];
+        {
+            const int pv = c64_pos(v), pmv = c64_pos((64 - v) & 63);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int u = 16 * h + i + 32 * hh, nu = (64 - u) & 63;
+                    const double2 z = t[c64_pos(u) * C64_TS + pv], zm = t[c64_pos(nu) * C64_TS + pmv];
+                    const float rr = (float)((z.x + zm.x) * 0.5), ri = (float)((z.y - zm.y) * 0.5);
+                    const float2 w = make_float2((float)((z.y + zm.y) * 0.5), (float)((zm.x - z.x) * 0.5));
+                    if (hh == 0) {
+                        re[i].x = rr;
+                        im[i].x = ri;
+                        Wl[i] = w;
+                    } else {
+                        re[i].y = rr;
+                        im[i].y = ri;
+                        Wh[i] = w;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int u = 16 * h + i;
+            ub[u * 64 + v] = make_float4(Wh[i].x, Wl[i].x, Wh[i].y, Wl[i].y);
+            ub[(u + 32) * 64 + v] = make_float4(Wl[i].x, Wh[i].x, Wl[i].y, Wh[i].y);
+        }
+        // early-stop energy: CTA sum
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
+        if (lane == 0) sm.esum[wid] = energy;
+        __syncthreads();
+        const float w00 = ub[32 * 64].x;  // U64[32][0].x = Wx[0][0]
+        int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        if (!(w00 > 0.f)) {
+            if (tid == 0) {
+                unsigned slot = atomicAdd(a.empty_count, 1u);
+                a.empty_list[slot] = (int32_t)bid;
+                if (a.done) a.done[bid] = 0;
+            }
+            if (sel_b)
+                for (int it = tid; it < a.iterations; it += C64_THREADS) sel_b[it] = -1;
+            __syncthreads();
+            continue;
+        }
+        const float thr = a.early_stop ? 1e-12f * (float)(sm.esum[0] + sm.esum[1] + sm.esum[2] + sm.esum[3])
+                                       : 0.f;
+        float2 wf2[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            wf2[i] = make_float2(__ldg(a.wf + (16 * h + i) * 64 + v), __ldg(a.wf + (16 * h + i + 32) * 64 + v));
+        const float ginv = a.gamma / w00;
+        const int pm_ = a.L + tid / a.B, pn_ = a.L + tid % a.B;
+        float acc = 0.f, gr = 0.f, gi = 0.f;
+        bool herm = true, flagged = false;
+        int pu = 0, pv = 0, it = 0;
+        for (; it < a.iterations; ++it) {
+            uint32_t m1, m2;
+            const float4 *up = ub + (32 + 16 * h - (pu & 31)) * 64 + ((v - pv) & 63);
+            const bool swap = pu >= 32;
+            if (it == 0)
+                pass64<GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+            else if (herm)
+                swap ? pass64<GUARD, true, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
+                     : pass64<GUARD, true, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+            else
+                swap ? pass64<GUARD, false, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
+                     : pass64<GUARD, false, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+            // phase 1: in-warp argmax, coefficient of the warp's best bin
+            const uint32_t kw = __reduce_max_sync(0xffffffffu, m1);
+            const int wl = __ffs(__ballot_sync(0xffffffffu, m1 == kw)) - 1;
+            const uint32_t k2w = GUARD ? __reduce_max_sync(0xffffffffu, lane == wl ? m2 : m1) : 0u;
+            const int ur = 63 - (int)(kw & 63u);
+            float4 q;
+            switch ((ur & 31) & 15) {
+#define FSR_PK64(j) \
+    case j: q = make_float4(re[j].x, re[j].y, im[j].x, im[j].y); break;
+                FSR_PK64(0) FSR_PK64(1) FSR_PK64(2) FSR_PK64(3) FSR_PK64(4) FSR_PK64(5) FSR_PK64(6)
+                FSR_PK64(7) FSR_PK64(8) FSR_PK64(9) FSR_PK64(10) FSR_PK64(11) FSR_PK64(12) FSR_PK64(13)
+                FSR_PK64(14)
+                default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); break;
+#undef FSR_PK64
+            }
+            float cre = ur < 32 ? q.x : q.y, cim = ur < 32 ? q.z : q.w;
+            cre = __shfl_sync(0xffffffffu, cre, wl);
+            cim = __shfl_sync(0xffffffffu, cim, wl);
+            C64Slot *sl = sm.slot[it & 1];
+            if (lane == 0) {
+                sl[wid].k1 = kw;
+                sl[wid].k2 = k2w;
+                sl[wid].cre = cre;
+                sl[wid].cim = cim;
+                sl[wid].lane = wl;
+            }
+            __syncthreads();
+            // phase 2: across the 4 warps (max key, then lowest warp = lowest tid)
+            uint32_t best = sl[0].k1, second = sl[0].k2;
+            int bw = 0;
+#pragma unroll
+            for (int w = 1; w < 4; ++w) {
+                const uint32_t k = sl[w].k1;
+                if (k > best) {
+                    second = max(best, max(second, sl[w].k2));
+                    best = k;
+                    bw = w;
+                } else {
+                    second = max(second, k);
+                }
+            }
+            const int bu = 63 - (int)(best & 63u);
+            const int bv = (bw * 32 + sl[bw].lane) & 63;
+            const float b1 = __uint_as_float(best & ~63u);
+            if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
+            if (b1 < thr) {
+                if (GUARD && b1 >= thr * one_minus_tau) flagged = true;
+                break;
+            }
+            gr = sl[bw].cre * ginv;
+            gi = sl[bw].cim * ginv;
+            pu = bu;
+            pv = bv;
+            if (GUARD) {
+                const float b2 = __uint_as_float(second & ~63u);
+                flagged |= b2 >= b1 * one_minus_tau;
+                flagged |= b1 * one_minus_tau < thr;
+            }
+            if (herm) herm = ((bu & 31) == 0) && ((bv & 31) == 0);
+            const float2 e = sm.cs[(bu * pm_ + bv * pn_) & 63];
+            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+        }
+        const int done = it;
+        if (sel_b)
+            for (int jj = done + tid; jj < a.iterations; jj += C64_THREADS) sel_b[jj] = -1;
+        if (tid == 0) {
+            if (a.done) a.done[bid] = done;
+            if (GUARD && flagged && a.rerun_list) {
+                unsigned slot = atomicAdd(a.rerun_count, 1u);
+                a.rerun_list[slot] = (int32_t)bid;
+            }
+        }
+        if (tid < a.B * a.B) {
+            const int m = tid / a.B, n = tid % a.B;
+            const int64_t y = r0 + m, xx = c0 + n;
+            if (y < a.H && xx < a.W)
+                a.out[y * a.out_pitch + xx] = a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+        }
+        __syncthreads();  // the region is rewritten by the next block's gather
+    }
+}
+
+}  // namespace fsr

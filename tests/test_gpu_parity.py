@@ -236,7 +236,7 @@ def test_device_api_matches_host_api():
     assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
 
 
-@pytest.mark.parametrize("support", [32, 16])
+@pytest.mark.parametrize("support", [32, 16, 64])
 @pytest.mark.parametrize("shape", [(96, 128), (1080 // 8, 1920 // 8)])
 def test_tma_gather_matches_plain_loads(monkeypatch, shape, support):
     """The N=32 fp32 kernel gathers each 32x32 window with 2-D TMA (zero fill
@@ -253,7 +253,8 @@ def test_tma_gather_matches_plain_loads(monkeypatch, shape, support):
         monkeypatch.setenv("FSR_NO_TMA", no_tma)
         eng = _lib.Engine([0])
         for precision in ("fp32", "fp32_unguarded"):
-            p = _lib.make_params(4, (support - 4) // 2, 100, precision=precision, argmax="redux")
+            p = _lib.make_params(4, (support - 4) // 2, 100, precision=precision, argmax="redux",
+                                 reducer="linear" if support == 64 else "tree")
             out = np.zeros_like(px)
             eng.reconstruct_rows(px, m8, p, 0, (H + 3) // 4, out)
             outs[no_tma, precision] = (out, eng.last_stats()["flags"])
@@ -334,3 +335,17 @@ def test_psnr_device_matches_reference():
     assert abs(r.psnr_db - want) <= 1e-9 * abs(want)
     same = psnr_device(torch.tensor(ref32, device="cuda"), torch.tensor(ref32, device="cuda"))
     assert same.identical and same.psnr_db == float("inf")
+
+
+def test_support64_fp32_kernel_matches_oracle():
+    """The N=64 CTA kernel (linear reducer only: beyond the reference's S^2 <= 1024
+    cap): guarded fp32 within the production tolerance of the
+    reference restatement, known pixels exact."""
+    img = oracle.synthetic_frame(72, 80, 23)
+    sampled, mask = oracle.quarter_sample(img, 9)
+    ref = oracle.reconstruct_image(sampled, mask, 4, 30, 60, 0.7, 0.5, "linear")
+    out = fsr.reconstruct(sampled.astype(np.float32), mask, 4, 64, 60, reducer="linear",
+                          precision="fp32", argmax="redux").astype(np.float64)
+    assert float(np.abs(out - ref).max()) <= FP32_TOL
+    assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
+    assert np.array_equal(out[mask], sampled[mask].astype(np.float32).astype(np.float64))
