@@ -77,7 +77,8 @@ def main():
                         "mpixel_per_s": H * W / (frame_ms * 1e-3) / 1e6,
                         "rerun_fraction": stats["rerun_blocks"] / max(1, rows * bcols),
                         "kernel": {(32, False): "warp32 (+pair64 re-runs)", (32, True): "pair64",
-                                   (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d"}
+                                   (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d",
+                                   (64, False): "cta64, in-warp redux (+generic fp64 re-runs)"}
                                   .get((N, args.precision == "fp64"), "generic")}
                 print(json.dumps(line), flush=True)
 
