@@ -126,8 +126,8 @@ __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const
         const float2 mag = __ffma2_rn(r, r, __fmul2_rn(m, m));
         const float2 o = __fmul2_rn(mag, wf2[i]);
         const uint32_t u = (uint32_t)(16 * h + i);  // h is uniform per warp
-        uint32_t ka = (f2u(o.x) & hmask) | (63u - u);
-        uint32_t kb = (f2u(o.y) & hmask) | (31u - u);  // row u + 32: 63 - (u + 32)
+        uint32_t ka = and_or(f2u(o.x), hmask, 63u - u);
+        uint32_t kb = and_or(f2u(o.y), hmask, 31u - u);  // row u + 32: 63 - (u + 32)
         if (HERM && GUARD) {
             ka = ((canon >> i) & 1u) ? ka : 0u;
             kb = ((canon >> (i + 16)) & 1u) ? kb : 0u;

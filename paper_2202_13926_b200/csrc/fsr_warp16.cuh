@@ -82,8 +82,8 @@ __device__ __forceinline__ void pass16(float2 (&re)[4], float2 (&im)[4], const f
         const float2 o = __fmul2_rn(mag, wf2[i]);
         const uint32_t rka = TREE ? bitrev3(i) : (uint32_t)i;          // j = i
         const uint32_t rkb = TREE ? bitrev3(i + 4) : (uint32_t)(i + 4); // j = i + 4
-        uint32_t ka = (f2u(o.x) & hmask) | (31u ^ rka);
-        uint32_t kb = (f2u(o.y) & hmask) | (31u ^ rkb);
+        uint32_t ka = and_or(f2u(o.x), hmask, 31u ^ rka);
+        uint32_t kb = and_or(f2u(o.y), hmask, 31u ^ rkb);
         if (HERM && GUARD) {
             ka = ((canon >> i) & 1u) ? ka : 0u;
             kb = ((canon >> (i + 4)) & 1u) ? kb : 0u;

@@ -152,20 +152,28 @@ __device__ __forceinline__ int ucol(int c) {
     return TREE ? (((c & 3) << 3) | (c >> 2)) : c;
 }
 __device__ __forceinline__ uint32_t umax3(uint32_t a, uint32_t b, uint32_t c) { return max(max(a, b), c); }
+// (a & m) | c as ONE LOP3 (ptxas otherwise sometimes splits it when m is a register)
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t m, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(m), "r"(c));
+    return d;
+}
 
-// (Re, Im) of R[u][lane] for a warp-uniform dynamic u (uniform branches only).
-__device__ __forceinline__ float2 pick_pair(const float2 (&re)[16], const float2 (&im)[16], int u) {
+// Row pair (u mod 16, u mod 16 + 16) of this lane for a warp-uniform dynamic u
+// (uniform branches only): q = (Re lo, Re hi, Im lo, Im hi), wfp = (wf lo, wf hi).
+__device__ __forceinline__ float4 pick_pair(const float2 (&re)[16], const float2 (&im)[16],
+                                            const float2 (&wf2)[16], int u, float2 &wfp) {
     float4 q;
     switch (u & 15) {
 #define FSR_PICK(i) \
-    case i: q = make_float4(re[i].x, re[i].y, im[i].x, im[i].y); break;
+    case i: q = make_float4(re[i].x, re[i].y, im[i].x, im[i].y); wfp = wf2[i]; break;
         FSR_PICK(0) FSR_PICK(1) FSR_PICK(2) FSR_PICK(3) FSR_PICK(4) FSR_PICK(5) FSR_PICK(6)
         FSR_PICK(7) FSR_PICK(8) FSR_PICK(9) FSR_PICK(10) FSR_PICK(11) FSR_PICK(12)
         FSR_PICK(13) FSR_PICK(14)
-        default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); break;
+        default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); wfp = wf2[15]; break;
 #undef FSR_PICK
     }
-    return u < 16 ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
+    return q;
 }
 
 // Cross-lane argmax on (key desc, lane asc).  Lanes hold spectral columns in
@@ -217,6 +225,8 @@ __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int
 //   UPDATE: apply R -= gp * W(. - pu, . - pv) first (fused residual update)
 //   SWAP:   pu >= 16, the U float4 halves are exchanged
 //   HERM:   the state is exactly Hermitian; keys of non-canonical bins are zeroed
+//   m1:     the lane's best key; m2 (GUARD): the second largest of the lane's 16
+//           row-pair maxima
 //   hmask:  ~31, passed in from a kernel argument so that ptxas keeps it in a
 //           register: with both constants immediate it splits the key
 //           formation (o & ~31) | c into two LOP3s
@@ -226,6 +236,7 @@ __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], cons
                                         uint32_t hmask, uint32_t &m1, uint32_t &m2) {
     m1 = 0;
     m2 = 0;
+    uint32_t hpend = 0;
     const float2 ngr = make_float2(-gr, -gr), pgi = make_float2(gi, gi), ngi = make_float2(-gi, -gi);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -248,16 +259,24 @@ __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], cons
         const uint32_t rka = TREE ? ((i & 1) << 4 | (i & 2) << 2 | (i & 4) | (i & 8) >> 2) : (uint32_t)i;
         const uint32_t rkb = TREE ? (rka | 1u) : (uint32_t)(i + 16);
         // low 5 bits = 31 - rank(u)
-        uint32_t ka = (f2u(o.x) & hmask) | (31u ^ rka);
-        uint32_t kb = (f2u(o.y) & hmask) | (31u ^ rkb);
+        uint32_t ka = and_or(f2u(o.x), hmask, 31u ^ rka);
+        uint32_t kb = and_or(f2u(o.y), hmask, 31u ^ rkb);
         if (HERM && GUARD) {
             ka = ((canon >> i) & 1u) ? ka : 0u;
             kb = ((canon >> (i + 16)) & 1u) ? kb : 0u;
         }
         if (GUARD) {
-            const uint32_t hi = max(ka, kb), lo = min(ka, kb);
-            m2 = umax3(m2, lo, min(m1, hi));
-            m1 = max(m1, hi);
+            // top-2 over the 16 PAIR maxima, two pairs per step (3.5 ops per pair); the
+            // lane's true runner-up is max(m2, partner of the best bin), and the caller
+            // recomputes that partner for the winning lane only (pass_x2 contract)
+            const uint32_t h = max(ka, kb);
+            if ((i & 1) == 0) {
+                hpend = h;
+            } else {
+                const uint32_t hmax = max(hpend, h), hmin = min(hpend, h);
+                m2 = umax3(m2, hmin, min(m1, hmax));
+                m1 = max(m1, hmax);
+            }
         } else {
             m1 = umax3(m1, ka, kb);
         }
@@ -520,7 +539,10 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
                 if (GUARD && b1 >= thr * one_minus_tau) flagged = true;  // a stop decision within tau
                 break;
             }
-            float2 c = pick_pair(re, im, bu);
+            float2 wfp;
+            const float4 q = pick_pair(re, im, wf2, bu, wfp);
+            const bool lo = bu < 16;
+            float2 c = lo ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             gr = c.x * ginv;
@@ -528,8 +550,16 @@ __global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
             pu = bu;
             pv = bv;
             if (GUARD) {
-                // second-best objective: the winner lane's runner-up or any other lane's best
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
+                // second-best objective: any other lane's best, or the winner lane's
+                // runner-up = max(its second pair maximum, the winner's pair partner);
+                // the partner's key is recomputed exactly as the pass computed it
+                const int up_row = bu ^ 16;
+                const float pre = lo ? q.y : q.x, pim = lo ? q.w : q.z, pwf = lo ? wfp.y : wfp.x;
+                const float po = fmaf(pre, pre, pim * pim) * pwf;
+                const uint32_t prk = TREE ? bitrev5((uint32_t)up_row) : (uint32_t)up_row;
+                uint32_t kp = (f2u(po) & a.key_mask) | (31u ^ prk);
+                if (herm && !((canon >> up_row) & 1u)) kp = 0u;
+                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 flagged |= b2 >= b1 * one_minus_tau;
                 // a continue decision within tau of the stop threshold is ambiguous too
