@@ -464,7 +464,7 @@ def main():
     traffic, traffic_src = None, None
     if (kernel == "warp32_kernel" and args.workload == "4k" and world == 1
             and args.precision == "fp32" and args.reducer == "tree" and args.argmax == "redux"):
-        traffic = ncu_traffic("void warp32_kernel<4, 1, 2, 1, 0>")
+        traffic = ncu_traffic("void warp32_kernel<4, 1, 2, 1, 0")
         if traffic is not None:
             traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                            "(profiles/r01/warp32_ncu.json); algorithmic I/O bytes " + str(io_bytes))
