@@ -349,3 +349,37 @@ def test_support64_fp32_kernel_matches_oracle():
     assert float(np.abs(out - ref).max()) <= FP32_TOL
     assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
     assert np.array_equal(out[mask], sampled[mask].astype(np.float32).astype(np.float64))
+
+
+EDGE_CASES = [(32, 4, "tree"), (32, 2, "linear"), (16, 4, "linear"), (16, 2, "tree"), (64, 4, "linear")]
+
+
+@pytest.mark.parametrize("early_stop", [False, True])
+@pytest.mark.parametrize("N,B,reducer", EDGE_CASES)
+def test_register_kernels_edges(N, B, reducer, early_stop):
+    """Every register kernel (warp32, warp16/warp16d, cta64) on a frame whose
+    height is not a multiple of B (truncated bottom target blocks), whose
+    width is 16-aligned (TMA gather on) and which has a 26x26 unsampled hole
+    (empty-support windows for N=16 -> mean fill, reconstruction.py:272-275),
+    with and without early stop, in fp32 (guarded) and fp64."""
+    H, W, I = 50, 80, 60
+    img = oracle.synthetic_frame(H, W, 31)
+    sampled, mask = oracle.quarter_sample(img, 12)
+    mask[10:36, 20:46] = False
+    sampled = np.where(mask, sampled, 0.0)
+    L = (N - B) // 2
+    ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, reducer, early_stop)
+    # the fp32 path takes f32 pixels: compare it with the reference on the SAME
+    # (f32-representable) inputs -- this frame has a block (N=16, B=2) whose
+    # greedy path hinges on a 3e-8 relative near-tie, below the f32 input rounding
+    s32 = sampled.astype(np.float32)
+    ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer, early_stop)
+    out32 = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer,
+                            early_stop=early_stop, precision="fp32", argmax="redux")
+    err = float(np.abs(out32.astype(np.float64) - ref32).max())
+    assert err <= FP32_TOL, err
+    out64, tr = fsr.reconstruct(sampled, mask, B, N, I, reducer=reducer, early_stop=early_stop,
+                                precision="fp64", argmax="redux", return_trace=True)
+    oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, 0.7, 0.5, reducer,
+                                    tr.selections, FP64_TOL)
+    assert np.array_equal(out64[mask], sampled[mask])
