@@ -13,11 +13,12 @@
         = the traced per-block path (reconstruction.py:138-209); transforms on
           the host with numpy.fft as the reference does, the loop on the GPU.
 
-Precision modes: "fp64" (default; production and validation: the whole path in
-fp64, the N=32 case on the warp-pair register kernel), "fp32" (fp32 loop with
-blocks whose greedy decisions were near-tied re-run in fp64) and
-"fp32_unguarded" (pure fp32 ablation).  DESIGN.md §4 explains why fp32 cannot
-meet the 1e-3 pixel tolerance on this algorithm.  There is no CPU fallback.
+Precision modes: "fp64" (default: the reference's arithmetic, the validation
+mode -- N=32 on the warp-pair register kernel, N=16 on warp16d), "fp32" (the
+production mode: fp32 register loop with the near-tie guard, blocks whose
+greedy decisions were near-tied re-run in fp64; within the north-star
+tolerance) and "fp32_unguarded" (pure fp32 ablation: PSNR
+close, max |error| not bounded).  There is no CPU fallback.
 """
 
 from __future__ import annotations
