@@ -439,8 +439,11 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 // production launches without them carry no per-iteration checks for either.
 constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_ALL = 3;
 
+#ifndef FSR_W32_WARPS_PER_SM
+#define FSR_W32_WARPS_PER_SM 12  // resident warps (blocks) per SM the register budget targets
+#endif
 template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY, int OPTS = W32_ALL>
-__global__ void __launch_bounds__(WARPS * 32, 12 / WARPS)
+__global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
