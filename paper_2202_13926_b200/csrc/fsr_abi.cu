@@ -427,10 +427,10 @@ int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32M
     return fail(eng, FSR_EINVAL, "unknown argmax implementation");
 }
 
-template <int WARPS, bool TREE, int AM, bool GUARD>
+template <int WARPS, bool TREE, int AM, bool GUARD, int OPTS = W32_ALL>
 int launch_warp16_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
                     cudaStream_t st) {
-    auto k = warp16_kernel<WARPS, TREE, AM, GUARD>;
+    auto k = warp16_kernel<WARPS, TREE, AM, GUARD, OPTS>;
     const size_t smem = sizeof(Warp16Smem<WARPS>);
     CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -447,6 +447,12 @@ int launch_warp16_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp3
 
 int launch_warp16(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps, bool tree,
                   int am, bool guard, cudaStream_t st) {
+    if (am == AM_REDUX && !a.sel && !a.early_stop) {  // production: no trace / early-stop checks
+        if (tree) return guard ? launch_warp16_t<kWarps, true, AM_REDUX, true, 0>(eng, d, a, maps, st)
+                               : launch_warp16_t<kWarps, true, AM_REDUX, false, 0>(eng, d, a, maps, st);
+        return guard ? launch_warp16_t<kWarps, false, AM_REDUX, true, 0>(eng, d, a, maps, st)
+                     : launch_warp16_t<kWarps, false, AM_REDUX, false, 0>(eng, d, a, maps, st);
+    }
 #define FSR_W16(T, A, G) \
     if (tree == T && am == A && guard == G) return launch_warp16_t<kWarps, T, A, G>(eng, d, a, maps, st);
     FSR_W16(true, AM_SHFL, true) FSR_W16(true, AM_SHFL, false)

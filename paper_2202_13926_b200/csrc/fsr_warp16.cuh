@@ -215,9 +215,10 @@ __device__ __forceinline__ double w16_prologue(const Warp32Args &a, const Warp32
     return energy;
 }
 
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD>
+template <int WARPS, bool TREE, int ARGMAX, bool GUARD, int OPTS = W32_ALL>
 __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
     warp16_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
+    constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp16Smem<WARPS> &sm = *reinterpret_cast<Warp16Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
         const float energy =
             (float)w16_prologue<TREE>(a, maps, ub, bar, phase, re, im, r0 - a.L, c0 - a.L, lane, v, p);
         const float w00 = ub[8 * W16_US].x;  // U16[8][0].x = Wx[0][0] = sum of the weights
-        int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        int32_t *sel_b = (TRACE && a.sel) ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
             if (lane == 0) {
                 unsigned slot = atomicAdd(a.empty_count, 1u);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             continue;
         }
         float thr = 0.f;
-        if (a.early_stop) {
+        if (EARLY && a.early_stop) {
             float e = energy;
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
@@ -304,8 +305,8 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             const int bu = (wl & 1) + 2 * j;
             const int bv = TREE ? (int)bitrev4((uint32_t)(wl >> 1)) : (wl >> 1);
             const float b1 = __uint_as_float(kmax & ~31u);
-            if (sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
-            if (b1 < thr) {
+            if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
+            if (EARLY && b1 < thr) {
                 if (GUARD && b1 >= thr * one_minus_tau) flagged = true;
                 break;
             }
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 flagged |= b2 >= b1 * one_minus_tau;
-                flagged |= b1 * one_minus_tau < thr;
+                if (EARLY) flagged |= b1 * one_minus_tau < thr;
             }
             if (herm) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
             const float2 e = sm.cs[(bu * pm + bv * pn) & 15];
