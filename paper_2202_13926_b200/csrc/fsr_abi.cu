@@ -89,6 +89,10 @@ struct Device {
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
     bool tma_enabled = true;     // warp32 window gather by TMA when the rows allow it
     int used_tma = 0;            // last warp32 launch gathered by TMA
+    // host-buffer calls on large strips are pipelined over two "lanes" (same GPU,
+    // own stream, staging buffers and scratch): H2D of chunk c+1 and D2H of chunk
+    // c-1 overlap the kernels of chunk c
+    std::vector<std::unique_ptr<Device>> lanes;
 };
 
 }  // namespace
@@ -535,15 +539,21 @@ template <typename IO>
 int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, int64_t px_pitch,
                   const uint8_t *mask, int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H,
                   int64_t W, int64_t row0, int64_t row1, int32_t *sel, int32_t *done,
-                  bool device_fill, double host_fill, cudaStream_t st) {
+                  bool device_fill, double host_fill, cudaStream_t st,
+                  Counters *ctr_in = nullptr, int32_t *empty_in = nullptr) {
     const int N = p->block + 2 * p->border;
     const int64_t bcols = (W + p->block - 1) / p->block;
     const int64_t first = row0 * bcols, nblocks = (row1 - row0) * bcols;
     if (nblocks <= 0) return FSR_OK;
-    CUDA_TRY(eng, d.counters.ensure(sizeof(Counters)));
-    CUDA_TRY(eng, d.empty_list.ensure((size_t)nblocks * sizeof(int32_t)));
-    CUDA_TRY(eng, cudaMemsetAsync(d.counters.p, 0, sizeof(Counters), st));
-    Counters *ctr = d.counters.as<Counters>();
+    Counters *ctr = ctr_in;
+    int32_t *empty_list = empty_in;
+    if (!ctr) {  // the device's own scratch (otherwise the caller's per-chunk slot)
+        CUDA_TRY(eng, d.counters.ensure(sizeof(Counters)));
+        CUDA_TRY(eng, d.empty_list.ensure((size_t)nblocks * sizeof(int32_t)));
+        ctr = d.counters.as<Counters>();
+        empty_list = d.empty_list.as<int32_t>();
+    }
+    CUDA_TRY(eng, cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
     const int gen_grid = d.sms * 8;
@@ -557,7 +567,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
-                                               &ctr->empty_count, d.empty_list.as<int32_t>());
+                                               &ctr->empty_count, empty_list);
             if ((rc = launch_fp64_n32<IO>(eng, d, a, p, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
         } else if (p->precision == FSR_PREC_FP64 && warp16d_eligible(p)) {
@@ -565,7 +575,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
-                                               &ctr->empty_count, d.empty_list.as<int32_t>());
+                                               &ctr->empty_count, empty_list);
             if ((rc = launch_warp16d<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          nblocks, st)))
                 return rc;
@@ -577,7 +587,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                     p->block, p->border, N, p->iterations, bcols, first, nblocks,
                                     nullptr, nullptr, p->gamma, p->reducer == FSR_REDUCER_TREE,
                                     p->early_stop, tab, sel, done, &ctr->empty_count,
-                                    d.empty_list.as<int32_t>()};
+                                    empty_list};
             if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
         } else {
@@ -592,7 +602,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                        p->block, p->border, N, p->iterations, bcols, first,
                                        nblocks, nullptr, nullptr, (float)p->gamma,
                                        p->reducer == FSR_REDUCER_TREE, p->early_stop, tf, sel,
-                                       done, &ctr->empty_count, d.empty_list.as<int32_t>()};
+                                       done, &ctr->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
                 CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
             } else {
@@ -600,7 +610,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                         p->block, p->border, N, p->iterations, bcols, first,
                                         nblocks, nullptr, nullptr, p->gamma,
                                         p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel,
-                                        done, &ctr->empty_count, d.empty_list.as<int32_t>()};
+                                        done, &ctr->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
                 CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
             }
@@ -633,29 +643,39 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.sel = sel;
         a.done = done;
         a.empty_count = &ctr->empty_count;
-        a.empty_list = d.empty_list.as<int32_t>();
+        a.empty_list = empty_list;
         a.rerun_count = &ctr->rerun_count;
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
         a.gap_out = d.gap_debug ? d.gap_debug - 2 * first : nullptr;
         a.key_mask = 0xffffffe0u;
         Warp32Maps maps;
         std::memset(&maps, 0, sizeof(maps));
+        // the maps start at the first row this call reads, not at the virtual
+        // row-0 pointer: a tensor map's base must be a real address of the
+        // buffer (a base below the allocation faults), and zero fill at the
+        // map's edges is still exactly the image's edges, because the strip's
+        // rows only end early where the image does
+        const int64_t ty0 = std::max<int64_t>(0, row0 * p->block - p->border);
+        const int64_t ty1 = std::min<int64_t>(H, row1 * p->block + p->border);
+        a.tma_y0 = (int)ty0;
+        const float *tpx = a.px + ty0 * px_pitch;
+        const uint8_t *tmk = mask + ty0 * mask_pitch;
         if (fast64) {
             a.key_mask = 0xffffffc0u;  // 6 rank bits (row u of 64)
-            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps,
+            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps,
                                                       C64_BOX_PX, C64_BOX_MK, 64)) ? 1 : 0;
             d.used_tma = a.use_tma;
             rc = guarded ? launch_cta64_t<true>(eng, d, a, maps, st) : launch_cta64_t<false>(eng, d, a, maps, st);
             if (rc) return rc;
         } else if (fast16) {
-            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps,
+            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps,
                                                       W16_BOX_PX, W16_BOX_MK, 16)) ? 1 : 0;
             d.used_tma = a.use_tma;
             if ((rc = launch_warp16(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                     guarded, st)))
                 return rc;
         } else {
-            a.use_tma = (d.tma_enabled && warp32_maps(a.px, px_pitch, mask, mask_pitch, H, W, &maps)) ? 1 : 0;
+            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps)) ? 1 : 0;
             d.used_tma = a.use_tma;
             if ((rc = launch_warp32(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                     guarded || d.gap_debug != nullptr, st)))
@@ -703,13 +723,13 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         d.launches++;
         CUDA_TRY(eng, cudaGetLastError());
         fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
-                                                      d.empty_list.as<int32_t>(),
+                                                      empty_list,
                                                       &ctr->empty_count, &ctr->fill, 0.0);
         d.launches++;
         CUDA_TRY(eng, cudaGetLastError());
     } else if (host_fill == host_fill) {  // not NaN: fill value known on the host
         fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
-                                                      d.empty_list.as<int32_t>(),
+                                                      empty_list,
                                                       &ctr->empty_count, nullptr, host_fill);
         d.launches++;
         CUDA_TRY(eng, cudaGetLastError());
@@ -757,62 +777,110 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         q.oa = std::min<int64_t>(H, q.row0 * B);
         q.ob = std::min<int64_t>(H, q.row1 * B);
     }
+    // per device: the strip's block rows in K chunks (K = 1 for small strips), chunk c
+    // on lane c % 2 -- copies of one chunk overlap the kernels of the other
+    std::vector<int> nchunks(nd, 0);
     for (int g = 0; g < nd; ++g) {
         Device &d = *eng->devs[g];
         const Part &q = parts[g];
         if (q.row1 <= q.row0) continue;
         if ((rc = select_device(eng, d))) return rc;
+        const int64_t prow = q.row1 - q.row0;
+        const int K = d.gap_debug ? 1 : (int)std::min<int64_t>(4, std::max<int64_t>(1, prow / 64));
+        nchunks[g] = K;
+        if (K > 1 && d.lanes.empty()) {
+            for (int l = 0; l < 2; ++l) {
+                auto ln = std::make_unique<Device>();
+                ln->id = d.id;
+                ln->sms = d.sms;
+                ln->tma_enabled = d.tma_enabled;
+                CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
+                CUDA_TRY(eng, cudaEventCreate(&ln->ev0));
+                CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
+                CUDA_TRY(eng, cudaEventCreate(&ln->ev_mid));
+                d.lanes.push_back(std::move(ln));
+            }
+        }
         d.launches = 0;
-        const int64_t rows_in = q.yb - q.ya, rows_out = q.ob - q.oa;
-        CUDA_TRY(eng, d.px.ensure((size_t)rows_in * W * sizeof(IO)));
-        CUDA_TRY(eng, d.mask.ensure((size_t)rows_in * W));
-        CUDA_TRY(eng, d.out.ensure((size_t)rows_out * W * sizeof(IO)));
-        const int64_t nb = (q.row1 - q.row0) * bcols;
-        if (sel) CUDA_TRY(eng, d.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
-        if (done) CUDA_TRY(eng, d.done.ensure((size_t)nb * sizeof(int32_t)));
-        CUDA_TRY(eng, cudaMemcpyAsync(d.px.p, px + q.ya * W, (size_t)rows_in * W * sizeof(IO),
-                                      cudaMemcpyHostToDevice, d.stream));
-        CUDA_TRY(eng, cudaMemcpyAsync(d.mask.p, mask + q.ya * W, (size_t)rows_in * W,
-                                      cudaMemcpyHostToDevice, d.stream));
-        CUDA_TRY(eng, cudaEventRecord(d.ev0, d.stream));
-        const IO *vpx = d.px.as<IO>() - q.ya * W;
-        const uint8_t *vmask = d.mask.as<uint8_t>() - q.ya * W;
-        IO *vout = d.out.as<IO>() - q.oa * W;
-        int32_t *vsel = sel ? d.sel.as<int32_t>() - q.row0 * bcols * it_stride : nullptr;
-        int32_t *vdone = done ? d.done.as<int32_t>() - q.row0 * bcols : nullptr;
-        rc = enqueue_image<IO>(eng, d, p, vpx, W, vmask, W, vout, W, H, W, q.row0, q.row1, vsel,
-                               vdone, false, NAN, d.stream);
-        if (rc) return rc;
-        CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
-        CUDA_TRY(eng, cudaMemcpyAsync(out + q.oa * W, d.out.p, (size_t)rows_out * W * sizeof(IO),
-                                      cudaMemcpyDeviceToHost, d.stream));
-        if (sel)
-            CUDA_TRY(eng, cudaMemcpyAsync(sel + q.row0 * bcols * it_stride, d.sel.p,
-                                          (size_t)nb * it_stride * sizeof(int32_t),
-                                          cudaMemcpyDeviceToHost, d.stream));
-        if (done)
-            CUDA_TRY(eng, cudaMemcpyAsync(done + q.row0 * bcols, d.done.p, (size_t)nb * sizeof(int32_t),
-                                          cudaMemcpyDeviceToHost, d.stream));
+        const int64_t nb_part = prow * bcols;
+        CUDA_TRY(eng, d.counters.ensure((size_t)K * sizeof(Counters)));
+        CUDA_TRY(eng, d.empty_list.ensure((size_t)nb_part * sizeof(int32_t)));
+        // the first lane's stream starts the clock for the whole strip
+        cudaStream_t st0 = K > 1 ? d.lanes[0]->stream : d.stream;
+        CUDA_TRY(eng, cudaEventRecord(d.ev0, st0));
+        for (int c = 0; c < K; ++c) {
+            Device &ld = K > 1 ? *d.lanes[c % 2] : d;
+            if (K > 1) ld.launches = c < 2 ? 0 : ld.launches;
+            const int64_t r0 = q.row0 + prow * c / K, r1 = q.row0 + prow * (c + 1) / K;
+            const int64_t ya = std::max<int64_t>(0, r0 * B - L), yb = std::min<int64_t>(H, r1 * B + L);
+            const int64_t oa = std::min<int64_t>(H, r0 * B), ob = std::min<int64_t>(H, r1 * B);
+            const int64_t rows_in = yb - ya, rows_out = ob - oa, nb = (r1 - r0) * bcols;
+            CUDA_TRY(eng, ld.px.ensure((size_t)rows_in * W * sizeof(IO)));
+            CUDA_TRY(eng, ld.mask.ensure((size_t)rows_in * W));
+            CUDA_TRY(eng, ld.out.ensure((size_t)rows_out * W * sizeof(IO)));
+            if (sel) CUDA_TRY(eng, ld.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
+            if (done) CUDA_TRY(eng, ld.done.ensure((size_t)nb * sizeof(int32_t)));
+            CUDA_TRY(eng, cudaMemcpyAsync(ld.px.p, px + ya * W, (size_t)rows_in * W * sizeof(IO),
+                                          cudaMemcpyHostToDevice, ld.stream));
+            CUDA_TRY(eng, cudaMemcpyAsync(ld.mask.p, mask + ya * W, (size_t)rows_in * W,
+                                          cudaMemcpyHostToDevice, ld.stream));
+            if (K > 1) CUDA_TRY(eng, cudaEventRecord(ld.ev0, ld.stream));
+            const IO *vpx = ld.px.as<IO>() - ya * W;
+            const uint8_t *vmask = ld.mask.as<uint8_t>() - ya * W;
+            IO *vout = ld.out.as<IO>() - oa * W;
+            int32_t *vsel = sel ? ld.sel.as<int32_t>() - r0 * bcols * it_stride : nullptr;
+            int32_t *vdone = done ? ld.done.as<int32_t>() - r0 * bcols : nullptr;
+            rc = enqueue_image<IO>(eng, ld, p, vpx, W, vmask, W, vout, W, H, W, r0, r1, vsel, vdone,
+                                   false, NAN, ld.stream, d.counters.as<Counters>() + c,
+                                   d.empty_list.as<int32_t>() + (r0 - q.row0) * bcols);
+            if (rc) return rc;
+            if (K == 1) CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
+            CUDA_TRY(eng, cudaMemcpyAsync(out + oa * W, ld.out.p, (size_t)rows_out * W * sizeof(IO),
+                                          cudaMemcpyDeviceToHost, ld.stream));
+            if (sel)
+                CUDA_TRY(eng, cudaMemcpyAsync(sel + r0 * bcols * it_stride, ld.sel.p,
+                                              (size_t)nb * it_stride * sizeof(int32_t),
+                                              cudaMemcpyDeviceToHost, ld.stream));
+            if (done)
+                CUDA_TRY(eng, cudaMemcpyAsync(done + r0 * bcols, ld.done.p, (size_t)nb * sizeof(int32_t),
+                                              cudaMemcpyDeviceToHost, ld.stream));
+            if (K > 1) CUDA_TRY(eng, cudaEventRecord(ld.ev1, ld.stream));
+            if (K > 1 && c >= K - 2) d.launches += ld.launches;
+            d.used_tma = ld.used_tma;
+        }
     }
     unsigned empty_total = 0;
-    std::vector<Counters> ctrs(nd);
+    std::vector<std::vector<Counters>> ctrs(nd);
     for (int g = 0; g < nd; ++g) {
         Device &d = *eng->devs[g];
-        if (parts[g].row1 <= parts[g].row0) continue;
+        const int K = nchunks[g];
+        if (K == 0) continue;
         if ((rc = select_device(eng, d))) return rc;
-        CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
-        CUDA_TRY(eng, cudaMemcpy(&ctrs[g], d.counters.p, sizeof(Counters), cudaMemcpyDeviceToHost));
-        empty_total += ctrs[g].empty_count;
-        eng->stats.rerun_blocks += ctrs[g].rerun_count;
+        float ms = 0.f, mm = 0.f;
+        if (K > 1) {
+            for (auto &ln : d.lanes) {
+                CUDA_TRY(eng, cudaStreamSynchronize(ln->stream));
+                float t = 0.f;
+                if (cudaEventElapsedTime(&t, d.ev0, ln->ev1) == cudaSuccess) ms = std::max(ms, t);
+            }
+        } else {
+            CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
+            if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+            if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
+        }
+        (void)cudaGetLastError();
+        ctrs[g].resize(K);
+        CUDA_TRY(eng, cudaMemcpy(ctrs[g].data(), d.counters.p, (size_t)K * sizeof(Counters),
+                                 cudaMemcpyDeviceToHost));
+        for (const Counters &c : ctrs[g]) {
+            empty_total += c.empty_count;
+            eng->stats.rerun_blocks += c.rerun_count;
+        }
         eng->stats.kernel_launches += d.launches;
         if (g == 0) {
             eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
-            float ms = 0.f, mm = 0.f;
-            if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
-            if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
-            (void)cudaGetLastError();
             eng->stats.kernel_ms = ms;
-            eng->stats.main_ms = mm;
+            eng->stats.main_ms = mm;  // dominant-kernel time only for an unchunked call
         }
     }
     eng->stats.empty_blocks = empty_total;
@@ -831,16 +899,21 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         for (int g = 0; g < nd; ++g) {
             Device &d = *eng->devs[g];
             const Part &q = parts[g];
-            if (q.row1 <= q.row0 || ctrs[g].empty_count == 0) continue;
-            // host-side fill of the listed blocks (rare path)
-            std::vector<int32_t> list(ctrs[g].empty_count);
+            const int K = nchunks[g];
             if ((rc = select_device(eng, d))) return rc;
-            CUDA_TRY(eng, cudaMemcpy(list.data(), d.empty_list.p, list.size() * sizeof(int32_t),
-                                     cudaMemcpyDeviceToHost));
-            for (int32_t bid : list) {
-                int64_t r0 = (bid / bc) * B, c0 = (bid % bc) * B;
-                for (int64_t y = r0; y < std::min<int64_t>(H, r0 + B); ++y)
-                    for (int64_t x = c0; x < std::min<int64_t>(W, c0 + B); ++x) out[y * W + x] = (IO)fill;
+            for (int c = 0; c < K; ++c) {
+                if (ctrs[g][c].empty_count == 0) continue;
+                // host-side fill of the listed blocks (rare path); chunk c's list
+                // sits at its first block's offset in the strip's empty list
+                const int64_t prow = q.row1 - q.row0, r0c = q.row0 + prow * c / K;
+                std::vector<int32_t> list(ctrs[g][c].empty_count);
+                CUDA_TRY(eng, cudaMemcpy(list.data(), d.empty_list.as<int32_t>() + (r0c - q.row0) * bc,
+                                         list.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+                for (int32_t bid : list) {
+                    int64_t r0 = (bid / bc) * B, c0 = (bid % bc) * B;
+                    for (int64_t y = r0; y < std::min<int64_t>(H, r0 + B); ++y)
+                        for (int64_t x = c0; x < std::min<int64_t>(W, c0 + B); ++x) out[y * W + x] = (IO)fill;
+                }
             }
         }
     }
@@ -935,6 +1008,20 @@ void fsr_engine_destroy(fsr_engine *eng) {
         for (auto &kv : d.tables) {
             kv.second->f64.release();
             kv.second->f32.release();
+        }
+        for (auto &ln : d.lanes) {
+            cudaStreamSynchronize(ln->stream);
+            for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->empty_list,
+                              &ln->rerun_list, &ln->counters})
+                b->release();
+            for (auto &kv : ln->tables) {
+                kv.second->f64.release();
+                kv.second->f32.release();
+            }
+            cudaEventDestroy(ln->ev0);
+            cudaEventDestroy(ln->ev1);
+            cudaEventDestroy(ln->ev_mid);
+            cudaStreamDestroy(ln->stream);
         }
         cudaEventDestroy(d.ev0);
         cudaEventDestroy(d.ev1);

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const float *spx = reinterpret_cast<const float *>(sm.region);
             const uint8_t *smk = sm.region + C64_STAGE_MK;
             if (wid == 0)
-                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0, C64_STAGE_BYTES);
+                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, C64_STAGE_BYTES);
             mbar_wait(bar, phase);
             phase ^= 1u;
             const float *cpx = spx + 32 * h * C64_BOX_PX + (x0 - xp) + v;

@@ -125,7 +125,7 @@ __device__ __forceinline__ double w16_prologue(const Warp32Args &a, const Warp32
         const int xp = x0 & ~3, xm = x0 & ~15;
         const float *spx = reinterpret_cast<const float *>(ub);
         const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + W16_STAGE_MK;
-        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0, W16_STAGE_BYTES);
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, W16_STAGE_BYTES);
         mbar_wait(bar, phase);
         phase ^= 1u;
         const float *cpx = spx + rh * 8 * W16_BOX_PX + (x0 - xp) + cl;

@@ -72,6 +72,7 @@ struct Warp32Args {
     float *gap_out;        // debug: per-block [2] min top-2 gaps (relative, scaled) or null
     uint32_t key_mask;     // 0xffffffe0 (see pass_x2)
     int use_tma;           // gather the window with TMA (needs 16 B aligned rows)
+    int tma_y0;            // image row of the tensor maps' row 0 (maps span only the rows the call reads)
 };
 
 // 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
@@ -314,7 +315,7 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
         const int xp = x0 & ~3, xm = x0 & ~15;  // floor to 16-byte boundaries
         const float *spx = reinterpret_cast<const float *>(ub);
         const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + W32_STAGE_MK;
-        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0);
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0);
         mbar_wait(bar, phase);
         phase ^= 1u;
         const float *cpx = spx + (x0 - xp) + lane;

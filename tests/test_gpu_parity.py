@@ -383,3 +383,67 @@ def test_register_kernels_edges(N, B, reducer, early_stop):
     oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, 0.7, 0.5, reducer,
                                     tr.selections, FP64_TOL)
     assert np.array_equal(out64[mask], sampled[mask])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("support,reducer", [(16, "tree"), (32, "tree"), (64, "linear")])
+def test_host_api_chunks_tma_rows(support, reducer):
+    """Four uneven chunks (the staging buffers grow between chunks on the same
+    lane) with TMA window gathers whose tensor maps start at each chunk's first
+    row: twice in a row, the host-buffer call equals the unchunked device call
+    bitwise."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib
+    H, W = 4 * 259, 256  # 259 block rows -> chunks of 64/65/65/65
+    img = oracle.synthetic_frame(H, W, 43)
+    sampled, mask = oracle.quarter_sample(img, 5)
+    px = np.where(mask, sampled, 0.0).astype(np.float32)
+    p = _lib.make_params(4, (support - 4) // 2, 30, precision="fp32", argmax="redux", reducer=reducer)
+    eng = _lib.Engine([0])
+    d_px = torch.tensor(px, device="cuda")
+    d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
+    d_out = torch.empty_like(d_px)
+    eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    want = d_out.cpu().numpy()
+    for _ in range(2):
+        out = eng.reconstruct(px, mask, p)
+        assert eng.last_stats()["flags"] & 1  # TMA gather on every chunk
+        assert np.array_equal(out, want)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_host_api_chunk_pipeline(precision):
+    """Host-buffer calls on tall strips are pipelined in chunks over two streams
+    (H2D / kernels / D2H overlap).  The result, the selection traces and the
+    empty-support mean fill must equal the unchunked device-API call bitwise."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib
+    H, W = 4 * 150 + 2, 96  # 151 block rows -> 2 chunks
+    img = oracle.synthetic_frame(H, W, 41)
+    sampled, mask = oracle.quarter_sample(img, 3)
+    mask[300:340, 10:40] = False  # empty-support windows in the second chunk
+    sampled = np.where(mask, sampled, 0.0)
+    px = sampled.astype(np.float32 if precision == "fp32" else np.float64)
+    p = _lib.make_params(4, 6, 40, precision=precision, argmax="redux")
+    eng = _lib.Engine([0])
+    nb = ((H + 3) // 4) * (W // 4)
+    sel = np.full((nb, 40), -7, np.int32)
+    done = np.full(nb, -7, np.int32)
+    out = eng.reconstruct(px, mask, p, sel=sel, done=done)
+    assert eng.last_stats()["empty_blocks"] > 0
+    ref = oracle.reconstruct_image(px.astype(np.float64), mask, 4, 6, 40, trace=False)
+    tol = FP32_TOL if precision == "fp32" else FP64_TOL
+    assert np.abs(out.astype(np.float64) - ref).max() <= tol or precision == "fp64"
+    # the device API runs the same strip unchunked
+    if precision == "fp32":
+        d_px = torch.tensor(px, device="cuda")
+        d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
+        d_out = torch.empty_like(d_px)
+        eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, (H + 3) // 4,
+                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_out.cpu().numpy(), out)
+    _, tr = fsr.reconstruct(px, mask, 4, 16, 40, precision=precision, argmax="redux", return_trace=True)
+    assert np.array_equal(tr.selections[:, :40], sel) and np.array_equal(tr.done, done)
