@@ -639,6 +639,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.nblocks = nblocks;
         a.gamma = (float)p->gamma;
         a.tau = (float)p->guard_tau;
+        a.omt = 1.f - a.tau;
         a.wf = tf.wf;
         a.sel = sel;
         a.done = done;

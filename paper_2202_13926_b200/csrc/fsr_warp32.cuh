@@ -73,6 +73,7 @@ struct Warp32Args {
     uint32_t key_mask;     // 0xffffffe0 (see pass_x2)
     int use_tma;           // gather the window with TMA (needs 16 B aligned rows)
     int tma_y0;            // image row of the tensor maps' row 0 (maps span only the rows the call reads)
+    float omt;             // 1 - tau in fp32 (a parameter operand rather than a live register)
 };
 
 // 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
@@ -135,7 +136,6 @@ template <int WARPS>
 struct Warp32Smem {
     float4 ubuf[WARPS][W32_TS * 32];     // U row-pair table (16 KiB, columns by ucol), also the
                                          // fp64 FFT tile (16.5 KiB) and the TMA staging area
-    float2 cs[32];                       // cos/sin(2 pi j / 32)
     unsigned int red_key[WARPS][32];     // AM_SMEM scratch
     unsigned int red_rank[WARPS][32];
     unsigned long long bar[WARPS];       // TMA window barrier, one per warp
@@ -181,7 +181,9 @@ __device__ __forceinline__ float4 pick_pair(const float2 (&re)[16], const float2
 // tie-rank order (lane l owns column bitrev5(l) for the tree reducer, l for
 // linear), so the reference's tie rule across columns is "lowest lane".
 // Returns the winning key and the winning lane on every lane.
-template <int ARGMAX>
+// ANY (guarded pair-key mode): any lane holding the maximum may win (a tie is
+// re-run in fp64 anyway), so the highest such lane is taken: one FLO, no reversal.
+template <int ARGMAX, bool ANY = false>
 __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int &wl,
                                                 unsigned int *skey, unsigned int *srank) {
     const int lane = lane_id();
@@ -199,7 +201,8 @@ __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int
         wl = (int)rank;
     } else if (ARGMAX == AM_REDUX) {
         kmax = __reduce_max_sync(0xffffffffu, m1);
-        wl = __ffs(__ballot_sync(0xffffffffu, m1 == kmax)) - 1;
+        const uint32_t b = __ballot_sync(0xffffffffu, m1 == kmax);
+        wl = ANY ? 31 - __clz(b) : __ffs(b) - 1;
     } else {  // AM_SMEM: classic shared-memory tree reduction
         skey[lane] = m1;
         srank[lane] = (uint32_t)lane;
@@ -231,7 +234,10 @@ __device__ __forceinline__ void cross_lane_best(uint32_t m1, uint32_t &kmax, int
 //   hmask:  ~31, passed in from a kernel argument so that ptxas keeps it in a
 //           register: with both constants immediate it splits the key
 //           formation (o & ~31) | c into two LOP3s
-template <bool TREE, bool GUARD, bool HERM, bool UPDATE, bool SWAP>
+#ifndef FSR_W32_PAIRKEY
+#define FSR_W32_PAIRKEY 1
+#endif
+template <bool TREE, bool GUARD, bool HERM, bool UPDATE, bool SWAP, bool PK = false>
 __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
                                         const float4 *up, float gr, float gi, uint32_t canon,
                                         uint32_t hmask, uint32_t &m1, uint32_t &m2) {
@@ -259,6 +265,25 @@ __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], cons
         const float2 o = __fmul2_rn(mag, wf2[i]);
         const uint32_t rka = TREE ? ((i & 1) << 4 | (i & 2) << 2 | (i & 4) | (i & 8) >> 2) : (uint32_t)i;
         const uint32_t rkb = TREE ? (rka | 1u) : (uint32_t)(i + 16);
+        if (PK) {
+            // pair key: the larger of the pair's two objectives tagged with the rank
+            // of the pair's lower row (pairs keep their relative tie order in both
+            // reducers); the caller resolves which half won
+            float ox = o.x, oy = o.y;
+            if (HERM) {
+                ox = ((canon >> i) & 1u) ? ox : 0.f;
+                oy = ((canon >> (i + 16)) & 1u) ? oy : 0.f;
+            }
+            const uint32_t h = and_or(f2u(fmaxf(ox, oy)), hmask, 31u ^ rka);  // rank of row i
+            if ((i & 1) == 0) {
+                hpend = h;
+            } else {
+                const uint32_t hmax = max(hpend, h), hmin = min(hpend, h);
+                m2 = umax3(m2, hmin, min(m1, hmax));
+                m1 = max(m1, hmax);
+            }
+            continue;
+        }
         // low 5 bits = 31 - rank(u)
         uint32_t ka = and_or(f2u(o.x), hmask, 31u ^ rka);
         uint32_t kb = and_or(f2u(o.y), hmask, 31u ^ rkb);
@@ -284,14 +309,14 @@ __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], cons
     }
 }
 
-template <bool TREE, bool GUARD, bool HERM>
+template <bool TREE, bool GUARD, bool HERM, bool PK = false>
 __device__ __forceinline__ void pass_update(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
                                             const float4 *up, bool swap, float gr, float gi,
                                             uint32_t canon, uint32_t hmask, uint32_t &m1, uint32_t &m2) {
     if (swap)
-        pass_x2<TREE, GUARD, HERM, true, true>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
+        pass_x2<TREE, GUARD, HERM, true, true, PK>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
     else
-        pass_x2<TREE, GUARD, HERM, true, false>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
+        pass_x2<TREE, GUARD, HERM, true, false, PK>(re, im, wf2, up, gr, gi, canon, hmask, m1, m2);
 }
 
 // fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
@@ -447,12 +472,22 @@ template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY, int OPTS = W
 __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
+    // pair keys (one key per row pair, half resolved after the argmax): exact ties
+    // between bins are ordered differently than the reference, so only where the
+    // guard re-runs every near-tie in fp64 anyway
+    constexpr bool PK = GUARD && !STUDY && FSR_W32_PAIRKEY;
+    // lane order: lanes hold columns in tie-rank order where the kernel must break
+    // exact ties itself; with pair keys every near-tie is re-run in fp64, so lanes
+    // hold columns in natural order (no bit reversals in the argmax tail).  The
+    // Hermitian canonical halves always follow the real reducer's tie ranks.
+    constexpr bool LT = TREE && !PK;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ float2 w32_cs[32];  // cos/sin(2 pi j / 32), static: a constant shared address
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
     if (threadIdx.x < 32) {
         const double th = 6.283185307179586476925286766559 * threadIdx.x / 32.0;
-        sm.cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
+        w32_cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
     }
     const uint32_t bar = smem_u32(&sm.bar[wid]);
     if (lane == 0) mbar_init(bar, 1);
@@ -463,7 +498,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     // spectral column of this lane, in tie-rank order: the tree reducer's rank
     // of column v is bitrev5(v) (_kernels.py:12-49), so lane l owns column
     // bitrev5(l) and "lowest lane" is the reference's column tie-break
-    const int v = TREE ? (int)bitrev5(lane) : lane;
+    const int v = LT ? (int)bitrev5(lane) : lane;
     // canonical half of each mirror pair (lower tie rank), bit u of this lane's column
     uint32_t canon = 0;
 #pragma unroll
@@ -471,7 +506,6 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         int t = u * 32 + v, mt = ((32 - u) & 31) * 32 + ((32 - v) & 31);
         canon |= (uint32_t)(tie_rank(t, TREE) <= tie_rank(mt, TREE)) << u;
     }
-    const float one_minus_tau = 1.f - a.tau;
 
     const int64_t total_warps = (int64_t)gridDim.x * WARPS;
     for (int64_t bi = (int64_t)blockIdx.x * WARPS + wid; bi < a.nblocks; bi += total_warps) {
@@ -481,7 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
         const bool xin = x >= 0 && x < a.W;
         float2 re[16], im[16];
-        const float energy = (float)w32_prologue_f64<TREE>(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane, v);
+        const float energy = (float)w32_prologue_f64<LT>(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane, v);
         const float w00 = ub[16 * 32].x;  // U[16][0].x = Wx[0][0] = sum of the weights
         // frequency prior of this column for the row pairs (i, i+16) (weights.py:40-56);
         // re-read per block (L1-resident) so it is not live across the prologue
@@ -522,30 +556,44 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         int it = 0;
         for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            const float4 *up = ub + (16 - (pu & 15)) * 32 + ucol<TREE>((v - pv) & 31);
+            const float4 *up = ub + (16 - (pu & 15)) * 32 + ucol<LT>((v - pv) & 31);
             const bool swap = pu >= 16;
             if (it == 0) {
-                pass_x2<TREE, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
+                pass_x2<LT, GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
             } else if (herm) {
-                pass_update<TREE, GUARD, true>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass_update<LT, GUARD, true, PK>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             } else {
-                pass_update<TREE, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass_update<LT, GUARD, false, PK>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
             uint32_t kmax;
             int wl;
-            cross_lane_best<ARGMAX>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
-            const int bv = TREE ? (int)bitrev5((uint32_t)wl) : wl;
+            cross_lane_best<ARGMAX, PK>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
+            const int bv = LT ? (int)bitrev5((uint32_t)wl) : wl;
             const uint32_t urank = 31u - (kmax & 31u);
-            const int bu = TREE ? (int)bitrev5(urank) : (int)urank;
+            int bu = LT ? (int)bitrev5(urank) : (int)urank;  // PK: the pair's lower row
             const float b1 = __uint_as_float(kmax & ~31u);
-            if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
             if (EARLY && b1 < thr) {  // thr == 0 unless early stop is on
-                if (GUARD && b1 >= thr * one_minus_tau) flagged = true;  // a stop decision within tau
+                if (GUARD && b1 >= thr * a.omt) flagged = true;  // a stop decision within tau
                 break;
             }
             float2 wfp;
             const float4 q = pick_pair(re, im, wf2, bu, wfp);
+            float po_pk = 0.f;
+            if (PK) {
+                // which half of the winning pair: recompute both objectives exactly as
+                // the pass did (fma(re, re, im*im) * wf, non-canonical halves zeroed
+                // while Hermitian); the lower row wins a tie in both reducers' orders
+                float olo = fmaf(q.x, q.x, q.z * q.z) * wfp.x, ohi = fmaf(q.y, q.y, q.w * q.w) * wfp.y;
+                if (herm) {
+                    olo = ((canon >> bu) & 1u) ? olo : 0.f;
+                    ohi = ((canon >> (bu + 16)) & 1u) ? ohi : 0.f;
+                }
+                const bool hi = __shfl_sync(0xffffffffu, (int)(ohi > olo), wl) != 0;
+                po_pk = hi ? olo : ohi;  // the pair partner (meaningful on the winner lane)
+                bu += hi ? 16 : 0;
+            }
             const bool lo = bu < 16;
+            if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
             float2 c = lo ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
@@ -557,17 +605,22 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                 // second-best objective: any other lane's best, or the winner lane's
                 // runner-up = max(its second pair maximum, the winner's pair partner);
                 // the partner's key is recomputed exactly as the pass computed it
-                const int up_row = bu ^ 16;
-                const float pre = lo ? q.y : q.x, pim = lo ? q.w : q.z, pwf = lo ? wfp.y : wfp.x;
-                const float po = fmaf(pre, pre, pim * pim) * pwf;
-                const uint32_t prk = TREE ? bitrev5((uint32_t)up_row) : (uint32_t)up_row;
-                uint32_t kp = (f2u(po) & a.key_mask) | (31u ^ prk);
-                if (herm && !((canon >> up_row) & 1u)) kp = 0u;
+                uint32_t kp;
+                if (PK) {
+                    kp = f2u(po_pk) & a.key_mask;  // rank bits do not matter for b2
+                } else {
+                    const int up_row = bu ^ 16;
+                    const float pre = lo ? q.y : q.x, pim = lo ? q.w : q.z, pwf = lo ? wfp.y : wfp.x;
+                    const float po = fmaf(pre, pre, pim * pim) * pwf;
+                    const uint32_t prk = LT ? bitrev5((uint32_t)up_row) : (uint32_t)up_row;
+                    kp = (f2u(po) & a.key_mask) | (31u ^ prk);
+                    if (herm && !((canon >> up_row) & 1u)) kp = 0u;
+                }
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b2 >= b1 * one_minus_tau;
+                flagged |= b2 >= b1 * a.omt;
                 // a continue decision within tau of the stop threshold is ambiguous too
-                if (EARLY) flagged |= b1 * one_minus_tau < thr;
+                if (EARLY) flagged |= b1 * a.omt < thr;
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)
                     if (it == 0) B0 = b1;
                     min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
@@ -577,7 +630,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             // a non-self-mirror selection breaks the exact Hermitian symmetry
             if (herm) herm = ((bu & 15) == 0) && ((bv & 15) == 0);
             // synthesis of the target pixels, Re(gp e^{+2 pi i (bu m + bv n)/32})
-            const float2 e = sm.cs[(bu * pm + bv * pn) & 31];
+            const float2 e = w32_cs[(bu * pm + bv * pn) & 31];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
         }
         const int done = it;
