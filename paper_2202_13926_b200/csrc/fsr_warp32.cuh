@@ -266,15 +266,15 @@ __device__ __forceinline__ void pass_x2(float2 (&re)[16], float2 (&im)[16], cons
         const uint32_t rka = TREE ? ((i & 1) << 4 | (i & 2) << 2 | (i & 4) | (i & 8) >> 2) : (uint32_t)i;
         const uint32_t rkb = TREE ? (rka | 1u) : (uint32_t)(i + 16);
         if (PK) {
-            // pair key: the larger of the pair's two objectives tagged with the rank
-            // of the pair's lower row (pairs keep their relative tie order in both
-            // reducers); the caller resolves which half won
+            // pair key: the larger of the pair's two objectives tagged with the pair
+            // index (tie order is irrelevant here: the guard re-runs ties); the
+            // caller resolves which half won
             float ox = o.x, oy = o.y;
             if (HERM) {
                 ox = ((canon >> i) & 1u) ? ox : 0.f;
                 oy = ((canon >> (i + 16)) & 1u) ? oy : 0.f;
             }
-            const uint32_t h = and_or(f2u(fmaxf(ox, oy)), hmask, 31u ^ rka);  // rank of row i
+            const uint32_t h = and_or(f2u(fmaxf(ox, oy)), hmask, (uint32_t)i);  // the pair index
             if ((i & 1) == 0) {
                 hpend = h;
             } else {
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             cross_lane_best<ARGMAX, PK>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
             const int bv = LT ? (int)bitrev5((uint32_t)wl) : wl;
             const uint32_t urank = 31u - (kmax & 31u);
-            int bu = LT ? (int)bitrev5(urank) : (int)urank;  // PK: the pair's lower row
+            int bu = PK ? (int)(kmax & 15u) : LT ? (int)bitrev5(urank) : (int)urank;  // PK: the pair
             const float b1 = __uint_as_float(kmax & ~31u);
             if (EARLY && b1 < thr) {  // thr == 0 unless early stop is on
                 if (GUARD && b1 >= thr * a.omt) flagged = true;  // a stop decision within tau
@@ -579,6 +579,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             float2 wfp;
             const float4 q = pick_pair(re, im, wf2, bu, wfp);
             float po_pk = 0.f;
+            float2 c;
             if (PK) {
                 // which half of the winning pair: recompute both objectives exactly as
                 // the pass did (fma(re, re, im*im) * wf, non-canonical halves zeroed
@@ -588,13 +589,18 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                     olo = ((canon >> bu) & 1u) ? olo : 0.f;
                     ohi = ((canon >> (bu + 16)) & 1u) ? ohi : 0.f;
                 }
-                const bool hi = __shfl_sync(0xffffffffu, (int)(ohi > olo), wl) != 0;
-                po_pk = hi ? olo : ohi;  // the pair partner (meaningful on the winner lane)
+                // every lane resolves its own pair; the winner's half, coefficient
+                // and partner are then read from lane wl by independent shuffles
+                const bool hl = ohi > olo;
+                po_pk = hl ? olo : ohi;  // the pair partner (used on the winner lane)
+                c = hl ? make_float2(q.y, q.w) : make_float2(q.x, q.z);
+                const bool hi = __shfl_sync(0xffffffffu, (int)hl, wl) != 0;
                 bu += hi ? 16 : 0;
+            } else {
+                c = bu < 16 ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
             }
             const bool lo = bu < 16;
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
-            float2 c = lo ? make_float2(q.x, q.z) : make_float2(q.y, q.w);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             gr = c.x * ginv;
