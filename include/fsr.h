@@ -168,7 +168,7 @@ typedef struct {
     int32_t kernel_launches; /* kernels launched by the call (all devices) */
     int32_t flags;           /* FSR_STATS_* bits of the first device's launch */
     double kernel_ms;        /* device time of the last call's kernels (first device) */
-    double main_ms;          /* device time of the dominant kernel (first device) */
+    double main_ms;          /* device time of the dominant kernel (first device; summed over chunks) */
 } fsr_stats;
 /* fsr_stats.flags: the N=32 fp32 kernel gathered its windows with TMA (2-D
  * tensor maps, zero fill outside the image).  Set FSR_NO_TMA=1 in the

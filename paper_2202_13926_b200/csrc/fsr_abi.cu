@@ -88,11 +88,14 @@ struct Device {
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
     bool tma_enabled = true;     // warp32 window gather by TMA when the rows allow it
+    bool chunking = true;        // large calls in row chunks over two lanes (FSR_NO_CHUNK=1: off)
     int used_tma = 0;            // last warp32 launch gathered by TMA
     // host-buffer calls on large strips are pipelined over two "lanes" (same GPU,
     // own stream, staging buffers and scratch): H2D of chunk c+1 and D2H of chunk
     // c-1 overlap the kernels of chunk c
     std::vector<std::unique_ptr<Device>> lanes;
+    int dev_chunks = 1;  // chunks of the last device-API call (for its statistics)
+    cudaEvent_t ck0[4] = {}, ck1[4] = {};  // per-chunk main-kernel brackets
 };
 
 }  // namespace
@@ -360,7 +363,10 @@ bool pair64_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 32 && p->block * p->block <= 32;
 }
 
-constexpr int kWarps = 4;
+#ifndef FSR_W32_CTA_WARPS
+#define FSR_W32_CTA_WARPS 4
+#endif
+constexpr int kWarps = FSR_W32_CTA_WARPS;
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -540,7 +546,10 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                   const uint8_t *mask, int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H,
                   int64_t W, int64_t row0, int64_t row1, int32_t *sel, int32_t *done,
                   bool device_fill, double host_fill, cudaStream_t st,
-                  Counters *ctr_in = nullptr, int32_t *empty_in = nullptr) {
+                  Counters *ctr_in = nullptr, int32_t *empty_in = nullptr,
+                  cudaEvent_t ev_main0 = nullptr, cudaEvent_t ev_main1 = nullptr) {
+    // ev_main0/1 (chunked calls): bracket the main kernel; otherwise d.ev_mid marks its end
+    cudaEvent_t ev_end = ev_main1 ? ev_main1 : d.ev_mid;
     const int N = p->block + 2 * p->border;
     const int64_t bcols = (W + p->block - 1) / p->block;
     const int64_t first = row0 * bcols, nblocks = (row1 - row0) * bcols;
@@ -554,6 +563,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         empty_list = d.empty_list.as<int32_t>();
     }
     CUDA_TRY(eng, cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+    if (ev_main0) CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
     const int gen_grid = d.sms * 8;
@@ -569,7 +579,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                W, bcols, first, nblocks, tab, sel, done,
                                                &ctr->empty_count, empty_list);
             if ((rc = launch_fp64_n32<IO>(eng, d, a, p, nblocks, st))) return rc;
-            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+            CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64 && warp16d_eligible(p)) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
@@ -579,7 +589,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = launch_warp16d<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          nblocks, st)))
                 return rc;
-            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+            CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
@@ -589,7 +599,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                     p->early_stop, tab, sel, done, &ctr->empty_count,
                                     empty_list};
             if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
-            CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+            CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else {
             // fp32 on the generic kernel: no near-tie guard there, so a guarded
             // request is served in fp64 (exact) for these supports
@@ -604,7 +614,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                        p->reducer == FSR_REDUCER_TREE, p->early_stop, tf, sel,
                                        done, &ctr->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
-                CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+                CUDA_TRY(eng, cudaEventRecord(ev_end, st));
             } else {
                 ImageArgs<double, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
                                         p->block, p->border, N, p->iterations, bcols, first,
@@ -612,7 +622,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                         p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel,
                                         done, &ctr->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
-                CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+                CUDA_TRY(eng, cudaEventRecord(ev_end, st));
             }
         }
     } else {
@@ -682,7 +692,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                     guarded || d.gap_debug != nullptr, st)))
                 return rc;
         }
-        CUDA_TRY(eng, cudaEventRecord(d.ev_mid, st));
+        CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         if (guarded && fast64) {
             // fp64 re-run of ambiguous blocks on the exact generic kernel (list mode)
             Tables<double> tab;
@@ -743,6 +753,33 @@ int select_device(fsr_engine *eng, Device &d) {
     return FSR_OK;
 }
 
+// Large calls run in K row chunks alternating over two lanes (same GPU, own
+// stream, staging and scratch): one chunk's copies, fp64 re-run and launch tail
+// overlap the next chunk's main kernel.
+int chunk_count(const Device &d, int64_t block_rows) {
+    return (d.gap_debug || !d.chunking) ? 1 : (int)std::min<int64_t>(4, std::max<int64_t>(1, block_rows / 64));
+}
+
+int ensure_lanes(fsr_engine *eng, Device &d) {
+    while (d.lanes.size() < 2) {
+        auto ln = std::make_unique<Device>();
+        ln->id = d.id;
+        ln->sms = d.sms;
+        ln->tma_enabled = d.tma_enabled;
+        CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
+        CUDA_TRY(eng, cudaEventCreateWithFlags(&ln->ev0, cudaEventDisableTiming));
+        CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
+        CUDA_TRY(eng, cudaEventCreate(&ln->ev_mid));
+        d.lanes.push_back(std::move(ln));
+    }
+    for (int c = 0; c < 4; ++c)
+        if (!d.ck0[c]) {
+            CUDA_TRY(eng, cudaEventCreate(&d.ck0[c]));
+            CUDA_TRY(eng, cudaEventCreate(&d.ck1[c]));
+        }
+    return FSR_OK;
+}
+
 // Host-buffer whole-image call: split block rows over devices, H2D strip+halo,
 // enqueue, D2H target rows.  The empty-support fill value is computed on the
 // host (from the caller's full image) only if some block had an empty window.
@@ -787,21 +824,9 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         if (q.row1 <= q.row0) continue;
         if ((rc = select_device(eng, d))) return rc;
         const int64_t prow = q.row1 - q.row0;
-        const int K = d.gap_debug ? 1 : (int)std::min<int64_t>(4, std::max<int64_t>(1, prow / 64));
+        const int K = chunk_count(d, prow);
         nchunks[g] = K;
-        if (K > 1 && d.lanes.empty()) {
-            for (int l = 0; l < 2; ++l) {
-                auto ln = std::make_unique<Device>();
-                ln->id = d.id;
-                ln->sms = d.sms;
-                ln->tma_enabled = d.tma_enabled;
-                CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
-                CUDA_TRY(eng, cudaEventCreate(&ln->ev0));
-                CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
-                CUDA_TRY(eng, cudaEventCreate(&ln->ev_mid));
-                d.lanes.push_back(std::move(ln));
-            }
-        }
+        if (K > 1 && (rc = ensure_lanes(eng, d))) return rc;
         d.launches = 0;
         const int64_t nb_part = prow * bcols;
         CUDA_TRY(eng, d.counters.ensure((size_t)K * sizeof(Counters)));
@@ -833,7 +858,8 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
             int32_t *vdone = done ? ld.done.as<int32_t>() - r0 * bcols : nullptr;
             rc = enqueue_image<IO>(eng, ld, p, vpx, W, vmask, W, vout, W, H, W, r0, r1, vsel, vdone,
                                    false, NAN, ld.stream, d.counters.as<Counters>() + c,
-                                   d.empty_list.as<int32_t>() + (r0 - q.row0) * bcols);
+                                   d.empty_list.as<int32_t>() + (r0 - q.row0) * bcols,
+                                   K > 1 ? d.ck0[c] : nullptr, K > 1 ? d.ck1[c] : nullptr);
             if (rc) return rc;
             if (K == 1) CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
             CUDA_TRY(eng, cudaMemcpyAsync(out + oa * W, ld.out.p, (size_t)rows_out * W * sizeof(IO),
@@ -864,6 +890,10 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
                 float t = 0.f;
                 if (cudaEventElapsedTime(&t, d.ev0, ln->ev1) == cudaSuccess) ms = std::max(ms, t);
             }
+            for (int c = 0; c < K; ++c) {  // the chunks' main-kernel brackets
+                float t = 0.f;
+                if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) mm += t;
+            }
         } else {
             CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
             if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
@@ -881,7 +911,7 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         if (g == 0) {
             eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
             eng->stats.kernel_ms = ms;
-            eng->stats.main_ms = mm;  // dominant-kernel time only for an unchunked call
+            eng->stats.main_ms = mm;
         }
     }
     eng->stats.empty_blocks = empty_total;
@@ -987,6 +1017,8 @@ int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **ou
         d->sms = prop.multiProcessorCount;
         const char *no_tma = std::getenv("FSR_NO_TMA");  // A/B switch for the TMA window gather
         d->tma_enabled = !(no_tma && *no_tma && *no_tma != '0');
+        const char *no_chunk = std::getenv("FSR_NO_CHUNK");  // one launch per call (kernel timing)
+        d->chunking = !(no_chunk && *no_chunk && *no_chunk != '0');
         CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));
@@ -1024,6 +1056,11 @@ void fsr_engine_destroy(fsr_engine *eng) {
             cudaEventDestroy(ln->ev_mid);
             cudaStreamDestroy(ln->stream);
         }
+        for (int c = 0; c < 4; ++c)
+            if (d.ck0[c]) {
+                cudaEventDestroy(d.ck0[c]);
+                cudaEventDestroy(d.ck1[c]);
+            }
         cudaEventDestroy(d.ev0);
         cudaEventDestroy(d.ev1);
         cudaEventDestroy(d.ev_mid);
@@ -1066,9 +1103,39 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
     if ((rc = select_device(eng, d))) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     d.launches = 0;
+    const int K = chunk_count(d, row1 - row0);
+    d.dev_chunks = K;
     CUDA_TRY(eng, cudaEventRecord(d.ev0, st));
-    rc = enqueue_image<float>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
-                              height, width, row0, row1, nullptr, nullptr, true, NAN, st);
+    if (K == 1) {
+        rc = enqueue_image<float>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
+                                  height, width, row0, row1, nullptr, nullptr, true, NAN, st);
+    } else {
+        // chunks alternate over the two lanes, forked from and joined back into the
+        // caller's stream; chunk c uses counter slot c and its own empty-list region
+        if ((rc = ensure_lanes(eng, d))) return rc;
+        const int64_t bcols = (width + p->block - 1) / p->block;
+        CUDA_TRY(eng, d.counters.ensure((size_t)K * sizeof(Counters)));
+        CUDA_TRY(eng, d.empty_list.ensure((size_t)(row1 - row0) * bcols * sizeof(int32_t)));
+        for (auto &ln : d.lanes) {
+            ln->launches = 0;
+            CUDA_TRY(eng, cudaStreamWaitEvent(ln->stream, d.ev0, 0));
+        }
+        for (int c = 0; c < K && rc == FSR_OK; ++c) {
+            Device &ld = *d.lanes[c % 2];
+            const int64_t r0 = row0 + (row1 - row0) * c / K, r1 = row0 + (row1 - row0) * (c + 1) / K;
+            rc = enqueue_image<float>(eng, ld, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
+                                      height, width, r0, r1, nullptr, nullptr, true, NAN, ld.stream,
+                                      d.counters.as<Counters>() + c,
+                                      d.empty_list.as<int32_t>() + (r0 - row0) * bcols,
+                                      d.ck0[c], d.ck1[c]);
+            d.used_tma = ld.used_tma;
+        }
+        for (auto &ln : d.lanes) {
+            d.launches += ln->launches;
+            CUDA_TRY(eng, cudaEventRecord(ln->ev1, ln->stream));
+            CUDA_TRY(eng, cudaStreamWaitEvent(st, ln->ev1, 0));
+        }
+    }
     CUDA_TRY(eng, cudaEventRecord(d.ev1, st));
     eng->stats = fsr_stats{};
     eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
@@ -1120,14 +1187,26 @@ int fsr_last_stats(const fsr_engine *eng_c, fsr_stats *out) {
         CUDA_TRY(eng, cudaEventSynchronize(d.ev1));
         float ms = 0.f, mm = 0.f;
         if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
-        if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
+        if (d.dev_chunks > 1) {  // sum of the chunks' main-kernel brackets
+            for (int c = 0; c < d.dev_chunks; ++c) {
+                float t = 0.f;
+                if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) mm += t;
+            }
+        } else if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) {
+            mm = 0.f;
+        }
         (void)cudaGetLastError();
-        Counters c;
-        CUDA_TRY(eng, cudaMemcpy(&c, d.counters.p, sizeof c, cudaMemcpyDeviceToHost));
+        std::vector<Counters> cs(std::max(d.dev_chunks, 1));
+        CUDA_TRY(eng, cudaMemcpy(cs.data(), d.counters.p, cs.size() * sizeof(Counters),
+                                 cudaMemcpyDeviceToHost));
         eng->stats.kernel_ms = ms;
         eng->stats.main_ms = mm;
-        eng->stats.rerun_blocks = c.rerun_count;
-        eng->stats.empty_blocks = c.empty_count;
+        eng->stats.rerun_blocks = 0;
+        eng->stats.empty_blocks = 0;
+        for (const Counters &c : cs) {
+            eng->stats.rerun_blocks += c.rerun_count;
+            eng->stats.empty_blocks += c.empty_count;
+        }
         eng->device_stats_pending = false;
     }
     *out = eng->stats;

@@ -386,6 +386,42 @@ def test_register_kernels_edges(N, B, reducer, early_stop):
 
 
 @pytest.mark.gpu
+def test_device_api_chunks_equal_unchunked(monkeypatch):
+    """Device-API calls on tall ranges run in four row chunks over two streams,
+    forked from and joined into the caller's stream; output, empty-support fill
+    and re-run counts equal a single-launch (FSR_NO_CHUNK) engine bitwise."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib
+    H, W = 4 * 259, 256
+    img = oracle.synthetic_frame(H, W, 47)
+    sampled, mask = oracle.quarter_sample(img, 9)
+    mask[600:660, 100:160] = False  # empty supports in the third chunk
+    px = np.where(mask, sampled, 0.0).astype(np.float32)
+    p = _lib.make_params(4, 14, 40, precision="fp32", argmax="redux")
+    d_px = torch.tensor(px, device="cuda")
+    d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
+    outs, stats = [], []
+    for no_chunk in ("0", "1"):
+        monkeypatch.setenv("FSR_NO_CHUNK", no_chunk)
+        eng = _lib.Engine([0])
+        d_out = torch.full_like(d_px, -1.0)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                                   d_out.data_ptr(), W, p, s.cuda_stream)
+            st = eng.last_stats()
+        torch.cuda.synchronize()
+        outs.append(d_out.cpu().numpy())
+        stats.append(st)
+        eng.close()
+    assert stats[0]["empty_blocks"] > 0
+    assert stats[0]["empty_blocks"] == stats[1]["empty_blocks"]
+    assert stats[0]["rerun_blocks"] == stats[1]["rerun_blocks"]
+    assert stats[0]["kernel_launches"] > stats[1]["kernel_launches"]
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("support,reducer", [(16, "tree"), (32, "tree"), (64, "linear")])
 def test_host_api_chunks_tma_rows(support, reducer):
     """Four uneven chunks (the staging buffers grow between chunks on the same
