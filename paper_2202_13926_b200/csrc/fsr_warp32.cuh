@@ -556,7 +556,13 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         int it = 0;
         for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            const float4 *up = ub + (16 - (pu & 15)) * 32 + ucol<LT>((v - pv) & 31);
+            // U-table base and lane column re-derived from an opaque %tid.x read every
+            // iteration (one S2R): cheaper than the local-memory reload ptxas
+            // otherwise spills the warp's table base to
+            uint32_t tid;
+            asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+            const int vt = LT ? (int)bitrev5(tid & 31u) : (int)(tid & 31u);
+            const float4 *up = sm.ubuf[tid >> 5] + (16 - (pu & 15)) * 32 + ucol<LT>((vt - pv) & 31);
             const bool swap = pu >= 16;
             if (it == 0) {
                 pass_x2<LT, GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
@@ -642,6 +648,14 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         const int done = it;
         if (sel_b)
             for (int j = done + lane; j < a.iterations; j += 32) sel_b[j] = -1;
+        {
+        // the block's coordinates are re-derived after the loop from an opaque copy
+        // of bi, so they are not held in registers across it
+        int64_t bi2;
+        asm volatile("mov.b64 %0, %1;" : "=l"(bi2) : "l"(bi));
+        const int64_t bid = a.first + bi2;
+        const int64_t brow2 = bid / a.bcols;
+        const int64_t r0 = brow2 * a.B, c0 = (bid - brow2 * a.bcols) * a.B;
         if (lane == 0) {
             if (a.done) a.done[bid] = done;
             if (STUDY) {
@@ -660,6 +674,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             if (y < a.H && xx < a.W)
                 a.out[y * a.out_pitch + xx] =
                     a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+        }
         }
         __syncwarp();
     }
