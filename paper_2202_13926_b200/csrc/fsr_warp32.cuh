@@ -160,20 +160,50 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t m, uint32_t c) {
     return d;
 }
 
-// Row pair (u mod 16, u mod 16 + 16) of this lane for a warp-uniform dynamic u
-// (uniform branches only): q = (Re lo, Re hi, Im lo, Im hi), wfp = (wf lo, wf hi).
+// Row pair (u mod 16, u mod 16 + 16) of this lane, q = (Re lo, Re hi, Im lo, Im hi),
+// wfp = (wf lo, wf hi), by an indirect branch (BRX through a jump
+// table): one dispatch instead of a four-level compare tree.  u must be warp-uniform.
 __device__ __forceinline__ float4 pick_pair(const float2 (&re)[16], const float2 (&im)[16],
                                             const float2 (&wf2)[16], int u, float2 &wfp) {
     float4 q;
-    switch (u & 15) {
-#define FSR_PICK(i) \
-    case i: q = make_float4(re[i].x, re[i].y, im[i].x, im[i].y); wfp = wf2[i]; break;
-        FSR_PICK(0) FSR_PICK(1) FSR_PICK(2) FSR_PICK(3) FSR_PICK(4) FSR_PICK(5) FSR_PICK(6)
-        FSR_PICK(7) FSR_PICK(8) FSR_PICK(9) FSR_PICK(10) FSR_PICK(11) FSR_PICK(12)
-        FSR_PICK(13) FSR_PICK(14)
-        default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); wfp = wf2[15]; break;
-#undef FSR_PICK
-    }
+    asm volatile(
+        "{\n ts%=: .branchtargets L0_%=, L1_%=, L2_%=, L3_%=, L4_%=, L5_%=, L6_%=, L7_%=, L8_%=, L9_%=, L10_%=, L11_%=, L12_%=, L13_%=, L14_%=, L15_%=;\n"
+        " brx.idx %6, ts%=;\n"
+        " L0_%=: mov.f32 %0, %7; mov.f32 %1, %8; mov.f32 %2, %9; mov.f32 %3, %10; mov.f32 %4, %11; mov.f32 %5, %12; bra.uni Le_%=;\n"
+        " L1_%=: mov.f32 %0, %13; mov.f32 %1, %14; mov.f32 %2, %15; mov.f32 %3, %16; mov.f32 %4, %17; mov.f32 %5, %18; bra.uni Le_%=;\n"
+        " L2_%=: mov.f32 %0, %19; mov.f32 %1, %20; mov.f32 %2, %21; mov.f32 %3, %22; mov.f32 %4, %23; mov.f32 %5, %24; bra.uni Le_%=;\n"
+        " L3_%=: mov.f32 %0, %25; mov.f32 %1, %26; mov.f32 %2, %27; mov.f32 %3, %28; mov.f32 %4, %29; mov.f32 %5, %30; bra.uni Le_%=;\n"
+        " L4_%=: mov.f32 %0, %31; mov.f32 %1, %32; mov.f32 %2, %33; mov.f32 %3, %34; mov.f32 %4, %35; mov.f32 %5, %36; bra.uni Le_%=;\n"
+        " L5_%=: mov.f32 %0, %37; mov.f32 %1, %38; mov.f32 %2, %39; mov.f32 %3, %40; mov.f32 %4, %41; mov.f32 %5, %42; bra.uni Le_%=;\n"
+        " L6_%=: mov.f32 %0, %43; mov.f32 %1, %44; mov.f32 %2, %45; mov.f32 %3, %46; mov.f32 %4, %47; mov.f32 %5, %48; bra.uni Le_%=;\n"
+        " L7_%=: mov.f32 %0, %49; mov.f32 %1, %50; mov.f32 %2, %51; mov.f32 %3, %52; mov.f32 %4, %53; mov.f32 %5, %54; bra.uni Le_%=;\n"
+        " L8_%=: mov.f32 %0, %55; mov.f32 %1, %56; mov.f32 %2, %57; mov.f32 %3, %58; mov.f32 %4, %59; mov.f32 %5, %60; bra.uni Le_%=;\n"
+        " L9_%=: mov.f32 %0, %61; mov.f32 %1, %62; mov.f32 %2, %63; mov.f32 %3, %64; mov.f32 %4, %65; mov.f32 %5, %66; bra.uni Le_%=;\n"
+        " L10_%=: mov.f32 %0, %67; mov.f32 %1, %68; mov.f32 %2, %69; mov.f32 %3, %70; mov.f32 %4, %71; mov.f32 %5, %72; bra.uni Le_%=;\n"
+        " L11_%=: mov.f32 %0, %73; mov.f32 %1, %74; mov.f32 %2, %75; mov.f32 %3, %76; mov.f32 %4, %77; mov.f32 %5, %78; bra.uni Le_%=;\n"
+        " L12_%=: mov.f32 %0, %79; mov.f32 %1, %80; mov.f32 %2, %81; mov.f32 %3, %82; mov.f32 %4, %83; mov.f32 %5, %84; bra.uni Le_%=;\n"
+        " L13_%=: mov.f32 %0, %85; mov.f32 %1, %86; mov.f32 %2, %87; mov.f32 %3, %88; mov.f32 %4, %89; mov.f32 %5, %90; bra.uni Le_%=;\n"
+        " L14_%=: mov.f32 %0, %91; mov.f32 %1, %92; mov.f32 %2, %93; mov.f32 %3, %94; mov.f32 %4, %95; mov.f32 %5, %96; bra.uni Le_%=;\n"
+        " L15_%=: mov.f32 %0, %97; mov.f32 %1, %98; mov.f32 %2, %99; mov.f32 %3, %100; mov.f32 %4, %101; mov.f32 %5, %102; bra.uni Le_%=;\n"
+        " Le_%=:\n}"
+        : "=f"(q.x), "=f"(q.y), "=f"(q.z), "=f"(q.w), "=f"(wfp.x), "=f"(wfp.y)
+        : "r"(u & 15),
+          "f"(re[0].x), "f"(re[0].y), "f"(im[0].x), "f"(im[0].y), "f"(wf2[0].x), "f"(wf2[0].y),
+          "f"(re[1].x), "f"(re[1].y), "f"(im[1].x), "f"(im[1].y), "f"(wf2[1].x), "f"(wf2[1].y),
+          "f"(re[2].x), "f"(re[2].y), "f"(im[2].x), "f"(im[2].y), "f"(wf2[2].x), "f"(wf2[2].y),
+          "f"(re[3].x), "f"(re[3].y), "f"(im[3].x), "f"(im[3].y), "f"(wf2[3].x), "f"(wf2[3].y),
+          "f"(re[4].x), "f"(re[4].y), "f"(im[4].x), "f"(im[4].y), "f"(wf2[4].x), "f"(wf2[4].y),
+          "f"(re[5].x), "f"(re[5].y), "f"(im[5].x), "f"(im[5].y), "f"(wf2[5].x), "f"(wf2[5].y),
+          "f"(re[6].x), "f"(re[6].y), "f"(im[6].x), "f"(im[6].y), "f"(wf2[6].x), "f"(wf2[6].y),
+          "f"(re[7].x), "f"(re[7].y), "f"(im[7].x), "f"(im[7].y), "f"(wf2[7].x), "f"(wf2[7].y),
+          "f"(re[8].x), "f"(re[8].y), "f"(im[8].x), "f"(im[8].y), "f"(wf2[8].x), "f"(wf2[8].y),
+          "f"(re[9].x), "f"(re[9].y), "f"(im[9].x), "f"(im[9].y), "f"(wf2[9].x), "f"(wf2[9].y),
+          "f"(re[10].x), "f"(re[10].y), "f"(im[10].x), "f"(im[10].y), "f"(wf2[10].x), "f"(wf2[10].y),
+          "f"(re[11].x), "f"(re[11].y), "f"(im[11].x), "f"(im[11].y), "f"(wf2[11].x), "f"(wf2[11].y),
+          "f"(re[12].x), "f"(re[12].y), "f"(im[12].x), "f"(im[12].y), "f"(wf2[12].x), "f"(wf2[12].y),
+          "f"(re[13].x), "f"(re[13].y), "f"(im[13].x), "f"(im[13].y), "f"(wf2[13].x), "f"(wf2[13].y),
+          "f"(re[14].x), "f"(re[14].y), "f"(im[14].x), "f"(im[14].y), "f"(wf2[14].x), "f"(wf2[14].y),
+          "f"(re[15].x), "f"(re[15].y), "f"(im[15].x), "f"(im[15].y), "f"(wf2[15].x), "f"(wf2[15].y));
     return q;
 }
 
