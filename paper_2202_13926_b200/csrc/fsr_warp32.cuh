@@ -584,15 +584,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int it = 0;
+        const float4 *up = ub;  // U-table read pointer of the next pass (unused by the first)
         for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            // U-table base and lane column re-derived from an opaque %tid.x read every
-            // iteration (one S2R): cheaper than the local-memory reload ptxas
-            // otherwise spills the warp's table base to
-            uint32_t tid;
-            asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-            const int vt = LT ? (int)bitrev5(tid & 31u) : (int)(tid & 31u);
-            const float4 *up = sm.ubuf[tid >> 5] + (16 - (pu & 15)) * 32 + ucol<LT>((vt - pv) & 31);
             const bool swap = pu >= 16;
             if (it == 0) {
                 pass_x2<LT, GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
@@ -603,6 +597,11 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             }
             uint32_t kmax;
             int wl;
+            // U-table base and lane column for the next pass, re-derived from an opaque
+            // %tid.x read (one S2R, issued here so its latency hides under the argmax):
+            // cheaper than the local-memory reload ptxas otherwise spills them to
+            uint32_t tid;
+            asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
             cross_lane_best<ARGMAX, PK>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
             const int bv = LT ? (int)bitrev5((uint32_t)wl) : wl;
             const uint32_t urank = 31u - (kmax & 31u);
@@ -643,6 +642,8 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             gi = c.y * ginv;
             pu = bu;
             pv = bv;
+            up = sm.ubuf[tid >> 5] + (16 - (pu & 15)) * 32 +
+                 ucol<LT>(((LT ? (int)bitrev5(tid & 31u) : (int)(tid & 31u)) - pv) & 31);
             if (GUARD) {
                 // second-best objective: any other lane's best, or the winner lane's
                 // runner-up = max(its second pair maximum, the winner's pair partner);
