@@ -219,6 +219,10 @@ template <int WARPS, bool TREE, int ARGMAX, bool GUARD, int OPTS = W32_ALL>
 __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
     warp16_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
+    // lane order as in warp32: tie-rank order only where the kernel breaks exact
+    // ties itself; guarded, every near-tie is re-run in fp64, so natural order
+    // (no bit reversals in the argmax tail) and any maximal lane may win
+    constexpr bool LT = TREE && !GUARD;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp16Smem<WARPS> &sm = *reinterpret_cast<Warp16Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
@@ -233,7 +237,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
     uint32_t phase = 0;
     float4 *ub = sm.ubuf[wid];
     const int p = lane & 1;
-    const int v = TREE ? (int)bitrev4((uint32_t)(lane >> 1)) : (lane >> 1);
+    const int v = LT ? (int)bitrev4((uint32_t)(lane >> 1)) : (lane >> 1);
     // canonical half of each mirror pair: bit i (row p+2i), bit i+4 (row p+2i+8)
     uint32_t canon = 0;
 #pragma unroll
@@ -245,7 +249,6 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             canon |= (uint32_t)(tie_rank(t, TREE) <= tie_rank(mt, TREE)) << (i + 4 * hh);
         }
     }
-    const float one_minus_tau = 1.f - a.tau;
     float2 wf2[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
         const int64_t r0 = brow * a.B, c0 = bcol * a.B;
         float2 re[4], im[4];
         const float energy =
-            (float)w16_prologue<TREE>(a, maps, ub, bar, phase, re, im, r0 - a.L, c0 - a.L, lane, v, p);
+            (float)w16_prologue<LT>(a, maps, ub, bar, phase, re, im, r0 - a.L, c0 - a.L, lane, v, p);
         const float w00 = ub[8 * W16_US].x;  // U16[8][0].x = Wx[0][0] = sum of the weights
         int32_t *sel_b = (TRACE && a.sel) ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
@@ -288,26 +291,26 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
         int it = 0;
         for (; it < a.iterations; ++it) {
             uint32_t m1, m2;
-            const float4 *up = ub + (8 + p - (pu & 7)) * W16_US + ucol16<TREE>((v - pv) & 15);
+            const float4 *up = ub + (8 + p - (pu & 7)) * W16_US + ucol16<LT>((v - pv) & 15);
             const bool swap = pu >= 8;
             if (it == 0) {
-                pass16<TREE, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
+                pass16<LT, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
             } else if (herm) {
-                pass16_update<TREE, GUARD, true>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass16_update<LT, GUARD, true>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             } else {
-                pass16_update<TREE, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass16_update<LT, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
             uint32_t kmax;
             int wl;
-            cross_lane_best<ARGMAX>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
+            cross_lane_best<ARGMAX, GUARD>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
             const uint32_t rank = 31u - (kmax & 31u);
-            const int j = TREE ? (int)bitrev3(rank) : (int)rank;
+            const int j = LT ? (int)bitrev3(rank) : (int)rank;
             const int bu = (wl & 1) + 2 * j;
-            const int bv = TREE ? (int)bitrev4((uint32_t)(wl >> 1)) : (wl >> 1);
+            const int bv = LT ? (int)bitrev4((uint32_t)(wl >> 1)) : (wl >> 1);
             const float b1 = __uint_as_float(kmax & ~31u);
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
             if (EARLY && b1 < thr) {
-                if (GUARD && b1 >= thr * one_minus_tau) flagged = true;
+                if (GUARD && b1 >= thr * a.omt) flagged = true;
                 break;
             }
             float4 q;
@@ -327,8 +330,8 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             if (GUARD) {
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b2 >= b1 * one_minus_tau;
-                if (EARLY) flagged |= b1 * one_minus_tau < thr;
+                flagged |= b2 >= b1 * a.omt;
+                if (EARLY) flagged |= b1 * a.omt < thr;
             }
             if (herm) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
             const float2 e = sm.cs[(bu * pm + bv * pn) & 15];
