@@ -1148,7 +1148,7 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
 // Not part of include/fsr.h: development hook for the guard study
 // (tools/guard_study.py).  Runs the N=32 fp32 kernel on one device with the
 // top-2 tracking on but no re-run, returning each block's minimum relative
-// top-2 objective gap over its iterations, plus the selection trace.
+// top-2 objective gap over its iterations and the first iteration whose gap is below guard_tau, plus the selection trace.
 int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *px,
                          const uint8_t *mask, int64_t H, int64_t W, float *out, float *gaps,
                          int32_t *sel) {

@@ -41,6 +41,7 @@
 #pragma once
 
 #include <cuda.h>  // CUtensorMap
+#include <type_traits>
 
 #include "fsr_common.cuh"
 #include "fsr_fft.cuh"
@@ -580,20 +581,25 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         float acc = 0.f;
         bool herm = true;
         bool flagged = false;
-        float min_gap = 1.f, min_gap2 = 1.f, B0 = 0.f;
+        float min_gap = 1.f, min_gap2 = 1e9f;
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int it = 0;
         const float4 *up = ub;  // U-table read pointer of the next pass (unused by the first)
-        for (; it < a.iterations; ++it) {
+        // the guard's main test accumulated as a float: flagged iff fl >= 0
+        // (b2 >= b1 (1 - tau) <=> b2 - b1 (1 - tau) >= 0, exact in float)
+        float fl = -1.f;
+        // One greedy iteration; H: the state is still exactly Hermitian.  The
+        // Hermitian phase (a few iterations at most) and the rest run as two
+        // loops, so the main loop carries no Hermitian bookkeeping.
+        auto step = [&](auto hconst) -> bool {
+            constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
             const bool swap = pu >= 16;
-            if (it == 0) {
+            if (H && it == 0) {
                 pass_x2<LT, GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
-            } else if (herm) {
-                pass_update<LT, GUARD, true, PK>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             } else {
-                pass_update<LT, GUARD, false, PK>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass_update<LT, GUARD, H, PK>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
             uint32_t kmax;
             int wl;
@@ -609,7 +615,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             const float b1 = __uint_as_float(kmax & ~31u);
             if (EARLY && b1 < thr) {  // thr == 0 unless early stop is on
                 if (GUARD && b1 >= thr * a.omt) flagged = true;  // a stop decision within tau
-                break;
+                return false;
             }
             float2 wfp;
             const float4 q = pick_pair(re, im, wf2, bu, wfp);
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                 // the pass did (fma(re, re, im*im) * wf, non-canonical halves zeroed
                 // while Hermitian); the lower row wins a tie in both reducers' orders
                 float olo = fmaf(q.x, q.x, q.z * q.z) * wfp.x, ohi = fmaf(q.y, q.y, q.w * q.w) * wfp.y;
-                if (herm) {
+                if (H) {
                     olo = ((canon >> bu) & 1u) ? olo : 0.f;
                     ohi = ((canon >> (bu + 16)) & 1u) ? ohi : 0.f;
                 }
@@ -657,25 +663,35 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                     const float po = fmaf(pre, pre, pim * pim) * pwf;
                     const uint32_t prk = LT ? bitrev5((uint32_t)up_row) : (uint32_t)up_row;
                     kp = (f2u(po) & a.key_mask) | (31u ^ prk);
-                    if (herm && !((canon >> up_row) & 1u)) kp = 0u;
+                    if (H && !((canon >> up_row) & 1u)) kp = 0u;
                 }
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b2 >= b1 * a.omt;
+                fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));  // no FMA contraction: same test
                 // a continue decision within tau of the stop threshold is ambiguous too
                 if (EARLY) flagged |= b1 * a.omt < thr;
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)
-                    if (it == 0) B0 = b1;
-                    min_gap = fminf(min_gap, b1 > 0.f ? (b1 - b2) / b1 : 1.f);
-                    min_gap2 = fminf(min_gap2, b1 > 0.f ? (b1 - b2) * rsqrtf(b1 * B0) : 1.f);
+                    const float g = b1 > 0.f ? (b1 - b2) / b1 : 1.f;
+                    min_gap = fminf(min_gap, g);
+                    // first iteration whose decision the guard would flag
+                    if (g < a.tau && min_gap2 > (float)it) min_gap2 = (float)it;
                 }
             }
             // a non-self-mirror selection breaks the exact Hermitian symmetry
-            if (herm) herm = ((bu & 15) == 0) && ((bv & 15) == 0);
+            if (H) herm = ((bu & 15) == 0) && ((bv & 15) == 0);
             // synthesis of the target pixels, Re(gp e^{+2 pi i (bu m + bv n)/32})
             const float2 e = w32_cs[(bu * pm + bv * pn) & 31];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            return true;
+        };
+        bool live = true;  // false after an early stop (the iteration is not counted)
+        while (live && herm && it < a.iterations) {
+            if (step(std::true_type{})) ++it; else live = false;
         }
+        while (live && it < a.iterations) {
+            if (step(std::false_type{})) ++it; else live = false;
+        }
+        flagged |= fl >= 0.f;
         const int done = it;
         if (sel_b)
             for (int j = done + lane; j < a.iterations; j += 32) sel_b[j] = -1;

@@ -34,7 +34,7 @@ def study(name, img, B=4, N=32, I=100, reducer="tree"):
     px = np.where(mask, img, 0.0)
     eng = _lib.default_engine([0])
     nb = frames.n_blocks(H, W, B)
-    p32 = _lib.make_params(B, (N - B) // 2, I, reducer=reducer, precision="fp32_unguarded")
+    p32 = _lib.make_params(B, (N - B) // 2, I, reducer=reducer, precision="fp32_unguarded", argmax="redux")
     out32 = np.empty((H, W), np.float32)
     gaps2 = np.empty((nb, 2), np.float32)
     sel32 = np.empty((nb, I), np.int32)
@@ -46,7 +46,7 @@ def study(name, img, B=4, N=32, I=100, reducer="tree"):
     p64 = _lib.make_params(B, (N - B) // 2, I, reducer=reducer, precision="fp64")
     sel64 = np.empty((nb, I), np.int32)
     out64 = eng.reconstruct(px, mask, p64, sel64, None)
-    gaps, gapsc = gaps2[:, 0], gaps2[:, 1]
+    gaps, gapsc = gaps2[:, 0], gaps2[:, 1]  # min relative gap, first flagged iteration
     eq = np.all(sel32 == sel64, axis=1) | np.all(sel32 == mirror(sel64, N), axis=1)
     flipped = ~eq
     # per-block max error
@@ -72,14 +72,16 @@ def study(name, img, B=4, N=32, I=100, reducer="tree"):
                          "max_err_unflagged": float(left.max()) if left.size else 0.0,
                          "flipped_unflagged": int((flipped & ~flag).sum())})
     res["tau"] = tau_rows
-    rows2 = []
-    for tau in (1e-6, 2e-6, 5e-6, 1e-5, 2e-5, 5e-5, 1e-4):
-        flag = gapsc < tau
-        left = eb[~flag]
-        rows2.append({"tau": tau, "rerun_frac": float(flag.mean()),
-                      "max_err_unflagged": float(left.max()) if left.size else 0.0,
-                      "flipped_unflagged": int((flipped & ~flag).sum())})
-    res["tau_scaled"] = rows2
+    # first flagged iteration (relative gap < guard_tau = 5e-5) of the flagged
+    # blocks: how long a prefix of each re-run is already decided in fp32
+    t0 = gapsc[gapsc < 1e8].astype(np.int64)
+    res["first_flag_iteration"] = {
+        "flagged": int(t0.size), "tau": 5e-5,
+        "quantiles": {str(q): float(np.quantile(t0, q)) for q in (0.1, 0.25, 0.5, 0.75, 0.9)}
+        if t0.size else None,
+        "mean_prefix_fraction": float(t0.mean() / I) if t0.size else None,
+        "histogram_by_decile": np.bincount(np.minimum(t0 * 10 // I, 9), minlength=10).tolist()
+        if t0.size else None}
     print(json.dumps(res), flush=True)
     return res
 
