@@ -289,16 +289,17 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
         float gr = 0.f, gi = 0.f;
         int pu = 0, pv = 0;
         int it = 0;
-        for (; it < a.iterations; ++it) {
+        float fl = -1.f;  // guard test as a float max (see warp32): flagged iff fl >= 0
+        // one iteration; H: Hermitian phase (run as its own loop, see warp32)
+        auto step = [&](auto hconst) -> bool {
+            constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
             const float4 *up = ub + (8 + p - (pu & 7)) * W16_US + ucol16<LT>((v - pv) & 15);
             const bool swap = pu >= 8;
-            if (it == 0) {
+            if (H && it == 0) {
                 pass16<LT, GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
-            } else if (herm) {
-                pass16_update<LT, GUARD, true>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             } else {
-                pass16_update<LT, GUARD, false>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
+                pass16_update<LT, GUARD, H>(re, im, wf2, up, swap, gr, gi, canon, a.key_mask, m1, m2);
             }
             uint32_t kmax;
             int wl;
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
             if (EARLY && b1 < thr) {
                 if (GUARD && b1 >= thr * a.omt) flagged = true;
-                break;
+                return false;
             }
             float4 q;
             switch (j & 3) {
@@ -330,13 +331,22 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             if (GUARD) {
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                flagged |= b2 >= b1 * a.omt;
+                fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));
                 if (EARLY) flagged |= b1 * a.omt < thr;
             }
-            if (herm) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
+            if (H) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
             const float2 e = sm.cs[(bu * pm + bv * pn) & 15];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            return true;
+        };
+        bool live = true;  // false after an early stop (the iteration is not counted)
+        while (live && herm && it < a.iterations) {
+            if (step(std::true_type{})) ++it; else live = false;
         }
+        while (live && it < a.iterations) {
+            if (step(std::false_type{})) ++it; else live = false;
+        }
+        flagged |= fl >= 0.f;
         const int done = it;
         if (sel_b)
             for (int jj = done + lane; jj < a.iterations; jj += 32) sel_b[jj] = -1;
