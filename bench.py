@@ -52,6 +52,20 @@ def flops_per_block(N: int, I: int) -> float:
     return N * N * (12.0 * I + 30.0 * math.log2(N))
 
 
+def cpu_model() -> str:
+    """The host CPU (SURVEY §8d asks the baseline to name it) and os.cpu_count()."""
+    name = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    name = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return f"{name} (os.cpu_count()={os.cpu_count()})"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,6 +232,7 @@ def run_reference(args):
                    "B": B, "N": N, "iterations": I, "rho": 0.7, "gamma": 0.5,
                    "reducer": args.reducer, "image": args.image},
         "cpu_baseline": {"value": fps, "unit": "fps", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"first {k} block rows ({nb} of {total} blocks) per step, "
                                    "extrapolated by block count (per-block cost is "
                                    "data-independent at fixed I)"},
@@ -535,9 +550,15 @@ def main():
         line["quality"] = quality_vs_cpu(original, gpu_rows, cpu_rows)
         total = brows * bcols
         cfps = nb / t / total
+        # SURVEY §8d also asks for the single-thread figure: a short 1-thread sample
+        t1, nb1, k1, _ = cpu_port_sample(sampled, mask, B, N, I, args.reducer,
+                                         min(3.0, args.cpu_seconds), 1)
         line["cpu_baseline"] = {"value": cfps, "unit": "fps", "cores": threads, "kind": "port",
+                                "cpu_model": cpu_model(),
                                 "sample": f"first {k} block rows ({nb} of {total} blocks), "
-                                          f"{t:.1f} s, extrapolated by block count"}
+                                          f"{t:.1f} s, extrapolated by block count",
+                                "single_thread": {"value": nb1 / t1 / total, "unit": "fps",
+                                                  "sample": f"first {k1} block rows, {t1:.1f} s"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
