@@ -592,9 +592,16 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         // One greedy iteration; H: the state is still exactly Hermitian.  The
         // Hermitian phase (a few iterations at most) and the rest run as two
         // loops, so the main loop carries no Hermitian bookkeeping.
+        // synthesis is deferred by one iteration: the cos/sin read of iteration
+        // it-1 is issued before pass it and consumed after it, off the chain
+        int sidx = 0;
+        bool has_pend = false;
         auto step = [&](auto hconst) -> bool {
             constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
+            const bool pend = !H || has_pend;  // the main loop always has one pending
+            float2 e_pend = make_float2(0.f, 0.f);
+            if (pend) e_pend = w32_cs[sidx];
             const bool swap = pu >= 16;
             if (H && it == 0) {
                 pass_x2<LT, GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, a.key_mask, m1, m2);
@@ -609,6 +616,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             uint32_t tid;
             asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
             cross_lane_best<ARGMAX, PK>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
+            // iteration it-1's target-pixel term (gr, gi are still its coefficient)
+            if (pend) acc = fmaf(gr, e_pend.x, fmaf(-gi, e_pend.y, acc));
+            has_pend = false;
             const int bv = LT ? (int)bitrev5((uint32_t)wl) : wl;
             const uint32_t urank = 31u - (kmax & 31u);
             int bu = PK ? (int)(kmax & 15u) : LT ? (int)bitrev5(urank) : (int)urank;  // PK: the pair
@@ -665,7 +675,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                     kp = (f2u(po) & a.key_mask) | (31u ^ prk);
                     if (H && !((canon >> up_row) & 1u)) kp = 0u;
                 }
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? max(m2, kp) : m1);
+                // lane id from the tail's opaque tid read (not a second S2R)
+                const uint32_t k2 = __reduce_max_sync(0xffffffffu,
+                                                      ((int)(tid & 31u) == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));  // no FMA contraction: same test
                 // a continue decision within tau of the stop threshold is ambiguous too
@@ -679,9 +691,10 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             }
             // a non-self-mirror selection breaks the exact Hermitian symmetry
             if (H) herm = ((bu & 15) == 0) && ((bv & 15) == 0);
-            // synthesis of the target pixels, Re(gp e^{+2 pi i (bu m + bv n)/32})
-            const float2 e = w32_cs[(bu * pm + bv * pn) & 31];
-            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            // synthesis of the target pixels, Re(gp e^{+2 pi i (bu m + bv n)/32}),
+            // applied at the start of the next iteration (or after the loops)
+            sidx = (bu * pm + bv * pn) & 31;
+            has_pend = true;
             return true;
         };
         bool live = true;  // false after an early stop (the iteration is not counted)
@@ -692,6 +705,10 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             if (step(std::false_type{})) ++it; else live = false;
         }
         flagged |= fl >= 0.f;
+        if (has_pend) {
+            const float2 e = w32_cs[sidx];
+            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+        }
         const int done = it;
         if (sel_b)
             for (int j = done + lane; j < a.iterations; j += 32) sel_b[j] = -1;
