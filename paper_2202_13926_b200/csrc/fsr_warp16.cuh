@@ -291,9 +291,15 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
         int it = 0;
         float fl = -1.f;  // guard test as a float max (see warp32): flagged iff fl >= 0
         // one iteration; H: Hermitian phase (run as its own loop, see warp32)
+        // synthesis deferred by one iteration (see warp32)
+        int sidx = 0;
+        bool has_pend = false;
         auto step = [&](auto hconst) -> bool {
             constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
+            const bool pend = !H || has_pend;
+            float2 e_pend = make_float2(0.f, 0.f);
+            if (pend) e_pend = sm.cs[sidx];
             const float4 *up = ub + (8 + p - (pu & 7)) * W16_US + ucol16<LT>((v - pv) & 15);
             const bool swap = pu >= 8;
             if (H && it == 0) {
@@ -304,6 +310,8 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             uint32_t kmax;
             int wl;
             cross_lane_best<ARGMAX, GUARD>(m1, kmax, wl, sm.red_key[wid], sm.red_rank[wid]);
+            if (pend) acc = fmaf(gr, e_pend.x, fmaf(-gi, e_pend.y, acc));
+            has_pend = false;
             const uint32_t rank = 31u - (kmax & 31u);
             const int j = LT ? (int)bitrev3(rank) : (int)rank;
             const int bu = (wl & 1) + 2 * j;
@@ -335,8 +343,8 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
                 if (EARLY) flagged |= b1 * a.omt < thr;
             }
             if (H) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
-            const float2 e = sm.cs[(bu * pm + bv * pn) & 15];
-            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            sidx = (bu * pm + bv * pn) & 15;
+            has_pend = true;
             return true;
         };
         bool live = true;  // false after an early stop (the iteration is not counted)
@@ -347,6 +355,10 @@ __global__ void __launch_bounds__(WARPS * 32, 20 / WARPS)
             if (step(std::false_type{})) ++it; else live = false;
         }
         flagged |= fl >= 0.f;
+        if (has_pend) {
+            const float2 e = sm.cs[sidx];
+            acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+        }
         const int done = it;
         if (sel_b)
             for (int jj = done + lane; jj < a.iterations; jj += 32) sel_b[jj] = -1;
