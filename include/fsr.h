@@ -15,6 +15,8 @@
  *                                    pkg/src/fsrkit/_kernels.py:62-149
  *   fsr_params_init / validation  <- fsrkit.core.FsrParams
  *                                    pkg/src/fsrkit/core.py:45-85
+ *   fsr_spatial_oracle            <- fsrkit.oracle.oracle_reconstruct_traced
+ *                                    pkg/src/fsrkit/oracle.py:25-132
  * The reference has no compiled FFI; INTEGRATION.md shows the ctypes binding
  * (the package's own shim, paper_2202_13926_b200/_lib.py) a maintainer of
  * the reference would add.
@@ -138,6 +140,20 @@ int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int
                         double *R, double *G, const double *W, const double *wf,
                         const double *thr, int32_t *sel, double *obj, uint8_t *ties,
                         int32_t *done);
+
+/*
+ * FFT-free spatial-domain oracle (oracle.oracle_reconstruct_traced), an
+ * independent cross-check of the frequency-domain path, supports S <= 16.
+ * Host arrays: signal/spatial [count, S, S] f64 (spatial = decay * mask, the
+ * WeightSet's w), mask [count, S, S] u8, wf [S, S] f64; outputs out
+ * [count, S, S] (mask ? signal : Re model), objectives/selections/ties
+ * [count, iterations], energies [count, iterations + 1].  fp64; the first
+ * maximum in flat order; a tie is > 1 objective within 1e-9 of the maximum.
+ */
+int fsr_spatial_oracle(fsr_engine *eng, int32_t support, int32_t iterations, double gamma,
+                       int64_t count, const double *signal, const uint8_t *mask,
+                       const double *spatial, const double *wf, double *out, double *objectives,
+                       int32_t *selections, uint8_t *ties, double *energies);
 
 /*
  * The callers either side of the loop, on the engine's first device,

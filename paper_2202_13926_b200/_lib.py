@@ -94,6 +94,8 @@ def load():
         L.fsr_reconstruct_device_f32.restype = ctypes.c_int
         L.fsr_iterate_spectra.argtypes = [P, pp, i64, i32, P, P, P, P, P, P, P, P, P]
         L.fsr_iterate_spectra.restype = ctypes.c_int
+        L.fsr_spatial_oracle.argtypes = [P, i32, i32, ctypes.c_double, i64, P, P, P, P, P, P, P, P, P]
+        L.fsr_spatial_oracle.restype = ctypes.c_int
         L.fsr_quarter_sample_device.argtypes = [P, P, i64, i64, i64, ctypes.c_uint64, P, i64, P, i64, P]
         L.fsr_quarter_sample_device.restype = ctypes.c_int
         L.fsr_sq_error_device.argtypes = [P, P, i64, P, i64, i64, i64, P, P]
@@ -107,7 +109,7 @@ def load():
 EXPORTED = ["fsr_params_init", "fsr_params_validate", "fsr_engine_create", "fsr_engine_destroy",
             "fsr_last_error", "fsr_status_string", "fsr_abi_version", "fsr_reconstruct_f64",
             "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_device_f32", "fsr_iterate_spectra",
-            "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats"]
+            "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats", "fsr_spatial_oracle"]
 
 
 def _ptr(a):
@@ -219,6 +221,27 @@ class Engine:
         self._check(self._L.fsr_iterate_spectra(
             self._h, ctypes.byref(params), count, n, _ptr(R), _ptr(G), _ptr(W), _ptr(wf),
             _ptr(thr), _ptr(sel), _ptr(obj), _ptr(ties), _ptr(done)))
+
+    def spatial_oracle(self, signal, mask, spatial, wf, gamma: float, iterations: int):
+        """FFT-free spatial-domain oracle (oracle.py:25-132) on [count, S, S] blocks:
+        returns (out, objectives, selections, ties, energies)."""
+        signal = np.ascontiguousarray(signal, dtype=np.float64)
+        if signal.ndim != 3 or signal.shape[1] != signal.shape[2]:
+            raise ValueError("signal must be [count, S, S]")
+        count, S, _ = signal.shape
+        mask = np.ascontiguousarray(mask, dtype=np.uint8).reshape(count, S, S)
+        spatial = np.ascontiguousarray(spatial, dtype=np.float64).reshape(count, S, S)
+        wf = np.ascontiguousarray(wf, dtype=np.float64).reshape(S, S)
+        it = int(iterations)
+        out = np.empty((count, S, S), np.float64)
+        obj = np.empty((count, max(it, 1)), np.float64)
+        sel = np.empty((count, max(it, 1)), np.int32)
+        ties = np.empty((count, max(it, 1)), np.uint8)
+        en = np.empty((count, it + 1), np.float64)
+        self._check(self._L.fsr_spatial_oracle(
+            self._h, S, it, float(gamma), count, _ptr(signal), _ptr(mask), _ptr(spatial), _ptr(wf),
+            _ptr(out), _ptr(obj), _ptr(sel), _ptr(ties), _ptr(en)))
+        return out, obj[:, :it], sel[:, :it], ties[:, :it].astype(bool), en
 
     def quarter_sample_device(self, d_img, img_pitch, height, width, seed, d_sampled, sampled_pitch,
                               d_mask, mask_pitch, stream=0):

@@ -36,6 +36,7 @@
 #include "fsr_cta64.cuh"
 #include "fsr_pair64.cuh"
 #include "fsr_aux.cuh"
+#include "fsr_spatial.cuh"
 #include "fsr_warp64.cuh"
 
 using namespace fsr;
@@ -1211,6 +1212,67 @@ int fsr_last_stats(const fsr_engine *eng_c, fsr_stats *out) {
     }
     *out = eng->stats;
     return FSR_OK;
+}
+
+int fsr_spatial_oracle(fsr_engine *eng, int32_t support, int32_t iterations, double gamma,
+                       int64_t count, const double *signal, const uint8_t *mask,
+                       const double *spatial, const double *wf, double *out, double *objectives,
+                       int32_t *selections, uint8_t *ties, double *energies) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    if (support < 1 || support > 16)
+        return fail(eng, FSR_EUNSUPPORTED, "spatial oracle supports S <= 16 (got %d)", support);
+    if (iterations < 0) return fail(eng, FSR_EINVAL, "iteration count must be non-negative");
+    if (!(gamma > 0.0 && gamma <= 1.0)) return fail(eng, FSR_EINVAL, "gamma must lie in (0, 1]");
+    if (count < 0 || !signal || !mask || !spatial || !wf || !out || !objectives || !selections ||
+        !ties || !energies)
+        return fail(eng, FSR_EINVAL, "null or empty arrays");
+    if (count == 0) return FSR_OK;
+    if (count > (int64_t)INT32_MAX) return fail(eng, FSR_EINVAL, "too many blocks");
+    Device &d = *eng->devs[0];
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    const size_t n = (size_t)support * support, it = (size_t)std::max(iterations, 1);
+    DevBuf b_sig, b_mask, b_w, b_wf, b_out, b_obj, b_sel, b_ties, b_en;
+    auto cleanup = [&]() {
+        for (DevBuf *b : {&b_sig, &b_mask, &b_w, &b_wf, &b_out, &b_obj, &b_sel, &b_ties, &b_en})
+            b->release();
+    };
+    auto run = [&]() -> int {
+        CUDA_TRY(eng, b_sig.ensure(count * n * sizeof(double)));
+        CUDA_TRY(eng, b_mask.ensure(count * n));
+        CUDA_TRY(eng, b_w.ensure(count * n * sizeof(double)));
+        CUDA_TRY(eng, b_wf.ensure(n * sizeof(double)));
+        CUDA_TRY(eng, b_out.ensure(count * n * sizeof(double)));
+        CUDA_TRY(eng, b_obj.ensure(count * it * sizeof(double)));
+        CUDA_TRY(eng, b_sel.ensure(count * it * sizeof(int32_t)));
+        CUDA_TRY(eng, b_ties.ensure(count * it));
+        CUDA_TRY(eng, b_en.ensure(count * (it + 1) * sizeof(double)));
+        CUDA_TRY(eng, cudaMemcpyAsync(b_sig.p, signal, count * n * sizeof(double), cudaMemcpyHostToDevice, d.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(b_mask.p, mask, count * n, cudaMemcpyHostToDevice, d.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(b_w.p, spatial, count * n * sizeof(double), cudaMemcpyHostToDevice, d.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(b_wf.p, wf, n * sizeof(double), cudaMemcpyHostToDevice, d.stream));
+        SpatialArgs a{b_sig.as<double>(), b_mask.as<uint8_t>(), b_w.as<double>(), b_wf.as<double>(),
+                      b_out.as<double>(), b_obj.as<double>(), b_sel.as<int32_t>(), b_ties.as<uint8_t>(),
+                      b_en.as<double>(), count, support, iterations, gamma};
+        spatial_oracle_kernel<<<(unsigned)count, SP_THREADS, 0, d.stream>>>(a);
+        CUDA_TRY(eng, cudaGetLastError());
+        CUDA_TRY(eng, cudaMemcpyAsync(out, b_out.p, count * n * sizeof(double), cudaMemcpyDeviceToHost, d.stream));
+        if (iterations > 0) {
+            CUDA_TRY(eng, cudaMemcpyAsync(objectives, b_obj.p, count * iterations * sizeof(double),
+                                          cudaMemcpyDeviceToHost, d.stream));
+            CUDA_TRY(eng, cudaMemcpyAsync(selections, b_sel.p, count * iterations * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, d.stream));
+            CUDA_TRY(eng, cudaMemcpyAsync(ties, b_ties.p, count * iterations, cudaMemcpyDeviceToHost, d.stream));
+        }
+        CUDA_TRY(eng, cudaMemcpyAsync(energies, b_en.p, count * (iterations + 1) * sizeof(double),
+                                      cudaMemcpyDeviceToHost, d.stream));
+        CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
+        return FSR_OK;
+    };
+    rc = run();
+    cleanup();
+    return rc;
 }
 
 int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int32_t N,

@@ -195,7 +195,40 @@ def make_kats():
     print("kats:", len(d))
 
 
+def make_spatial_fixtures():
+    """oracle.oracle_reconstruct_traced (the reference's FFT-free spatial-domain
+    oracle, oracle.py:25-132) on quarter-sampled random blocks, the way the
+    reference's acceptance criterion 1 draws them (test_acceptance.py:32-91,
+    conftest.random_quarter_block): S = 4, 8, 16, 32 iterations."""
+    from fsrkit.core import SampledBlock
+    from fsrkit.oracle import oracle_reconstruct_traced
+    rng = np.random.default_rng(1001)
+    d = {}
+    for support, block_size, border in ((4, 2, 1), (8, 2, 3), (16, 4, 6)):
+        params = FsrParams(block=block_size, border=border, rho=0.7, gamma=0.5, iterations=32)
+        cols = {k: [] for k in ("signal", "mask", "spatial", "output", "objectives",
+                                "selections", "ties", "energies")}
+        for trial in range(12):
+            image = GrayImage(rng.uniform(0.0, 255.0, (support, support)))
+            sampled = quarter_sample(image, trial * 31 + support)
+            block = SampledBlock(signal=np.where(sampled.mask, image.pixels, 0.0), mask=sampled.mask)
+            ws = build_weight_set(support, 0.7, block.mask)
+            run = oracle_reconstruct_traced(block, ws, params)
+            for k, v in (("signal", block.signal), ("mask", block.mask), ("spatial", ws.spatial),
+                         ("output", run.output), ("objectives", run.objectives),
+                         ("selections", run.selections), ("ties", run.ties),
+                         ("energies", run.energies)):
+                cols[k].append(np.asarray(v))
+        for k, v in cols.items():
+            d[f"s{support}_{k}"] = np.stack(v)
+        d[f"s{support}_wf"] = frequency_weight(support)
+        d[f"s{support}_params"] = np.array([block_size, border, 32], np.int64)
+    np.savez_compressed(os.path.join(HERE, "spatial_oracle.npz"), **d)
+    print("spatial oracle:", len(d))
+
+
 if __name__ == "__main__":
     make_kats()
     make_loop_fixtures()
     make_image_fixtures()
+    make_spatial_fixtures()

@@ -127,3 +127,43 @@ def test_mirror_comparator():
     assert counts == {"equal": 0, "mirror": 1, "diverged": 0}
     counts, _ = oracle.compare_sequences(a, a, s)
     assert counts["equal"] == 1
+
+
+def _spatial_restated(signal, w, wf, gamma, iterations):
+    """numpy restatement of fsrkit.oracle._step (oracle.py:66-98): explicit basis
+    images, direct-summation projection, first maximum, recompute from scratch."""
+    s = signal.shape[0]
+    t = np.arange(s * s)
+    k, l = t // s, t % s
+    phi = np.exp(1j * 2.0 * np.pi / s * (np.outer(k, k) + np.outer(l, l)))
+    model = np.zeros((s, s), complex)
+    rw = signal * w
+    w00 = float(np.sum(w))
+    sels, objs = [], []
+    for _ in range(iterations):
+        proj = phi.conj() @ rw.ravel()
+        obj = wf.ravel() * (proj.real ** 2 + proj.imag ** 2)
+        ti = int(np.argmax(obj))
+        sels.append(ti)
+        objs.append(float(obj[ti]))
+        p = proj[ti] / w00
+        model = model + (gamma * p) * phi[ti].reshape(s, s)
+        rw = (signal - model) * w
+    return np.array(sels), np.array(objs)
+
+
+def test_spatial_oracle_golden_restated():
+    """The GPU spatial oracle's fixtures (fsrkit.oracle output) pinned by a plain
+    numpy restatement of the same algorithm (S = 4 and 8, 32 iterations)."""
+    from conftest import load_golden
+    d = load_golden("spatial_oracle.npz")
+    for s in (4, 8):
+        k = f"s{s}_"
+        for b in range(4):
+            sel, obj = _spatial_restated(d[k + "signal"][b], d[k + "spatial"][b], d[k + "wf"], 0.5, 32)
+            ref_sel, ref_obj = d[k + "selections"][b], d[k + "objectives"][b]
+            diff = np.nonzero(sel != ref_sel)[0]
+            upto = 32 if diff.size == 0 else int(diff[0]) + 1
+            np.testing.assert_allclose(obj[:upto], ref_obj[:upto], rtol=1e-9, atol=0)
+            if diff.size:  # a different branch only at a recorded tie
+                assert d[k + "ties"][b][diff[0]]
