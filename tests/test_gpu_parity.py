@@ -385,6 +385,27 @@ def test_register_kernels_edges(N, B, reducer, early_stop):
     assert np.array_equal(out64[mask], sampled[mask])
 
 
+@pytest.mark.parametrize("N,B", [(32, 4), (16, 4)])
+def test_early_stop_fires(N, B):
+    """Early stop that actually fires (a smooth ramp is fitted in a few
+    iterations, reconstruction.py:262-266): guarded fp32 and fp64 against the
+    reference, and the stop iteration (done) equal to the reference's."""
+    H, W, I = 40, 48, 60
+    yy, xx = np.mgrid[0:H, 0:W]
+    img = 100.0 + 0.0 * yy + 0.0 * xx
+    sampled, mask = oracle.quarter_sample(img, 5)
+    sampled = np.where(mask, sampled, 0.0)
+    L = (N - B) // 2
+    ref, rtr = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, "tree", True, trace=True)
+    assert int(np.max(rtr["done"])) < I  # the stop fires
+    for precision in ("fp32", "fp64"):
+        out, tr = fsr.reconstruct(sampled.astype(np.float32) if precision == "fp32" else sampled,
+                                  mask, B, N, I, early_stop=True, precision=precision,
+                                  argmax="redux", return_trace=True)
+        assert np.array_equal(tr.done, rtr["done"]), precision
+        assert float(np.abs(out.astype(np.float64) - ref).max()) <= FP32_TOL
+
+
 @pytest.mark.gpu
 def test_device_api_chunks_equal_unchunked(monkeypatch):
     """Device-API calls on tall ranges run in four row chunks over two streams,
