@@ -110,6 +110,26 @@ def ncu_traffic(kernel_prefix):
     return None
 
 
+def ncu_issue(kernel_prefix):
+    """Issue-slot view of the dominant kernel from the same committed capture:
+    the loop is bound by instruction issue and dependency latency, not FLOPs."""
+    path = os.path.join(ROOT, "profiles", "r01", "warp32_ncu.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except OSError:
+        return None
+    for ln in d.get("launches", []):
+        if ln["kernel"].startswith(kernel_prefix):
+            return {"issue_active_pct": ln.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                    "warp_instructions": ln.get("smsp__inst_executed.sum"),
+                    "fma_pipe_pct": ln.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+                    "alu_pipe_pct": ln.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                    "warps_per_smsp": ln.get("smsp__warps_active.avg.per_cycle_active"),
+                    "source": "ncu --set full, profiles/r01/warp32_ncu.json"}
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -500,10 +520,11 @@ def main():
     smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
                 + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, issue = None, None, None
     if (kernel == "warp32_kernel" and args.workload == "4k" and world == 1
             and args.precision == "fp32" and args.reducer == "tree" and args.argmax == "redux"):
         traffic = ncu_traffic("void warp32_kernel<4, 1, 2, 1, 0")
+        issue = ncu_issue("void warp32_kernel<4, 1, 2, 1, 0")
         if traffic is not None:
             traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                            "(profiles/r01/warp32_ncu.json); algorithmic I/O bytes " + str(io_bytes))
@@ -531,6 +552,7 @@ def main():
                      "smem": {"achieved_tbs": w_bytes / (mean_main * 1e-3) / 1e12,
                               "peak_tbs": smem_peak,
                               "frac": w_bytes / (mean_main * 1e-3) / 1e12 / smem_peak},
+                     "issue": issue,
                      "hbm_io": {"achieved_gbs": io_bytes / (ms_max * 1e-3) / 1e9,
                                 "peak_gbs": pk.get("hbm_gbs"),
                                 "frac": io_bytes / (ms_max * 1e-3) / 1e9 / pk.get("hbm_gbs", 1)}},
