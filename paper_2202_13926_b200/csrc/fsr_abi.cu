@@ -525,6 +525,24 @@ bool cta64_eligible(const fsr_params *p) {
            p->reducer == FSR_REDUCER_LINEAR && p->precision != FSR_PREC_FP64;
 }
 
+bool cta64d_eligible(const fsr_params *p) {
+    return p->block + 2 * p->border == 64 && p->block * p->block <= C64_THREADS &&
+           p->reducer == FSR_REDUCER_LINEAR;
+}
+
+template <typename IO>
+int launch_cta64d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
+                  cudaStream_t st) {
+    auto k = cta64d_kernel<IO>;
+    const size_t smem = sizeof(C64dSmem);
+    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(want_blocks, 1), (int64_t)d.sms);
+    k<<<grid, C64_THREADS, smem, st>>>(a);
+    d.launches++;
+    CUDA_TRY(eng, cudaGetLastError());
+    return FSR_OK;
+}
+
 bool warp16d_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 16 && p->block * p->block <= 32;
 }
@@ -590,6 +608,14 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = launch_warp16d<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          nblocks, st)))
                 return rc;
+            CUDA_TRY(eng, cudaEventRecord(ev_end, st));
+        } else if (p->precision == FSR_PREC_FP64 && cta64d_eligible(p)) {
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, first, nblocks, tab, sel, done,
+                                               &ctr->empty_count, empty_list);
+            if ((rc = launch_cta64d<IO>(eng, d, a, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
@@ -695,15 +721,15 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         }
         CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         if (guarded && fast64) {
-            // fp64 re-run of ambiguous blocks on the exact generic kernel (list mode)
+            // fp64 re-run of ambiguous blocks on the N=64 fp64 kernel (list mode)
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
-            ImageArgs<double, IO> r{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
-                                    p->block, p->border, N, p->iterations, bcols, 0, 0,
-                                    d.rerun_list.as<int32_t>(), &ctr->rerun_count, p->gamma,
-                                    p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel, done,
-                                    &ctr->ticket /* empties already counted */, nullptr};
-            if ((rc = launch_generic(eng, d, r, d.sms * 8, st))) return rc;
+            Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, 0, 0, tab, sel, done,
+                                               &ctr->ticket /* empties already counted */, nullptr);
+            r.list = d.rerun_list.as<int32_t>();
+            r.list_count = &ctr->rerun_count;
+            if ((rc = launch_cta64d<IO>(eng, d, r, (int64_t)d.sms, st))) return rc;
         } else if (guarded && fast16) {
             // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)
             Tables<double> tab;

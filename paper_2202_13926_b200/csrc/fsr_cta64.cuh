@@ -29,6 +29,7 @@
 #pragma once
 
 #include "fsr_warp32.cuh"
+#include "fsr_pair64.cuh"  // Pair64Args (the fp64 kernels' argument block)
 
 namespace fsr {
 
@@ -375,6 +376,223 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 a.out[y * a.out_pitch + xx] = a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
         }
         __syncthreads();  // the region is rewritten by the next block's gather
+    }
+}
+
+// ---------------------------------------------------------------------------
+// cta64d: the N = 64 loop in fp64 -- the fp64 (validation) precision for N = 64
+// and the re-run of the guarded fp32 kernel's flagged blocks (list mode), in
+// place of the CTA-per-block generic kernel.  Same thread map as cta64 (thread
+// (v, h) owns column v, rows 16h + i and 16h + i + 32), R register-resident in
+// fp64 (128 registers), the weight spectrum W as a plain 64 x 64 complex
+// double table (64 KiB) NEXT TO the FFT tile, so the split writes W while the
+// tile is still being read (no register staging); one CTA per SM.
+// Keys: the fp64 objective wf * fma(re, re, im*im) with its 6 low mantissa bits
+// replaced by 63 - u (comparisons exact to 2^-46 relative, as pair64's 2^-47),
+// warp max by a redux on the high word (the low word only breaks exact ties
+// there), then the 4 warps through a double-buffered slot: max key, then the
+// lowest warp = lowest column -- the linear reducer's order (_kernels.py:52-59).
+// ---------------------------------------------------------------------------
+struct __align__(16) C64dSlot {
+    unsigned long long key;
+    double cre, cim;  // R[u*][v*] of the warp's best bin
+    int32_t lane;
+    int32_t pad[3];
+};
+
+struct C64dSmem {
+    double2 tile[64 * C64_TS];  // fp64 FFT tile (66 560 B)
+    double2 W[64 * 64];         // W[u][v] (65 536 B)
+    double2 tw[64];             // e^{-2 pi i j / 64}
+    double2 cs[64];             // (cos, sin)(2 pi j / 64)
+    C64dSlot slot[2][4];
+    double esum[4];
+};
+
+__device__ __forceinline__ unsigned long long c64d_key(double o, int u) {
+    return ((unsigned long long)__double_as_longlong(o) & ~63ull) | (unsigned long long)(63 - u);
+}
+
+template <bool UPDATE>
+__device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], double2 (&rh)[16],
+                                                        const double (&wl)[16], const double (&wh)[16],
+                                                        const double2 *Wt, int h, int v, int pu, int pv,
+                                                        double gr, double gi) {
+    unsigned long long m = 0ull;
+    const int col = (v - pv) & 63;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int u = 16 * h + i;
+        double2 a = rl[i], b = rh[i];
+        if (UPDATE) {
+            const double2 wa = Wt[((u - pu) & 63) * 64 + col];
+            const double2 wb = Wt[((u + 32 - pu) & 63) * 64 + col];
+            a.x = fma(-gr, wa.x, a.x);
+            a.x = fma(gi, wa.y, a.x);
+            a.y = fma(-gr, wa.y, a.y);
+            a.y = fma(-gi, wa.x, a.y);
+            b.x = fma(-gr, wb.x, b.x);
+            b.x = fma(gi, wb.y, b.x);
+            b.y = fma(-gr, wb.y, b.y);
+            b.y = fma(-gi, wb.x, b.y);
+            rl[i] = a;
+            rh[i] = b;
+        }
+        const unsigned long long ka = c64d_key(fma(a.x, a.x, a.y * a.y) * wl[i], u);
+        const unsigned long long kb = c64d_key(fma(b.x, b.x, b.y * b.y) * wh[i], u + 32);
+        m = max(m, max(ka, kb));
+    }
+    return m;
+}
+
+template <typename IO>
+__global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    C64dSmem &sm = *reinterpret_cast<C64dSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int h = tid >> 6, v = tid & 63;
+    if (tid < 64) {
+        double sn, cn;
+        sincospi(tid / 32.0, &sn, &cn);
+        sm.tw[tid] = make_double2(cn, -sn);
+        sm.cs[tid] = make_double2(cn, sn);
+    }
+    // frequency prior of the thread's 32 bins (weights.py:40-56)
+    double wl[16], wh[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        wl[i] = __ldg(a.wf + (16 * h + i) * 64 + v);
+        wh[i] = __ldg(a.wf + (16 * h + i + 32) * 64 + v);
+    }
+    __syncthreads();
+    const int64_t nblocks = a.list_count ? (int64_t)*a.list_count : a.nblocks;
+    for (int64_t bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
+        const int64_t bid = a.list ? (int64_t)a.list[bi] : a.first + bi;
+        const int64_t brow = bid / a.bcols, bcol = bid - brow * a.bcols;
+        const int64_t r0 = brow * a.B, c0 = bcol * a.B;
+        const int64_t wr0 = r0 - a.L, wc0 = c0 - a.L;
+        // ---- gather + spatial weight (sampling.py:93-107, weights.py:18-37)
+        double energy = 0.0;
+        {
+            const int64_t x = wc0 + v;
+            const bool xin = x >= 0 && x < a.W;
+#pragma unroll 4
+            for (int k = 0; k < 32; ++k) {
+                const int r = 32 * h + k;
+                const int64_t y = wr0 + r;
+                double f = 0.0, w = 0.0;
+                if (xin && y >= 0 && y < a.H && a.mask[y * a.mask_pitch + x]) {
+                    f = (double)a.px[y * a.px_pitch + x];
+                    w = __ldg(a.decay + r * 64 + v);
+                }
+                sm.tile[r * C64_TS + v] = make_double2(f * w, w);
+                energy = fma(f * f, w, energy);
+            }
+        }
+        __syncthreads();
+        c64_fft_lines(sm.tile, C64_TS, 1, sm.tw, tid);  // rows
+        c64_fft_lines(sm.tile, 1, C64_TS, sm.tw, tid);  // columns
+        // ---- Hermitian split: R to registers, W to its own table
+        double2 rl[16], rh[16];
+        {
+            const int pv_ = c64_pos(v), pmv = c64_pos((64 - v) & 63);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int u = 16 * h + i + 32 * hh, nu = (64 - u) & 63;
+                    const double2 z = sm.tile[c64_pos(u) * C64_TS + pv_];
+                    const double2 zm = sm.tile[c64_pos(nu) * C64_TS + pmv];
+                    const double2 r = make_double2((z.x + zm.x) * 0.5, (z.y - zm.y) * 0.5);
+                    sm.W[u * 64 + v] = make_double2((z.y + zm.y) * 0.5, (zm.x - z.x) * 0.5);
+                    if (hh == 0) rl[i] = r; else rh[i] = r;
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
+        if (lane == 0) sm.esum[wid] = energy;
+        __syncthreads();
+        const double w00 = sm.W[0].x;  // W[0][0] = sum of the weights
+        int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        if (!(w00 > 0.0)) {  // empty support (reconstruction.py:272-275)
+            if (tid == 0) {
+                unsigned slot = atomicAdd(a.empty_count, 1u);
+                if (a.empty_list) a.empty_list[slot] = (int32_t)bid;
+                if (a.done) a.done[bid] = 0;
+            }
+            if (sel_b)
+                for (int it = tid; it < a.iterations; it += C64_THREADS) sel_b[it] = -1;
+            __syncthreads();
+            continue;
+        }
+        const double thr =
+            a.early_stop ? 1e-12 * (sm.esum[0] + sm.esum[1] + sm.esum[2] + sm.esum[3]) : 0.0;
+        const double ginv = a.gamma / w00;
+        const int pm_ = a.L + tid / a.B, pn_ = a.L + tid % a.B;
+        double acc = 0.0, gr = 0.0, gi = 0.0;
+        int pu = 0, pv = 0, it = 0;
+        for (; it < a.iterations; ++it) {
+            const unsigned long long kb =
+                it == 0 ? c64d_pass<false>(rl, rh, wl, wh, sm.W, h, v, pu, pv, gr, gi)
+                        : c64d_pass<true>(rl, rh, wl, wh, sm.W, h, v, pu, pv, gr, gi);
+            // phase 1: warp max of the u64 keys (redux on the high word)
+            const uint32_t hi = (uint32_t)(kb >> 32);
+            const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+            uint32_t cand = __ballot_sync(0xffffffffu, hi == mh);
+            if (__popc(cand) > 1) {
+                const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? (uint32_t)kb : 0u);
+                cand = __ballot_sync(0xffffffffu, hi == mh && (uint32_t)kb == ml);
+            }
+            const int wl_ = __ffs(cand) - 1;
+            C64dSlot *sl = sm.slot[it & 1];
+            if (lane == wl_) {
+                const int u = 63 - (int)(kb & 63ull);
+                double2 c = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {  // one thread: a predicated sweep
+                    if (u == 16 * h + i) c = rl[i];
+                    if (u == 16 * h + i + 32) c = rh[i];
+                }
+                sl[wid].key = kb;
+                sl[wid].cre = c.x;
+                sl[wid].cim = c.y;
+                sl[wid].lane = lane;
+            }
+            __syncthreads();
+            // phase 2: the 4 warps (max key, then the lowest warp)
+            unsigned long long best = sl[0].key;
+            int bw = 0;
+#pragma unroll
+            for (int w = 1; w < 4; ++w)
+                if (sl[w].key > best) {
+                    best = sl[w].key;
+                    bw = w;
+                }
+            const int bu = 63 - (int)(best & 63ull);
+            const int bv = (bw * 32 + sl[bw].lane) & 63;
+            const double b1 = __longlong_as_double((long long)(best & ~63ull));
+            if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
+            if (b1 < thr) break;  // thr == 0 unless early stop is on
+            gr = sl[bw].cre * ginv;
+            gi = sl[bw].cim * ginv;
+            pu = bu;
+            pv = bv;
+            const double2 e = sm.cs[(bu * pm_ + bv * pn_) & 63];
+            acc = fma(gr, e.x, fma(-gi, e.y, acc));
+        }
+        const int done = it;
+        if (sel_b)
+            for (int jj = done + tid; jj < a.iterations; jj += C64_THREADS) sel_b[jj] = -1;
+        if (tid == 0 && a.done) a.done[bid] = done;
+        if (tid < a.B * a.B) {
+            const int m = tid / a.B, n = tid % a.B;
+            const int64_t y = r0 + m, xx = c0 + n;
+            if (y < a.H && xx < a.W)
+                a.out[y * a.out_pitch + xx] =
+                    a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : (IO)acc;
+        }
+        __syncthreads();  // tile / W / slots are rewritten by the next block
     }
 }
 
