@@ -84,7 +84,7 @@ struct Device {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
     DevBuf px, mask, out, sel, done, empty_list, rerun_list, counters;
-    DevBuf R, G, W, wf, thr, obj, ties, partials;
+    DevBuf R, G, W, wf, thr, obj, ties, partials, c64scratch;
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
@@ -536,8 +536,14 @@ int launch_cta64d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t w
     auto k = cta64d_kernel<IO>;
     const size_t smem = sizeof(C64dSmem);
     CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = (int)std::min<int64_t>(std::max<int64_t>(want_blocks, 1), (int64_t)d.sms);
-    k<<<grid, C64_THREADS, smem, st>>>(a);
+    int per_sm = 0;
+    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C64_THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    const int grid = (int)std::min<int64_t>(std::max<int64_t>(want_blocks, 1), (int64_t)d.sms * per_sm);
+    CUDA_TRY(eng, d.c64scratch.ensure((size_t)grid * 4096 * sizeof(double2)));
+    Pair64Args<IO> b = a;
+    b.scratch = d.c64scratch.as<double2>();
+    k<<<grid, C64_THREADS, smem, st>>>(b);
     d.launches++;
     CUDA_TRY(eng, cudaGetLastError());
     return FSR_OK;
@@ -1063,7 +1069,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
         cudaSetDevice(d.id);
         cudaStreamSynchronize(d.stream);
         for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list,
-                          &d.counters, &d.R, &d.G, &d.W, &d.wf, &d.thr, &d.obj, &d.ties})
+                          &d.counters, &d.R, &d.G, &d.W, &d.wf, &d.thr, &d.obj, &d.ties, &d.c64scratch})
             b->release();
         for (auto &kv : d.tables) {
             kv.second->f64.release();
@@ -1072,7 +1078,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
         for (auto &ln : d.lanes) {
             cudaStreamSynchronize(ln->stream);
             for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->empty_list,
-                              &ln->rerun_list, &ln->counters})
+                              &ln->rerun_list, &ln->counters, &ln->c64scratch, &ln->partials})
                 b->release();
             for (auto &kv : ln->tables) {
                 kv.second->f64.release();

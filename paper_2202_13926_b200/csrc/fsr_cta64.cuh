@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
 // (v, h) owns column v, rows 16h + i and 16h + i + 32), R register-resident in
 // fp64 (128 registers), the weight spectrum W as a plain 64 x 64 complex
 // double table (64 KiB) NEXT TO the FFT tile, so the split writes W while the
-// tile is still being read (no register staging); one CTA per SM.
+// tile is still being read: W goes to a per-CTA global staging buffer (L2)
+// and is copied into the tile's space once the tile is consumed, so a CTA
+// needs 66.5 KiB of shared memory and two CTAs share an SM.
 // Keys: the fp64 objective wf * fma(re, re, im*im) with its 6 low mantissa bits
 // replaced by 63 - u (comparisons exact to 2^-46 relative, as pair64's 2^-47),
 // warp max by a redux on the high word (the low word only breaks exact ties
@@ -401,8 +403,7 @@ struct __align__(16) C64dSlot {
 };
 
 struct C64dSmem {
-    double2 tile[64 * C64_TS];  // fp64 FFT tile (66 560 B)
-    double2 W[64 * 64];         // W[u][v] (65 536 B)
+    double2 tile[64 * C64_TS];  // fp64 FFT tile (66 560 B), then W[u][v] (65 536 B)
     double2 tw[64];             // e^{-2 pi i j / 64}
     double2 cs[64];             // (cos, sin)(2 pi j / 64)
     C64dSlot slot[2][4];
@@ -446,7 +447,7 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
 }
 
 template <typename IO>
-__global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a) {
+__global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C64dSmem &sm = *reinterpret_cast<C64dSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -492,7 +493,8 @@ __global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a
         __syncthreads();
         c64_fft_lines(sm.tile, C64_TS, 1, sm.tw, tid);  // rows
         c64_fft_lines(sm.tile, 1, C64_TS, sm.tw, tid);  // columns
-        // ---- Hermitian split: R to registers, W to its own table
+        // ---- Hermitian split: R to registers, W staged through global memory
+        double2 *gW = a.scratch + (int64_t)blockIdx.x * 4096;
         double2 rl[16], rh[16];
         {
             const int pv_ = c64_pos(v), pmv = c64_pos((64 - v) & 63);
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a
                     const double2 z = sm.tile[c64_pos(u) * C64_TS + pv_];
                     const double2 zm = sm.tile[c64_pos(nu) * C64_TS + pmv];
                     const double2 r = make_double2((z.x + zm.x) * 0.5, (z.y - zm.y) * 0.5);
-                    sm.W[u * 64 + v] = make_double2((z.y + zm.y) * 0.5, (zm.x - z.x) * 0.5);
+                    gW[u * 64 + v] = make_double2((z.y + zm.y) * 0.5, (zm.x - z.x) * 0.5);
                     if (hh == 0) rl[i] = r; else rh[i] = r;
                 }
             }
@@ -512,8 +514,12 @@ __global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
         if (lane == 0) sm.esum[wid] = energy;
+        __syncthreads();  // the tile is consumed: W moves into its space
+        double2 *Wt = sm.tile;
+#pragma unroll 4
+        for (int e = tid; e < 4096; e += C64_THREADS) Wt[e] = gW[e];
         __syncthreads();
-        const double w00 = sm.W[0].x;  // W[0][0] = sum of the weights
+        const double w00 = Wt[0].x;  // W[0][0] = sum of the weights
         int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.0)) {  // empty support (reconstruction.py:272-275)
             if (tid == 0) {
@@ -534,8 +540,8 @@ __global__ void __launch_bounds__(C64_THREADS, 1) cta64d_kernel(Pair64Args<IO> a
         int pu = 0, pv = 0, it = 0;
         for (; it < a.iterations; ++it) {
             const unsigned long long kb =
-                it == 0 ? c64d_pass<false>(rl, rh, wl, wh, sm.W, h, v, pu, pv, gr, gi)
-                        : c64d_pass<true>(rl, rh, wl, wh, sm.W, h, v, pu, pv, gr, gi);
+                it == 0 ? c64d_pass<false>(rl, rh, wl, wh, Wt, h, v, pu, pv, gr, gi)
+                        : c64d_pass<true>(rl, rh, wl, wh, Wt, h, v, pu, pv, gr, gi);
             // phase 1: warp max of the u64 keys (redux on the high word)
             const uint32_t hi = (uint32_t)(kb >> 32);
             const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);

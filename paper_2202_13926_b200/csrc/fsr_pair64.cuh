@@ -53,6 +53,7 @@ struct Pair64Args {
     int32_t *done;
     unsigned int *empty_count;
     int32_t *empty_list;
+    double2 *scratch;               // cta64d: per-CTA 64 KiB staging of W (null elsewhere)
 };
 
 struct __align__(16) PairSlot {
