@@ -78,7 +78,7 @@ def main():
                         "rerun_fraction": stats["rerun_blocks"] / max(1, rows * bcols),
                         "kernel": {(32, False): "warp32 (+pair64 re-runs)", (32, True): "pair64",
                                    (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d",
-                                   (64, False): "cta64, in-warp redux (+generic fp64 re-runs)"}
+                                   (64, False): "cta64, in-warp redux (+cta64d fp64 re-runs)"}
                                   .get((N, args.precision == "fp64"), "generic")}
                 print(json.dumps(line), flush=True)
 
