@@ -28,16 +28,23 @@
 //              folds two bins per op), then a cross-lane step: __shfl_xor_sync
 //              butterfly on (key, lane rank) (the paper's register argmax), or
 //              redux.sync + ballot, or a shared-memory tree (the paper's
-//              comparison point) -- template ARGMAX.
+//              comparison point) -- template ARGMAX.  Guarded production mode
+//              (PK): one key per row pair (the pair's larger objective tagged
+//              with the pair index), lanes in natural column order, any
+//              maximal lane wins (FLO) -- every near-tie is re-run in fp64
+//              with the reference's tie order, so the kernel never needs it;
+//              the winning pair is fetched by one brx.idx jump.
 //   synthesis  lanes p < B*B accumulate g(m,n) += Re(gp e^{2 pi i(u m + v n)/32})
-//              every iteration (no inverse FFT, only the B x B target pixels),
-//              then merge (known pixels copied) and stitch.
+//              (no inverse FFT, only the B x B target pixels), deferred by one
+//              iteration so the cos/sin read overlaps the next pass, then merge
+//              (known pixels copied) and stitch.
 //   guard      fp32 near-tie guard: per-lane top-2 keys give the best and the
 //              second-best objective of every iteration (excluding the exact
 //              conjugate mirror while the state is exactly Hermitian); a block
 //              whose relative gap ever drops below tau is queued for an fp64
 //              re-run, which is what makes fp32 production match the fp64
-//              reference within tolerance.
+//              reference within tolerance.  The Hermitian phase
+//              (a few iterations) runs as its own loop.
 #pragma once
 
 #include <cuda.h>  // CUtensorMap
