@@ -514,8 +514,14 @@ def main():
     lanes = 64 if fp64 else 128  # B200: DFMA at half the FFMA rate
     peak_fl = 148 * lanes * 2 * clk_hz / 1e12
     fast = N == 32 and B * B <= 32
-    kernel = (("pair64_kernel" if args.kernel == "pair" else "warp64_kernel") if fp64
-              else "warp32_kernel") if fast else "image_generic_kernel"
+    if N == 32 and B * B <= 32:
+        kernel = ("warp64_kernel" if args.kernel == "warp" else "pair64_kernel") if fp64 else "warp32_kernel"
+    elif N == 16 and B * B <= 32:
+        kernel = "warp16d_kernel" if fp64 else "warp16_kernel"
+    elif N == 64 and B * B <= 128 and args.reducer == "linear":
+        kernel = "cta64d_kernel" if fp64 else "cta64_kernel"
+    else:
+        kernel = "image_generic_kernel"
     w_bytes = my_blocks * I * N * N * (16 if fp64 else 8)  # W read once per bin per iteration
     smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
