@@ -285,18 +285,17 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         float acc = 0.f, gr = 0.f, gi = 0.f;
         bool herm = true, flagged = false;
         int pu = 0, pv = 0, it = 0;
-        for (; it < a.iterations; ++it) {
+        // one iteration; H: Hermitian phase, run as its own loop (see warp32)
+        auto step = [&](auto hconst) -> bool {
+            constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
             const float4 *up = ub + (32 + 16 * h - (pu & 31)) * 64 + ((v - pv) & 63);
             const bool swap = pu >= 32;
-            if (it == 0)
+            if (H && it == 0)
                 pass64<GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
-            else if (herm)
-                swap ? pass64<GUARD, true, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
-                     : pass64<GUARD, true, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
             else
-                swap ? pass64<GUARD, false, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
-                     : pass64<GUARD, false, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+                swap ? pass64<GUARD, H, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
+                     : pass64<GUARD, H, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
             // phase 1: in-warp argmax, coefficient of the warp's best bin
             const uint32_t kw = __reduce_max_sync(0xffffffffu, m1);
             const int wl = __ffs(__ballot_sync(0xffffffffu, m1 == kw)) - 1;
@@ -344,7 +343,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
             if (b1 < thr) {
                 if (GUARD && b1 >= thr * one_minus_tau) flagged = true;
-                break;
+                return false;
             }
             gr = sl[bw].cre * ginv;
             gi = sl[bw].cim * ginv;
@@ -355,9 +354,17 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 flagged |= b2 >= b1 * one_minus_tau;
                 flagged |= b1 * one_minus_tau < thr;
             }
-            if (herm) herm = ((bu & 31) == 0) && ((bv & 31) == 0);
+            if (H) herm = ((bu & 31) == 0) && ((bv & 31) == 0);
             const float2 e = sm.cs[(bu * pm_ + bv * pn_) & 63];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
+            return true;
+        };
+        bool live = true;  // false after an early stop (the iteration is not counted)
+        while (live && herm && it < a.iterations) {
+            if (step(std::true_type{})) ++it; else live = false;
+        }
+        while (live && it < a.iterations) {
+            if (step(std::false_type{})) ++it; else live = false;
         }
         const int done = it;
         if (sel_b)
