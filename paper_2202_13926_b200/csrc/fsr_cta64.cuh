@@ -453,6 +453,50 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
     return m;
 }
 
+// Row pair i = u mod 16 of this thread in fp64, (rl[i], rh[i]), by one indirect branch
+// (brx.idx over a 16-entry jump table); i must be warp-uniform.
+__device__ __forceinline__ void c64d_pick(const double2 (&rl)[16], const double2 (&rh)[16], int i,
+                                          double2 &lo, double2 &hi) {
+    asm volatile(
+        "{\n ts%=: .branchtargets L0_%=, L1_%=, L2_%=, L3_%=, L4_%=, L5_%=, L6_%=, L7_%=, L8_%=, L9_%=, L10_%=, L11_%=, L12_%=, L13_%=, L14_%=, L15_%=;\n"
+        " brx.idx %4, ts%=;\n"
+        " L0_%=: mov.f64 %0, %5; mov.f64 %1, %6; mov.f64 %2, %7; mov.f64 %3, %8; bra.uni Le_%=;\n"
+        " L1_%=: mov.f64 %0, %9; mov.f64 %1, %10; mov.f64 %2, %11; mov.f64 %3, %12; bra.uni Le_%=;\n"
+        " L2_%=: mov.f64 %0, %13; mov.f64 %1, %14; mov.f64 %2, %15; mov.f64 %3, %16; bra.uni Le_%=;\n"
+        " L3_%=: mov.f64 %0, %17; mov.f64 %1, %18; mov.f64 %2, %19; mov.f64 %3, %20; bra.uni Le_%=;\n"
+        " L4_%=: mov.f64 %0, %21; mov.f64 %1, %22; mov.f64 %2, %23; mov.f64 %3, %24; bra.uni Le_%=;\n"
+        " L5_%=: mov.f64 %0, %25; mov.f64 %1, %26; mov.f64 %2, %27; mov.f64 %3, %28; bra.uni Le_%=;\n"
+        " L6_%=: mov.f64 %0, %29; mov.f64 %1, %30; mov.f64 %2, %31; mov.f64 %3, %32; bra.uni Le_%=;\n"
+        " L7_%=: mov.f64 %0, %33; mov.f64 %1, %34; mov.f64 %2, %35; mov.f64 %3, %36; bra.uni Le_%=;\n"
+        " L8_%=: mov.f64 %0, %37; mov.f64 %1, %38; mov.f64 %2, %39; mov.f64 %3, %40; bra.uni Le_%=;\n"
+        " L9_%=: mov.f64 %0, %41; mov.f64 %1, %42; mov.f64 %2, %43; mov.f64 %3, %44; bra.uni Le_%=;\n"
+        " L10_%=: mov.f64 %0, %45; mov.f64 %1, %46; mov.f64 %2, %47; mov.f64 %3, %48; bra.uni Le_%=;\n"
+        " L11_%=: mov.f64 %0, %49; mov.f64 %1, %50; mov.f64 %2, %51; mov.f64 %3, %52; bra.uni Le_%=;\n"
+        " L12_%=: mov.f64 %0, %53; mov.f64 %1, %54; mov.f64 %2, %55; mov.f64 %3, %56; bra.uni Le_%=;\n"
+        " L13_%=: mov.f64 %0, %57; mov.f64 %1, %58; mov.f64 %2, %59; mov.f64 %3, %60; bra.uni Le_%=;\n"
+        " L14_%=: mov.f64 %0, %61; mov.f64 %1, %62; mov.f64 %2, %63; mov.f64 %3, %64; bra.uni Le_%=;\n"
+        " L15_%=: mov.f64 %0, %65; mov.f64 %1, %66; mov.f64 %2, %67; mov.f64 %3, %68; bra.uni Le_%=;\n"
+        " Le_%=:\n}"
+        : "=d"(lo.x), "=d"(lo.y), "=d"(hi.x), "=d"(hi.y)
+        : "r"(i & 15),
+          "d"(rl[0].x), "d"(rl[0].y), "d"(rh[0].x), "d"(rh[0].y),
+          "d"(rl[1].x), "d"(rl[1].y), "d"(rh[1].x), "d"(rh[1].y),
+          "d"(rl[2].x), "d"(rl[2].y), "d"(rh[2].x), "d"(rh[2].y),
+          "d"(rl[3].x), "d"(rl[3].y), "d"(rh[3].x), "d"(rh[3].y),
+          "d"(rl[4].x), "d"(rl[4].y), "d"(rh[4].x), "d"(rh[4].y),
+          "d"(rl[5].x), "d"(rl[5].y), "d"(rh[5].x), "d"(rh[5].y),
+          "d"(rl[6].x), "d"(rl[6].y), "d"(rh[6].x), "d"(rh[6].y),
+          "d"(rl[7].x), "d"(rl[7].y), "d"(rh[7].x), "d"(rh[7].y),
+          "d"(rl[8].x), "d"(rl[8].y), "d"(rh[8].x), "d"(rh[8].y),
+          "d"(rl[9].x), "d"(rl[9].y), "d"(rh[9].x), "d"(rh[9].y),
+          "d"(rl[10].x), "d"(rl[10].y), "d"(rh[10].x), "d"(rh[10].y),
+          "d"(rl[11].x), "d"(rl[11].y), "d"(rh[11].x), "d"(rh[11].y),
+          "d"(rl[12].x), "d"(rl[12].y), "d"(rh[12].x), "d"(rh[12].y),
+          "d"(rl[13].x), "d"(rl[13].y), "d"(rh[13].x), "d"(rh[13].y),
+          "d"(rl[14].x), "d"(rl[14].y), "d"(rh[14].x), "d"(rh[14].y),
+          "d"(rl[15].x), "d"(rl[15].y), "d"(rh[15].x), "d"(rh[15].y));
+}
+
 template <typename IO>
 __global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -559,14 +603,12 @@ __global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a
             }
             const int wl_ = __ffs(cand) - 1;
             C64dSlot *sl = sm.slot[it & 1];
+            // the warp's winning row pair, fetched on every lane (uniform branch)
+            const int uw = 63 - (int)(__shfl_sync(0xffffffffu, (uint32_t)kb, wl_) & 63u);
+            double2 plo, phi;
+            c64d_pick(rl, rh, uw, plo, phi);
             if (lane == wl_) {
-                const int u = 63 - (int)(kb & 63ull);
-                double2 c = make_double2(0.0, 0.0);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {  // one thread: a predicated sweep
-                    if (u == 16 * h + i) c = rl[i];
-                    if (u == 16 * h + i + 32) c = rh[i];
-                }
+                const double2 c = uw >= 32 ? phi : plo;
                 sl[wid].key = kb;
                 sl[wid].cre = c.x;
                 sl[wid].cim = c.y;
