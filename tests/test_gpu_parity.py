@@ -507,21 +507,24 @@ def test_host_api_chunk_pipeline(precision):
 
 
 @pytest.mark.gpu
-def test_full_size_4k_properties():
-    """BASELINE configs[2] at full size (3840x2160, N=32, I=100, guarded fp32)
-    through size-independent properties: the chunked device call equals a
-    3-strip host-buffer split bitwise, known pixels are copied exactly, three
-    bands of block rows (top edge, middle, bottom edge) match the reference
-    restatement within the production tolerance, and the re-run fraction is
-    the guard study's (a few per cent)."""
+@pytest.mark.parametrize("H,W,N,reducer", [(2160, 3840, 32, "tree"), (1080, 1920, 16, "tree"),
+                                           (1080, 1920, 64, "linear")])
+def test_full_size_properties(H, W, N, reducer):
+    """BASELINE configs[2] (4K, N=32) and the C5 supports at 1080p, full size,
+    I=100, guarded fp32, through size-independent properties: the chunked
+    device call equals a 3-strip host-buffer split bitwise, known pixels are
+    copied exactly, three bands of block rows (top edge, middle, bottom edge)
+    match the reference restatement within the production tolerance, and the
+    re-run fraction is the guard study's (a few per cent)."""
     torch = pytest.importorskip("torch")
     from paper_2202_13926_b200 import _lib
-    H, W, B, L = 2160, 3840, 4, 14
+    B = 4
+    L = (N - B) // 2
     img = oracle.synthetic_frame(H, W, 7)
     sampled, mask = oracle.quarter_sample(img, 42)
     px = np.where(mask, sampled, 0.0).astype(np.float32)
     m8 = mask.astype(np.uint8)
-    p = _lib.make_params(B, L, 100, precision="fp32", argmax="redux")
+    p = _lib.make_params(B, L, 100, precision="fp32", argmax="redux", reducer=reducer)
     eng = _lib.Engine([0])
     d_px, d_mk = torch.tensor(px, device="cuda"), torch.tensor(m8, device="cuda")
     d_out = torch.empty_like(d_px)
@@ -532,13 +535,15 @@ def test_full_size_4k_properties():
     out = d_out.cpu().numpy()
     assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.1
     strips = np.zeros_like(px)
-    for r0, r1 in ((0, 170), (170, 371), (371, brows)):
+    c1, c2 = brows // 3, 2 * brows // 3 + 7  # uneven strips
+    for r0, r1 in ((0, c1), (c1, c2), (c2, brows)):
         eng.reconstruct_rows(px, m8, p, r0, r1, strips)
     assert np.array_equal(strips, out)
     assert np.array_equal(out[mask], px[mask])
     for r0 in (0, brows // 2, brows - 6):
         rows = (r0, r0 + 6)
-        ref = oracle.reconstruct_image(px.astype(np.float64), mask, B, L, 100, block_rows=rows)
+        ref = oracle.reconstruct_image(px.astype(np.float64), mask, B, L, 100, reducer=reducer,
+                                       block_rows=rows)
         y0, y1 = r0 * B, (r0 + 6) * B
         err = float(np.abs(out[y0:y1].astype(np.float64) - ref[y0:y1]).max())
         assert err <= FP32_TOL, (r0, err)
