@@ -1,0 +1,70 @@
+"""Randomised parity stress (GPU box): random frame sizes, block sizes, supports,
+reducers, early stop, seeds; guarded fp32 against the reference restatement
+within the production tolerance, fp64 through the reference's acceptance rule.
+
+    python tools/stress_parity.py [n_cases] [seed]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from oracle import port as oracle  # noqa: E402  (checker only)
+
+import paper_2202_13926_b200 as fsr  # noqa: E402
+
+FP32_TOL = 1e-3 * 255.0
+FP64_TOL = 1e-9 * 255.0
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2026)
+    fails = 0
+    t0 = time.time()
+    for c in range(n):
+        N = int(rng.choice([16, 32, 64]))
+        B = int(rng.choice([2, 4, 6] if N < 64 else [4, 6, 8]))
+        if (N - B) % 2:
+            B += 1
+        reducer = "linear" if N == 64 else str(rng.choice(["tree", "linear"]))
+        H, W = int(rng.integers(1, 160)), int(rng.integers(1, 200))
+        I = int(rng.choice([1, 17, 60, 100]))
+        early = bool(rng.integers(0, 2))
+        kind = str(rng.choice(["natural", "uniform"]))
+        img = oracle.synthetic_frame(H, W, int(rng.integers(0, 1000)), kind) if H > 1 and W > 1 \
+            else rng.uniform(0, 255, (H, W))
+        sampled, mask = oracle.quarter_sample(img, int(rng.integers(0, 2**31)))
+        if not mask.any():
+            continue
+        sampled = np.where(mask, sampled, 0.0)
+        L = (N - B) // 2
+        s32 = sampled.astype(np.float32)
+        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer, early)
+        out32 = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer, early_stop=early,
+                                precision="fp32", argmax="redux")
+        e32 = float(np.abs(out32.astype(np.float64) - ref32).max())
+        ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, reducer, early)
+        out64, tr = fsr.reconstruct(sampled, mask, B, N, I, reducer=reducer, early_stop=early,
+                                    precision="fp64", argmax="redux", return_trace=True)
+        ok64 = True
+        try:
+            oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, 0.7, 0.5, reducer,
+                                            tr.selections, FP64_TOL)
+        except AssertionError as exc:
+            ok64 = False
+            msg64 = str(exc)[:200]
+        ok = e32 <= FP32_TOL and ok64 and np.array_equal(out64[mask], sampled[mask])
+        fails += not ok
+        print(f"case {c}: {H}x{W} N={N} B={B} I={I} {reducer} early={early} {kind}: "
+              f"fp32 max|d|={e32:.3e} fp64={'ok' if ok64 else 'FAIL ' + msg64} -> {'ok' if ok else 'FAIL'}",
+              flush=True)
+    print(f"{n} cases, {fails} failures, {time.time() - t0:.1f} s")
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
