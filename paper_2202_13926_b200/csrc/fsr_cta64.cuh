@@ -103,12 +103,13 @@ __device__ __forceinline__ void c64_fft_lines(double2 *t, int ls, int es, const 
     __syncthreads();
 }
 
-template <bool GUARD, bool HERM, bool UPDATE, bool SWAP>
+template <bool GUARD, bool HERM, bool UPDATE, bool SWAP, bool PK = false>
 __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const float2 (&wf2)[16],
                                        const float4 *up, float gr, float gi, uint32_t canon,
                                        int h, uint32_t hmask, uint32_t &m1, uint32_t &m2) {
     m1 = 0;
     m2 = 0;
+    uint32_t hpend = 0;
     const float2 ngr = make_float2(-gr, -gr), pgi = make_float2(gi, gi), ngi = make_float2(-gi, -gi);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -127,6 +128,24 @@ __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const
         const float2 mag = __ffma2_rn(r, r, __fmul2_rn(m, m));
         const float2 o = __fmul2_rn(mag, wf2[i]);
         const uint32_t u = (uint32_t)(16 * h + i);  // h is uniform per warp
+        if (PK) {
+            // pair key (as warp32): the pair's larger objective tagged with its
+            // lower row; top-2 over pair keys, the half resolved after the argmax
+            float ox = o.x, oy = o.y;
+            if (HERM) {
+                ox = ((canon >> i) & 1u) ? ox : 0.f;
+                oy = ((canon >> (i + 16)) & 1u) ? oy : 0.f;
+            }
+            const uint32_t hk = and_or(f2u(fmaxf(ox, oy)), hmask, 63u - u);
+            if ((i & 1) == 0) {
+                hpend = hk;
+            } else {
+                const uint32_t hmax = max(hpend, hk), hmin = min(hpend, hk);
+                m2 = umax3(m2, hmin, min(m1, hmax));
+                m1 = max(m1, hmax);
+            }
+            continue;
+        }
         uint32_t ka = and_or(f2u(o.x), hmask, 63u - u);
         uint32_t kb = and_or(f2u(o.y), hmask, 31u - u);  // row u + 32: 63 - (u + 32)
         if (HERM && GUARD) {
@@ -143,9 +162,14 @@ __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const
     }
 }
 
+#ifndef FSR_C64_PAIRKEY
+#define FSR_C64_PAIRKEY 1
+#endif
 template <bool GUARD>
 __global__ void __launch_bounds__(C64_THREADS, 3)
     cta64_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
+    // pair keys in guarded mode (every near-tie is re-run in fp64, see warp32)
+    constexpr bool PK = GUARD && FSR_C64_PAIRKEY;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C64Smem &sm = *reinterpret_cast<C64Smem *>(smem_raw);
     const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
@@ -292,31 +316,59 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const float4 *up = ub + (32 + 16 * h - (pu & 31)) * 64 + ((v - pv) & 63);
             const bool swap = pu >= 32;
             if (H && it == 0)
-                pass64<GUARD, true, false, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+                pass64<GUARD, true, false, false, PK>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
             else
-                swap ? pass64<GUARD, H, true, true>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
-                     : pass64<GUARD, H, true, false>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
+                swap ? pass64<GUARD, H, true, true, PK>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
+                     : pass64<GUARD, H, true, false, PK>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
             // phase 1: in-warp argmax, coefficient of the warp's best bin
             const uint32_t kw = __reduce_max_sync(0xffffffffu, m1);
-            const int wl = __ffs(__ballot_sync(0xffffffffu, m1 == kw)) - 1;
-            const uint32_t k2w = GUARD ? __reduce_max_sync(0xffffffffu, lane == wl ? m2 : m1) : 0u;
-            const int ur = 63 - (int)(kw & 63u);
-            float4 q;
-            switch ((ur & 31) & 15) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, m1 == kw);
+            const int wl = PK ? 31 - __clz(bal) : __ffs(bal) - 1;
+            uint32_t k1w = kw, k2w = 0u;
+            float cre, cim;
+            if (PK) {
+                // the warp's winning pair (row 16h + i and + 32): both halves'
+                // objectives recomputed exactly as the pass did, the winner's half,
+                // coefficient and pair partner read from lane wl
+                const int ur0 = 63 - (int)(kw & 63u);
+                float2 wfp;
+                const float4 q = pick_pair(re, im, wf2, ur0, wfp);
+                float olo = fmaf(q.x, q.x, q.z * q.z) * wfp.x, ohi = fmaf(q.y, q.y, q.w * q.w) * wfp.y;
+                if (H) {
+                    olo = ((canon >> (ur0 & 15)) & 1u) ? olo : 0.f;
+                    ohi = ((canon >> ((ur0 & 15) + 16)) & 1u) ? ohi : 0.f;
+                }
+                const bool hl = ohi > olo;
+                const float po = hl ? olo : ohi;
+                cre = hl ? q.y : q.x;
+                cim = hl ? q.w : q.z;
+                const bool hi = __shfl_sync(0xffffffffu, (int)hl, wl) != 0;
+                cre = __shfl_sync(0xffffffffu, cre, wl);
+                cim = __shfl_sync(0xffffffffu, cim, wl);
+                const int ur = ur0 + (hi ? 32 : 0);
+                k1w = (kw & a.key_mask) | (uint32_t)(63 - ur);  // the bin's row for phase 2
+                k2w = __reduce_max_sync(0xffffffffu, lane == wl ? max(m2, f2u(po) & a.key_mask) : m1);
+            } else {
+                k2w = GUARD ? __reduce_max_sync(0xffffffffu, lane == wl ? m2 : m1) : 0u;
+                const int ur = 63 - (int)(kw & 63u);
+                float4 q;
+                switch ((ur & 31) & 15) {
 #define FSR_PK64(j) \
     case j: q = make_float4(re[j].x, re[j].y, im[j].x, im[j].y); break;
-                FSR_PK64(0) FSR_PK64(1) FSR_PK64(2) FSR_PK64(3) FSR_PK64(4) FSR_PK64(5) FSR_PK64(6)
-                FSR_PK64(7) FSR_PK64(8) FSR_PK64(9) FSR_PK64(10) FSR_PK64(11) FSR_PK64(12) FSR_PK64(13)
-                FSR_PK64(14)
-                default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); break;
+                    FSR_PK64(0) FSR_PK64(1) FSR_PK64(2) FSR_PK64(3) FSR_PK64(4) FSR_PK64(5) FSR_PK64(6)
+                    FSR_PK64(7) FSR_PK64(8) FSR_PK64(9) FSR_PK64(10) FSR_PK64(11) FSR_PK64(12) FSR_PK64(13)
+                    FSR_PK64(14)
+                    default: q = make_float4(re[15].x, re[15].y, im[15].x, im[15].y); break;
 #undef FSR_PK64
+                }
+                cre = ur < 32 ? q.x : q.y;
+                cim = ur < 32 ? q.z : q.w;
+                cre = __shfl_sync(0xffffffffu, cre, wl);
+                cim = __shfl_sync(0xffffffffu, cim, wl);
             }
-            float cre = ur < 32 ? q.x : q.y, cim = ur < 32 ? q.z : q.w;
-            cre = __shfl_sync(0xffffffffu, cre, wl);
-            cim = __shfl_sync(0xffffffffu, cim, wl);
             C64Slot *sl = sm.slot[it & 1];
             if (lane == 0) {
-                sl[wid].k1 = kw;
+                sl[wid].k1 = k1w;
                 sl[wid].k2 = k2w;
                 sl[wid].cre = cre;
                 sl[wid].cim = cim;
