@@ -33,6 +33,10 @@
 
 namespace fsr {
 
+#ifndef FSR_P64_BRX
+#define FSR_P64_BRX 1
+#endif
+
 template <typename IO>
 struct Pair64Args {
     const IO *px;
@@ -134,6 +138,50 @@ __device__ __forceinline__ double2 pick16(const cpx<double> (&R)[16], int i) {
         default: c = make_double2(R[15].re, R[15].im); break;
 #undef FSR_PICK
     }
+    return c;
+}
+
+// R[i] of this lane by one indirect branch (brx.idx jump table); i warp-uniform.
+__device__ __forceinline__ double2 pick16_brx(const cpx<double> (&R)[16], int i) {
+    double2 c;
+    asm volatile(
+        "{\n ts%=: .branchtargets L0_%=, L1_%=, L2_%=, L3_%=, L4_%=, L5_%=, L6_%=, L7_%=, L8_%=, L9_%=, L10_%=, L11_%=, L12_%=, L13_%=, L14_%=, L15_%=;\n"
+        " brx.idx %2, ts%=;\n"
+        " L0_%=: mov.f64 %0, %3; mov.f64 %1, %4; bra.uni Le_%=;\n"
+        " L1_%=: mov.f64 %0, %5; mov.f64 %1, %6; bra.uni Le_%=;\n"
+        " L2_%=: mov.f64 %0, %7; mov.f64 %1, %8; bra.uni Le_%=;\n"
+        " L3_%=: mov.f64 %0, %9; mov.f64 %1, %10; bra.uni Le_%=;\n"
+        " L4_%=: mov.f64 %0, %11; mov.f64 %1, %12; bra.uni Le_%=;\n"
+        " L5_%=: mov.f64 %0, %13; mov.f64 %1, %14; bra.uni Le_%=;\n"
+        " L6_%=: mov.f64 %0, %15; mov.f64 %1, %16; bra.uni Le_%=;\n"
+        " L7_%=: mov.f64 %0, %17; mov.f64 %1, %18; bra.uni Le_%=;\n"
+        " L8_%=: mov.f64 %0, %19; mov.f64 %1, %20; bra.uni Le_%=;\n"
+        " L9_%=: mov.f64 %0, %21; mov.f64 %1, %22; bra.uni Le_%=;\n"
+        " L10_%=: mov.f64 %0, %23; mov.f64 %1, %24; bra.uni Le_%=;\n"
+        " L11_%=: mov.f64 %0, %25; mov.f64 %1, %26; bra.uni Le_%=;\n"
+        " L12_%=: mov.f64 %0, %27; mov.f64 %1, %28; bra.uni Le_%=;\n"
+        " L13_%=: mov.f64 %0, %29; mov.f64 %1, %30; bra.uni Le_%=;\n"
+        " L14_%=: mov.f64 %0, %31; mov.f64 %1, %32; bra.uni Le_%=;\n"
+        " L15_%=: mov.f64 %0, %33; mov.f64 %1, %34; bra.uni Le_%=;\n"
+        " Le_%=:\n}"
+        : "=d"(c.x), "=d"(c.y)
+        : "r"(i & 15),
+          "d"(R[0].re), "d"(R[0].im),
+          "d"(R[1].re), "d"(R[1].im),
+          "d"(R[2].re), "d"(R[2].im),
+          "d"(R[3].re), "d"(R[3].im),
+          "d"(R[4].re), "d"(R[4].im),
+          "d"(R[5].re), "d"(R[5].im),
+          "d"(R[6].re), "d"(R[6].im),
+          "d"(R[7].re), "d"(R[7].im),
+          "d"(R[8].re), "d"(R[8].im),
+          "d"(R[9].re), "d"(R[9].im),
+          "d"(R[10].re), "d"(R[10].im),
+          "d"(R[11].re), "d"(R[11].im),
+          "d"(R[12].re), "d"(R[12].im),
+          "d"(R[13].re), "d"(R[13].im),
+          "d"(R[14].re), "d"(R[14].im),
+          "d"(R[15].re), "d"(R[15].im));
     return c;
 }
 
@@ -397,11 +445,22 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
                 wl = __ffs(__ballot_sync(0xffffffffu, kb == key)) - 1;
             }
             PairSlot *ps = &sm.slot[pair][parity][0];
+#if FSR_P64_BRX
+            // the winning row, made warp-uniform, then one indirect-branch pick on
+            // every lane; the winning lane publishes its coefficient R[u*][v]
+            const uint32_t klo = __shfl_sync(0xffffffffu, (uint32_t)kb, wl);
+            const uint32_t rrw = 31u - ((klo >> 5) & 31u);
+            const double2 cw = pick16_brx(R, p64_slot(H, TREE ? (int)bitrev5(rrw) : (int)rrw) & 15);
+#endif
             if (lane == wl) {
                 // only the winning lane extracts its coefficient R[u*][v] and publishes it
+#if FSR_P64_BRX
+                const double2 c = cw;
+#else
                 const uint32_t rr = 31u - (((uint32_t)kb >> 5) & 31u);
                 const int bu = TREE ? (int)bitrev5(rr) : (int)rr;
                 const double2 c = pick16(R, p64_slot(H, bu) & 15);
+#endif
                 ps[H].key = __longlong_as_double((long long)kb);
                 ps[H].cre = c.x;
                 ps[H].cim = c.y;
