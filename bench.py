@@ -52,6 +52,15 @@ def flops_per_block(N: int, I: int) -> float:
     return N * N * (12.0 * I + 30.0 * math.log2(N))
 
 
+def rank_device():
+    """(CUDA device, process-group backend) of this rank: LOCAL_RANK over NCCL.
+    FSR_BENCH_SINGLE_GPU=1 (path check only, never a measurement) puts every
+    rank on device 0 over gloo, so the N>1 code path runs on a one-GPU box."""
+    if os.environ.get("FSR_BENCH_SINGLE_GPU") == "1":
+        return 0, "gloo"
+    return int(os.environ.get("LOCAL_RANK", "0")), "nccl"
+
+
 def cpu_model() -> str:
     """The host CPU (SURVEY §8d asks the baseline to name it) and os.cpu_count()."""
     name = "unknown"
@@ -268,10 +277,10 @@ def run_stream(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local, backend = rank_device()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, device_id=torch.device("cuda", local))
     from paper_2202_13926_b200 import _lib, frames, shard, synth
     from paper_2202_13926_b200.stream import FrameStream
 
@@ -376,10 +385,10 @@ def main():
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local, backend = rank_device()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(backend, device_id=torch.device("cuda", local))
 
     from paper_2202_13926_b200 import _lib
 
