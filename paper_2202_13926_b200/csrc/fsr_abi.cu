@@ -89,9 +89,9 @@ struct Device {
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
     bool tma_enabled = true;     // warp32 window gather by TMA when the rows allow it
-    bool chunking = true;        // large calls in row chunks over two lanes (FSR_NO_CHUNK=1: off)
+    bool chunking = true;        // large calls in row chunks over kLanes streams (FSR_NO_CHUNK=1: off)
     int used_tma = 0;            // last warp32 launch gathered by TMA
-    // host-buffer calls on large strips are pipelined over two "lanes" (same GPU,
+    // host-buffer calls on large strips are pipelined over kLanes "lanes" (same GPU,
     // own stream, staging buffers and scratch): H2D of chunk c+1 and D2H of chunk
     // c-1 overlap the kernels of chunk c
     std::vector<std::unique_ptr<Device>> lanes;
@@ -786,7 +786,7 @@ int select_device(fsr_engine *eng, Device &d) {
     return FSR_OK;
 }
 
-// Large calls run in K row chunks alternating over two lanes (same GPU, own
+// Large calls run in K row chunks alternating over kLanes lanes (same GPU, own
 // stream, staging and scratch): one chunk's copies, fp64 re-run and launch tail
 // overlap the next chunk's main kernel.
 int chunk_count(const Device &d, int64_t block_rows) {
@@ -859,7 +859,7 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         q.ob = std::min<int64_t>(H, q.row1 * B);
     }
     // per device: the strip's block rows in K chunks (K = 1 for small strips), chunk c
-    // on lane c % 2 -- copies of one chunk overlap the kernels of the other
+    // on lane c % kLanes -- copies of one chunk overlap the kernels of the others
     std::vector<int> nchunks(nd, 0);
     for (int g = 0; g < nd; ++g) {
         Device &d = *eng->devs[g];
@@ -1153,7 +1153,7 @@ int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float
         rc = enqueue_image<float>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
                                   height, width, row0, row1, nullptr, nullptr, true, NAN, st);
     } else {
-        // chunks alternate over the two lanes, forked from and joined back into the
+        // chunks alternate over the lanes, forked from and joined back into the
         // caller's stream; chunk c uses counter slot c and its own empty-list region
         if ((rc = ensure_lanes(eng, d))) return rc;
         const int64_t bcols = (width + p->block - 1) / p->block;
