@@ -96,7 +96,7 @@ struct Device {
     // c-1 overlap the kernels of chunk c
     std::vector<std::unique_ptr<Device>> lanes;
     int dev_chunks = 1;  // chunks of the last device-API call (for its statistics)
-    cudaEvent_t ck0[8] = {}, ck1[8] = {};  // per-chunk main-kernel brackets (K <= 8)
+    cudaEvent_t ck0[16] = {}, ck1[16] = {};  // per-chunk main-kernel brackets (K <= 16)
 };
 
 }  // namespace
@@ -790,12 +790,15 @@ int select_device(fsr_engine *eng, Device &d) {
 // stream, staging and scratch): one chunk's copies, fp64 re-run and launch tail
 // overlap the next chunk's main kernel.
 int chunk_count(const Device &d, int64_t block_rows) {
+#ifndef FSR_CHUNK_ROWS
+#define FSR_CHUNK_ROWS 64  // block rows per chunk (at least)
+#endif
 #ifndef FSR_MAX_CHUNKS
 #define FSR_MAX_CHUNKS 8  // 4K (540 block rows): 8 chunks, +0.4 % e2e over 4
 #endif
     return (d.gap_debug || !d.chunking)
                ? 1
-               : (int)std::min<int64_t>(FSR_MAX_CHUNKS, std::max<int64_t>(1, block_rows / 64));
+               : (int)std::min<int64_t>(FSR_MAX_CHUNKS, std::max<int64_t>(1, block_rows / FSR_CHUNK_ROWS));
 }
 
 #ifndef FSR_LANES
@@ -815,7 +818,7 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
         CUDA_TRY(eng, cudaEventCreate(&ln->ev_mid));
         d.lanes.push_back(std::move(ln));
     }
-    for (int c = 0; c < 8; ++c)
+    for (int c = 0; c < 16; ++c)
         if (!d.ck0[c]) {
             CUDA_TRY(eng, cudaEventCreate(&d.ck0[c]));
             CUDA_TRY(eng, cudaEventCreate(&d.ck1[c]));
@@ -1099,7 +1102,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
             cudaEventDestroy(ln->ev_mid);
             cudaStreamDestroy(ln->stream);
         }
-        for (int c = 0; c < 8; ++c)
+        for (int c = 0; c < 16; ++c)
             if (d.ck0[c]) {
                 cudaEventDestroy(d.ck0[c]);
                 cudaEventDestroy(d.ck1[c]);
