@@ -298,7 +298,10 @@ int launch_pair64_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t
     return FSR_OK;
 }
 
-constexpr int kPairBPC = 4;
+#ifndef FSR_P64_BPC
+#define FSR_P64_BPC 4
+#endif
+constexpr int kPairBPC = FSR_P64_BPC;
 
 template <typename IO>
 int launch_pair64(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
