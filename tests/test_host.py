@@ -106,3 +106,16 @@ def test_reconstruct_argument_validation():
         fsr.reconstruct(np.ones((8, 8)), np.ones((8, 8), bool), 4, 9, 2)
     with pytest.raises(ValueError, match="unknown argmax strategy"):
         fsr.reconstruct(np.ones((8, 8)), np.ones((8, 8), bool), 4, 8, 2, reducer="x")
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """Without the built libfsr.so the package raises (no CPU fallback)."""
+    import subprocess
+    import sys
+    code = ("import numpy as np, paper_2202_13926_b200 as f\n"
+            "try:\n    f.reconstruct(np.ones((8, 8)), np.ones((8, 8), bool), 4, 8, 2)\n"
+            "except RuntimeError as e:\n    print('raised', 'missing' in str(e))\n")
+    env = dict(os.environ, FSR_LIBFSR=str(tmp_path / "nope.so"))
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=300)
+    assert "raised True" in out.stdout, out.stdout + out.stderr
