@@ -66,7 +66,8 @@ typedef struct {
     int32_t kernel;      /* N=32 fp64 kernel: 0 auto (= warp pair), 1 one warp per block, 2 warp pair */
     double rho;          /* (0, 1) */
     double gamma;        /* (0, 1] */
-    double guard_tau;    /* fp32 near-tie guard: relative top-2 gap that forces an fp64 re-run */
+    double guard_tau;    /* fp32 near-tie guard: relative top-2 gap that forces an fp64 re-run;
+                            0 (default) = chosen from N and I */
 } fsr_params;
 
 typedef struct fsr_engine fsr_engine;

@@ -566,6 +566,21 @@ bool warp32_eligible(const fsr_params *p) {
     return N == 32 && p->block * p->block <= 32 && p->precision != FSR_PREC_FP64;
 }
 
+// The near-tie guard's relative gap tau.  An explicit guard_tau > 0 is used as
+// given; 0 selects it from the support and the iteration count: the fp32
+// loop's objective error grows with both (late iterations compare objectives
+// of a residual far below R0), so tau = 5e-5 * k_N * max(1, I/100)^1.25 with
+// k_N = 2 for N = 64, else 1 -- measured (tools/guard_check.py, natural and
+// uniform frames): 5e-5 holds N = 16/32 at I = 100 (max error 0.14 / 0.19 of
+// the 0.255 tolerance) but not N = 64 at I = 100 (0.40) nor I = 500 (0.5-0.9).
+double guard_tau_for(const fsr_params *p) {
+    if (p->guard_tau > 0.0) return p->guard_tau;
+    const int N = p->block + 2 * p->border;
+    const double kn = N >= 64 ? 2.0 : 1.0;
+    const double it = std::max(1.0, p->iterations / 100.0);
+    return std::min(0.25, 5e-5 * kn * std::pow(it, 1.25));
+}
+
 // Enqueue the whole image path for target-block rows [row0, row1) on device d.
 // px/mask/out are "virtual" row-0 pointers (absolute row y at ptr + y*pitch).
 // device_fill: compute the empty-support fill value on the device from rows [0, H).
@@ -684,7 +699,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.first = first;
         a.nblocks = nblocks;
         a.gamma = (float)p->gamma;
-        a.tau = (float)p->guard_tau;
+        a.tau = (float)guard_tau_for(p);
         a.omt = 1.f - a.tau;
         a.wf = tf.wf;
         a.sel = sel;
@@ -1017,7 +1032,7 @@ void fsr_params_init(fsr_params *p) {
     p->argmax_impl = FSR_ARGMAX_SHFL;
     p->rho = 0.7;
     p->gamma = 0.5;
-    p->guard_tau = 5e-5;
+    p->guard_tau = 0.0;  // auto: guard_tau_for(p)
 }
 
 int fsr_params_validate(const fsr_params *p, char *msg, int msg_len) {

@@ -33,7 +33,7 @@ from .spectra import WeightSet
 
 REDUCERS = ("tree", "linear")
 EARLY_STOP_RELATIVE = 1e-12
-DEFAULT_GUARD_TAU = 5e-5
+DEFAULT_GUARD_TAU = 0.0  # 0: chosen by the engine from N and I (fsr.h)
 
 
 def _check_reducer(reducer: str) -> bool:
