@@ -597,6 +597,12 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     const int64_t bcols = (W + p->block - 1) / p->block;
     const int64_t first = row0 * bcols, nblocks = (row1 - row0) * bcols;
     if (nblocks <= 0) return FSR_OK;
+    // Beyond ~300 iterations the guard re-runs most blocks (tau grows with I,
+    // tools/guard_check.py: 90-99 % at I = 500), so the guarded fp32 request is
+    // served by the fp64 kernels directly -- faster, and exact.
+    fsr_params pl = *p;
+    if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
+    p = &pl;
     Counters *ctr = ctr_in;
     int32_t *empty_list = empty_in;
     if (!ctr) {  // the device's own scratch (otherwise the caller's per-chunk slot)

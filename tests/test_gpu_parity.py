@@ -533,7 +533,7 @@ def test_full_size_properties(H, W, N, reducer):
                            d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
     st = eng.last_stats()
     out = d_out.cpu().numpy()
-    assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.1
+    assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.2  # tau grows with N (guard_tau_for)
     strips = np.zeros_like(px)
     c1, c2 = brows // 3, 2 * brows // 3 + 7  # uneven strips
     for r0, r1 in ((0, c1), (c1, c2), (c2, brows)):
@@ -547,3 +547,55 @@ def test_full_size_properties(H, W, N, reducer):
         y0, y1 = r0 * B, (r0 + 6) * B
         err = float(np.abs(out[y0:y1].astype(np.float64) - ref[y0:y1]).max())
         assert err <= FP32_TOL, (r0, err)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_reference_psnr_kat_512(precision):
+    """The reference's own end-to-end KAT (test_output.txt:21): natural 512x512,
+    quarter-sampled with seed 42, B=4, L=6 (S=16), I=200, tree -> PSNR
+    42.312882 dB against the original.  fp64 reproduces it to 1e-6 dB and the
+    reference output to 1e-9 (0..1); guarded fp32 within the production
+    tolerance."""
+    d = golden_image("acc6_512_s16")
+    B, L, I = int(d["block"]), int(d["border"]), int(d["iterations"])
+    px = d["sampled"] if precision == "fp64" else d["sampled"].astype(np.float32)
+    out = fsr.reconstruct(px, d["mask"], B, B + 2 * L, I, reducer="tree", precision=precision,
+                          argmax="redux").astype(np.float64)
+    err = float(np.abs(out - d["out_tree"]).max())
+    dpsnr = abs(oracle.psnr(d["original"], out) - float(d["psnr_tree"]))
+    if precision == "fp64":
+        assert err <= FP64_TOL, err
+        assert dpsnr <= 1e-6, dpsnr
+    else:
+        # the fp32 entry point takes f32 pixels; rounding the reference's f64
+        # pixels already moves a near-tied block of this frame by ~0.8 gray
+        # levels, so pixel parity is judged against the reference on the same
+        # f32 inputs (DESIGN.md §4), PSNR against the published KAT
+        ref32 = oracle.reconstruct_image(px.astype(np.float64), d["mask"], B, L, I, 0.7, 0.5, "tree")
+        err32 = float(np.abs(out - ref32).max())
+        assert err32 <= FP32_TOL, err32
+        assert dpsnr <= PSNR_TOL, dpsnr
+    assert abs(float(d["psnr_tree"]) - 42.312882) < 5e-7
+
+
+@pytest.mark.parametrize("N,I,kind", [(16, 200, "natural"), (32, 200, "natural"),
+                                      (64, 100, "natural"), (64, 200, "uniform"),
+                                      (32, 400, "natural")])
+def test_guard_beyond_default_iterations(N, I, kind):
+    """The near-tie guard's tau grows with N and I (guard_tau_for): guarded fp32
+    stays within the production tolerance of the reference on the same f32
+    inputs where the fixed tau = 5e-5 of the N=32, I=100 study did not
+    (tools/guard_check.py; beyond I = 300 the request is served in fp64)."""
+    B = 4
+    L = (N - B) // 2
+    reducer = "linear" if N == 64 else "tree"
+    # 512x512 natural: the frame on which the fixed tau = 5e-5 fails at N=16 I=200
+    # (0.28 gray levels) and N=64 I=100 (0.40); smaller frames hit no flip
+    size = 512 if kind == "natural" and N != 32 else 192
+    img = oracle.synthetic_frame(size, size, 7 if kind == "natural" else 3, kind)
+    sampled, mask = oracle.quarter_sample(img, 42)
+    s32 = np.where(mask, sampled, 0.0).astype(np.float32)
+    ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer)
+    out = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer, precision="fp32", argmax="redux")
+    err = float(np.abs(out.astype(np.float64) - ref32).max())
+    assert err <= FP32_TOL, err
