@@ -32,7 +32,7 @@ def main():
             B += 1
         reducer = "linear" if N == 64 else str(rng.choice(["tree", "linear"]))
         H, W = int(rng.integers(1, 160)), int(rng.integers(1, 200))
-        I = int(rng.choice([1, 17, 60, 100]))
+        I = int(rng.choice([1, 17, 60, 100, 200, 350]))
         early = bool(rng.integers(0, 2))
         kind = str(rng.choice(["natural", "uniform"]))
         img = oracle.synthetic_frame(H, W, int(rng.integers(0, 1000)), kind) if H > 1 and W > 1 \

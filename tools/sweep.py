@@ -76,10 +76,12 @@ def main():
                         "frame_ms": frame_ms, "fps": 1e3 / frame_ms,
                         "mpixel_per_s": H * W / (frame_ms * 1e-3) / 1e6,
                         "rerun_fraction": stats["rerun_blocks"] / max(1, rows * bcols),
+                        # guarded fp32 beyond 300 iterations is served in fp64 (fsr_abi.cu)
                         "kernel": {(32, False): "warp32 (+pair64 re-runs)", (32, True): "pair64",
                                    (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d",
-                                   (64, False): "cta64, in-warp redux (+cta64d fp64 re-runs)"}
-                                  .get((N, args.precision == "fp64"), "generic")}
+                                   (64, False): "cta64, in-warp redux (+cta64d fp64 re-runs)",
+                                   (64, True): "cta64d"}
+                                  .get((N, args.precision == "fp64" or I > 300), "generic")}
                 print(json.dumps(line), flush=True)
 
 
