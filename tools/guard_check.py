@@ -19,6 +19,7 @@ def main():
     size = int(sys.argv[1]) if len(sys.argv) > 1 else 512
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 7
     kind = os.environ.get("KIND", "natural")
+    rho, gamma = float(os.environ.get("RHO", "0.7")), float(os.environ.get("GAMMA", "0.5"))
     img = oracle.synthetic_frame(size, size, seed, kind)
     sampled, mask = oracle.quarter_sample(img, 42)
     s32 = sampled.astype(np.float32)
@@ -31,13 +32,13 @@ def main():
         B = 4
         red = "linear" if N == 64 else "tree"
         L = (N - B) // 2
-        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, red)
+        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, rho, gamma, red)
         for tau in taus:
-            out, tr = fsr.reconstruct(s32, mask, B, N, I, reducer=red, precision="fp32",
+            out, tr = fsr.reconstruct(s32, mask, B, N, I, rho, gamma, reducer=red, precision="fp32",
                                       argmax="redux", return_trace=True, guard_tau=tau)
             err = np.abs(out.astype(np.float64) - ref32)
             bad = int((err > 0.255).sum())
-            print(f"N={N} I={I} tau={tau:g} (0 = auto): max|d|={err.max():.4f} (tol 0.255) pixels over "
+            print(f"rho={rho} gamma={gamma} N={N} I={I} tau={tau:g} (0 = auto): max|d|={err.max():.4f} (tol 0.255) pixels over "
                   f"tol={bad} reruns={tr.stats['rerun_blocks']}/{tr.stats['blocks']}", flush=True)
 
 
