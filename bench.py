@@ -391,6 +391,7 @@ def main():
         dist.init_process_group(backend, device_id=torch.device("cuda", local))
 
     from paper_2202_13926_b200 import _lib
+    from paper_2202_13926_b200.engine import effective_guard_tau
 
     H, W = WORKLOADS[args.workload]
     B, N, I = args.block, args.support, args.iterations
@@ -552,6 +553,7 @@ def main():
                                f"{world} GPU(s)", "B": B, "N": N, "iterations": I, "rho": 0.7,
                    "gamma": 0.5, "reducer": args.reducer, "precision": args.precision,
                    "argmax": args.argmax, "kernel": args.kernel, "image": args.image, "parallelism": f"strips{world}",
+                   "guard_tau": effective_guard_tau(N, I) if args.precision == "fp32" else None,
                    "io": "f32 pixels + u8 mask in, f32 out",
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,

@@ -36,6 +36,15 @@ EARLY_STOP_RELATIVE = 1e-12
 DEFAULT_GUARD_TAU = 0.0  # 0: chosen by the engine from N and I (fsr.h)
 
 
+def effective_guard_tau(support: int, iterations: int, guard_tau: float = DEFAULT_GUARD_TAU) -> float:
+    """The near-tie guard's tau as the engine applies it (fsr_abi.cu guard_tau_for):
+    an explicit tau > 0 as given, else 5e-5 * k_N * max(1, I/100)^1.25, k_N = 2 for N=64."""
+    if guard_tau > 0.0:
+        return float(guard_tau)
+    kn = 2.0 if support >= 64 else 1.0
+    return min(0.25, 5e-5 * kn * max(1.0, iterations / 100.0) ** 1.25)
+
+
 def _check_reducer(reducer: str) -> bool:
     if reducer not in REDUCERS:
         raise ValueError(f"unknown argmax strategy {reducer!r}, expected one of {REDUCERS}")
