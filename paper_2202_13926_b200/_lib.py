@@ -121,7 +121,7 @@ def _ptr(a):
 
 
 def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer="tree",
-                early_stop=False, precision="fp64", argmax="shfl", guard_tau=0.0,
+                early_stop=False, precision="fp64", argmax="redux", guard_tau=0.0,
                 kernel="auto") -> FsrParamsC:
     p = FsrParamsC()
     load().fsr_params_init(ctypes.byref(p))

@@ -63,7 +63,7 @@ class Trace:
 def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int = 100,
                 rho: float = 0.7, gamma: float = 0.5, *, reducer: str = "tree",
                 early_stop: bool = False, precision: str = "fp64", devices=None,
-                argmax: str = "shfl", guard_tau: float = DEFAULT_GUARD_TAU,
+                argmax: str = "redux", guard_tau: float = DEFAULT_GUARD_TAU,
                 return_trace: bool = False):
     """Reconstruct the unknown pixels of ``image`` (0..255 scale) given ``mask``.
 
@@ -71,7 +71,10 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
     (reference cli.py:186-188).  Supports up to 64 are accepted (the tree
     reducer is limited to N*N <= 1024, like the reference).  Returns an array of
     the compute precision's I/O type (float32 for fp32 modes, float64 for fp64),
-    or ``(array, Trace)`` with ``return_trace``.
+    or ``(array, Trace)`` with ``return_trace``.  ``argmax`` picks the warp
+    argmax implementation -- "redux" (redux.sync + ballot, the fastest on
+    B200), "shfl" (the paper's shuffle butterfly) or "smem" (the paper's
+    shared-memory comparison point); all three give bitwise-identical results.
     """
     _check_reducer(reducer)
     if (support - block) % 2 or support < block:
@@ -102,7 +105,7 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
 
 def reconstruct_image(sampled: SampledImage, params: FsrParams, reducer: str = "tree",
                       early_stop: bool = False, *, precision: str = "fp64", devices=None,
-                      argmax: str = "shfl", guard_tau: float = DEFAULT_GUARD_TAU) -> GrayImage:
+                      argmax: str = "redux", guard_tau: float = DEFAULT_GUARD_TAU) -> GrayImage:
     """Drop-in for fsrkit.reconstruct_image: every target block reconstructed
     independently on the GPU and stitched; empty-support blocks get the mean of
     the known samples ("no known samples" ValueError if there is none).
