@@ -2,7 +2,7 @@
 reducers, early stop, seeds; guarded fp32 against the reference restatement
 within the production tolerance, fp64 through the reference's acceptance rule.
 
-    python tools/stress_parity.py [n_cases] [seed]
+    python tools/stress_parity.py [n_cases] [seed] [vary_rho_gamma]
 """
 import os
 import sys
@@ -35,6 +35,8 @@ def main():
         I = int(rng.choice([1, 17, 60, 100, 200, 350]))
         early = bool(rng.integers(0, 2))
         kind = str(rng.choice(["natural", "uniform"]))
+        rho = float(rng.choice([0.7, 0.68, 0.82, 0.6, 0.9])) if len(sys.argv) > 3 else 0.7
+        gamma = float(rng.choice([0.5, 0.2, 0.6, 0.8])) if len(sys.argv) > 3 else 0.5
         img = oracle.synthetic_frame(H, W, int(rng.integers(0, 1000)), kind) if H > 1 and W > 1 \
             else rng.uniform(0, 255, (H, W))
         sampled, mask = oracle.quarter_sample(img, int(rng.integers(0, 2**31)))
@@ -43,23 +45,24 @@ def main():
         sampled = np.where(mask, sampled, 0.0)
         L = (N - B) // 2
         s32 = sampled.astype(np.float32)
-        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer, early)
-        out32 = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer, early_stop=early,
+        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, rho, gamma, reducer, early)
+        out32 = fsr.reconstruct(s32, mask, B, N, I, rho, gamma, reducer=reducer, early_stop=early,
                                 precision="fp32", argmax="redux")
         e32 = float(np.abs(out32.astype(np.float64) - ref32).max())
-        ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, reducer, early)
-        out64, tr = fsr.reconstruct(sampled, mask, B, N, I, reducer=reducer, early_stop=early,
-                                    precision="fp64", argmax="redux", return_trace=True)
+        ref = oracle.reconstruct_image(sampled, mask, B, L, I, rho, gamma, reducer, early)
+        out64, tr = fsr.reconstruct(sampled, mask, B, N, I, rho, gamma, reducer=reducer,
+                                    early_stop=early, precision="fp64", argmax="redux",
+                                    return_trace=True)
         ok64 = True
         try:
-            oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, 0.7, 0.5, reducer,
+            oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, rho, gamma, reducer,
                                             tr.selections, FP64_TOL)
         except AssertionError as exc:
             ok64 = False
             msg64 = str(exc)[:200]
         ok = e32 <= FP32_TOL and ok64 and np.array_equal(out64[mask], sampled[mask])
         fails += not ok
-        print(f"case {c}: {H}x{W} N={N} B={B} I={I} {reducer} early={early} {kind}: "
+        print(f"case {c}: {H}x{W} N={N} B={B} I={I} rho={rho} gamma={gamma} {reducer} early={early} {kind}: "
               f"fp32 max|d|={e32:.3e} fp64={'ok' if ok64 else 'FAIL ' + msg64} -> {'ok' if ok else 'FAIL'}",
               flush=True)
     print(f"{n} cases, {fails} failures, {time.time() - t0:.1f} s")
