@@ -72,7 +72,8 @@ typedef struct {
 
 typedef struct fsr_engine fsr_engine;
 
-/* Defaults of the BASELINE configs: B=4, L=14 (N=32), I=100, rho=0.7, gamma=0.5, tree. */
+/* Defaults of the BASELINE configs: B=4, L=14 (N=32), I=100, rho=0.7, gamma=0.5, tree;
+ * fp64 precision, redux argmax, guard_tau 0 (auto). */
 void fsr_params_init(fsr_params *p);
 
 /* Validate like FsrParams.__post_init__ (core.py:63-80); the S^2<=1024 cap is
