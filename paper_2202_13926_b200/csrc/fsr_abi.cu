@@ -257,7 +257,16 @@ int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, 
     size_t smem = generic_smem(a.N, sizeof(Real));
     auto k = image_generic_kernel<Real, IO>;
     if (smem > 48 * 1024) CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, GEN_THREADS, smem, st>>>(a);
+    // small supports (N*N <= 256: the paper grid's S = 8, 12) get a CTA sized to
+    // their bin count instead of 256 mostly idle threads, and proportionally
+    // more CTAs; the kernel's per-thread arrays cover 16 strides of the CTA
+    const int n = a.N * a.N;
+    int threads = GEN_THREADS;
+    if (n <= GEN_THREADS && a.B * a.B <= 16 * 64) threads = std::max(64, (n + 31) / 32 * 32);
+    int64_t g = (int64_t)grid * (GEN_THREADS / threads);
+    if (!a.list_count) g = std::min<int64_t>(g, std::max<int64_t>(a.nblocks, 1));
+    grid = (int)g;
+    k<<<grid, threads, smem, st>>>(a);
     d.launches++;
     CUDA_TRY(eng, cudaGetLastError());
     return FSR_OK;
