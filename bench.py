@@ -104,10 +104,10 @@ def make_frame(H, W, kind):
     return np.where(mask, img, 0.0), mask, img
 
 
-def ncu_traffic(kernel_prefix):
+def ncu_traffic(kernel_prefix, name="warp32_ncu.json"):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (tools/ncu_summary.py), for the workload it was taken on."""
-    path = os.path.join(ROOT, "profiles", "r01", "warp32_ncu.json")
+    path = os.path.join(ROOT, "profiles", "r01", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -119,10 +119,10 @@ def ncu_traffic(kernel_prefix):
     return None
 
 
-def ncu_issue(kernel_prefix):
+def ncu_issue(kernel_prefix, name="warp32_ncu.json"):
     """Issue-slot view of the dominant kernel from the same committed capture:
     the loop is bound by instruction issue and dependency latency, not FLOPs."""
-    path = os.path.join(ROOT, "profiles", "r01", "warp32_ncu.json")
+    path = os.path.join(ROOT, "profiles", "r01", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -135,7 +135,7 @@ def ncu_issue(kernel_prefix):
                     "fma_pipe_pct": ln.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
                     "alu_pipe_pct": ln.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
                     "warps_per_smsp": ln.get("smsp__warps_active.avg.per_cycle_active"),
-                    "source": "ncu --set full, profiles/r01/warp32_ncu.json"}
+                    "source": f"ncu --set full, profiles/r01/{name}"}
     return None
 
 
@@ -537,13 +537,18 @@ def main():
     io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
                 + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
     traffic, traffic_src, issue = None, None, None
-    if (kernel == "warp32_kernel" and args.workload == "4k" and world == 1
-            and args.precision == "fp32" and args.reducer == "tree" and args.argmax == "redux"):
-        traffic = ncu_traffic("void warp32_kernel<4, 1, 2, 1, 0")
-        issue = ncu_issue("void warp32_kernel<4, 1, 2, 1, 0")
+    # committed ncu captures (tools/profile_round.sh) for the default line of each kernel
+    captured = {("warp32_kernel", "4k"): ("warp32_ncu.json", "void warp32_kernel<4, 1, 2, 1, 0"),
+                ("warp16_kernel", "1080p"): ("warp16_ncu.json", "void warp16_kernel<4, 1, 2, 1, 0"),
+                ("cta64_kernel", "1080p"): ("cta64_ncu.json", "void cta64_kernel<1>")}
+    cap = captured.get((kernel, args.workload))
+    if (cap is not None and world == 1 and args.precision == "fp32" and args.argmax == "redux"
+            and I == 100 and B == 4):
+        traffic = ncu_traffic(cap[1], cap[0])
+        issue = ncu_issue(cap[1], cap[0])
         if traffic is not None:
             traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
-                           "(profiles/r01/warp32_ncu.json); algorithmic I/O bytes " + str(io_bytes))
+                           f"(profiles/r01/{cap[0]}); algorithmic I/O bytes " + str(io_bytes))
     line = {
         "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
