@@ -192,7 +192,7 @@ typedef struct {
  * tensor maps, zero fill outside the image).  Set FSR_NO_TMA=1 in the
  * environment before fsr_engine_create to force the plain-load gather.
  * Calls over more than 128 block rows run in up to 8 row chunks alternating
- * over four internal streams (forked from / joined into the caller's stream
+ * over up to eight internal streams (forked from / joined into the caller's stream
  * for the device API); results are identical to one launch.  FSR_NO_CHUNK=1
  * at fsr_engine_create makes every call a single launch (kernel timing). */
 #define FSR_STATS_TMA_GATHER 1

@@ -835,7 +835,7 @@ int chunk_count(const Device &d, int64_t block_rows) {
 }
 
 #ifndef FSR_LANES
-#define FSR_LANES 4  // 4K: e2e 37.6 -> 38.2 fps over 2 lanes
+#define FSR_LANES 8  // one stream per chunk at 4K (2 lanes: e2e 37.6, 4: 38.2, 8: 38.4 fps; device 38.8)
 #endif
 constexpr int kLanes = FSR_LANES;  // streams a chunked call alternates over
 
