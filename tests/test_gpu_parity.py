@@ -408,7 +408,7 @@ def test_early_stop_fires(N, B):
 
 @pytest.mark.gpu
 def test_device_api_chunks_equal_unchunked(monkeypatch):
-    """Device-API calls on tall ranges run in four row chunks over two streams,
+    """Device-API calls on tall ranges run in row chunks over several streams,
     forked from and joined into the caller's stream; output, empty-support fill
     and re-run counts equal a single-launch (FSR_NO_CHUNK) engine bitwise."""
     torch = pytest.importorskip("torch")
@@ -445,13 +445,13 @@ def test_device_api_chunks_equal_unchunked(monkeypatch):
 @pytest.mark.gpu
 @pytest.mark.parametrize("support,reducer", [(16, "tree"), (32, "tree"), (64, "linear")])
 def test_host_api_chunks_tma_rows(support, reducer):
-    """Four uneven chunks (the staging buffers grow between chunks on the same
+    """Uneven chunks (the staging buffers grow between chunks on the same
     lane) with TMA window gathers whose tensor maps start at each chunk's first
     row: twice in a row, the host-buffer call equals the unchunked device call
     bitwise."""
     torch = pytest.importorskip("torch")
     from paper_2202_13926_b200 import _lib
-    H, W = 4 * 259, 256  # 259 block rows -> chunks of 64/65/65/65
+    H, W = 4 * 259, 256  # 259 block rows -> 6 uneven chunks
     img = oracle.synthetic_frame(H, W, 43)
     sampled, mask = oracle.quarter_sample(img, 5)
     px = np.where(mask, sampled, 0.0).astype(np.float32)
