@@ -191,7 +191,7 @@ typedef struct {
 /* fsr_stats.flags: the N=32 fp32 kernel gathered its windows with TMA (2-D
  * tensor maps, zero fill outside the image).  Set FSR_NO_TMA=1 in the
  * environment before fsr_engine_create to force the plain-load gather.
- * Calls over at least 80 block rows run in up to 8 row chunks alternating
+ * Calls over at least 80 block rows run in up to 12 row chunks alternating
  * over up to eight internal streams (forked from / joined into the caller's stream
  * for the device API); results are identical to one launch.  FSR_NO_CHUNK=1
  * at fsr_engine_create makes every call a single launch (kernel timing). */
