@@ -1,7 +1,7 @@
 # ncu evidence for profiles/r01/ (run from the repo root under gpurun): launch list of
 # the default bench command, --set full captures of warp32 and pair64, summaries.
 # launch list of the default bench command + one full ncu capture of the 4K main kernel (unchunked)
-ncu --metrics gpu__time_duration.sum --clock-control none -s 12 -c 60 --csv --log-file gpurun_out/launches_4k.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/launch_run.log 2>&1
+FSR_NO_CHUNK=1 ncu --metrics gpu__time_duration.sum --clock-control none -s 12 -c 40 --csv --log-file gpurun_out/launches_4k.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/launch_run.log 2>&1
 FSR_NO_CHUNK=1 ncu --set full --clock-control none --import-source on -k regex:warp32_kernel -s 2 -c 1 -o gpurun_out/w32_4k python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_run.log 2>&1
 FSR_NO_CHUNK=1 ncu --set full --clock-control none --import-source on -k regex:pair64_kernel -s 2 -c 1 -o /tmp/p64_4k python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_run2.log 2>&1
 python tools/ncu_summary.py gpurun_out/w32_4k.ncu-rep gpurun_out/warp32_ncu > gpurun_out/sum1.log 2>&1
