@@ -90,6 +90,8 @@ def parse():
     ap.add_argument("--support", type=int, default=32)
     ap.add_argument("--block", type=int, default=4)
     ap.add_argument("--image", default="natural", choices=["natural", "uniform"])
+    ap.add_argument("--io", default="f64", choices=["f64", "f32"],
+                    help="pixel type in and out: f64 is the reference's own (core.py:24)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
@@ -104,10 +106,15 @@ def make_frame(H, W, kind):
     return np.where(mask, img, 0.0), mask, img
 
 
+PROFILE_ROUND = "r02"  # the committed ncu captures the roofline's traffic / issue come from
+
+
 def ncu_traffic(kernel_prefix, name="warp32_ncu.json"):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (tools/ncu_summary.py), for the workload it was taken on."""
-    path = os.path.join(ROOT, "profiles", "r01", name)
+    path = os.path.join(ROOT, "profiles", PROFILE_ROUND, name)
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -122,7 +129,9 @@ def ncu_traffic(kernel_prefix, name="warp32_ncu.json"):
 def ncu_issue(kernel_prefix, name="warp32_ncu.json"):
     """Issue-slot view of the dominant kernel from the same committed capture:
     the loop is bound by instruction issue and dependency latency, not FLOPs."""
-    path = os.path.join(ROOT, "profiles", "r01", name)
+    path = os.path.join(ROOT, "profiles", PROFILE_ROUND, name)
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", "r01", name)
     try:
         with open(path) as f:
             d = json.load(f)
@@ -135,7 +144,7 @@ def ncu_issue(kernel_prefix, name="warp32_ncu.json"):
                     "fma_pipe_pct": ln.get("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
                     "alu_pipe_pct": ln.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
                     "warps_per_smsp": ln.get("smsp__warps_active.avg.per_cycle_active"),
-                    "source": f"ncu --set full, profiles/r01/{name}"}
+                    "source": f"ncu --set full, {os.path.relpath(path, ROOT)}"}
     return None
 
 
@@ -145,6 +154,25 @@ def peaks():
             return json.load(f), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+FP_PEAKS = os.path.join("profiles", "r02", "b200_fp_peaks.json")
+
+
+def fp_peak(fp64: bool):
+    """Measured non-tensor FP32 / FP64 peak of this pool's B200 (saturating
+    FFMA / DFMA at 16 warps per SMSP, tools/micro/peak_flops.cu; committed
+    under profiles/).  Falls back to the nominal 148 SM x lanes x 2 x clock."""
+    try:
+        with open(os.path.join(ROOT, FP_PEAKS)) as f:
+            d = json.load(f)
+        v = d["fp64_tflops" if fp64 else "fp32_tflops"]
+        mhz = d["rows"][0]["sm_mhz"]
+        return v, (f"measured: {FP_PEAKS} ({'DFMA' if fp64 else d['fp32_form']}, 16 warps/SMSP, "
+                   f"{mhz:.0f} MHz)")
+    except (OSError, KeyError, IndexError):
+        lanes = 64 if fp64 else 128
+        return 148 * lanes * 2 * 1.965e9 / 1e12, f"nominal: 148 SM x {lanes} lanes x 2 flop x 1965 MHz"
 
 
 class Clocks:
@@ -380,51 +408,60 @@ def main():
     if args.workload == "stream64":
         run_stream(args)
         return
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        # make the communicator visible in the log: NCCL prints nranks at init
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     local, backend = rank_device()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group(backend, device_id=torch.device("cuda", local))
 
-    from paper_2202_13926_b200 import _lib
+    import paper_2202_13926_b200 as fsr
+    from paper_2202_13926_b200 import _lib, shard
     from paper_2202_13926_b200.engine import effective_guard_tau
 
     H, W = WORKLOADS[args.workload]
     B, N, I = args.block, args.support, args.iterations
     L = (N - B) // 2
     sampled, mask, original = make_frame(H, W, args.image)
-    px32 = sampled.astype(np.float32)
+    io = args.io
+    npdt = np.float64 if io == "f64" else np.float32
+    tdt = torch.float64 if io == "f64" else torch.float32
+    esz = 8 if io == "f64" else 4
+    pxh = np.ascontiguousarray(sampled, dtype=npdt)
     m8 = mask.astype(np.uint8)
-    from paper_2202_13926_b200 import shard
 
     brows, bcols = -(-H // B), -(-W // B)
     row0, row1 = shard.strip_rows(brows, rank, world)
     my_blocks = (row1 - row0) * bcols
+    fill = shard.frame_fill(sampled, mask)  # the frame-wide empty-support value (never used here)
 
     eng = _lib.Engine([local])
     params = _lib.make_params(B, L, I, 0.7, 0.5, args.reducer, False, args.precision, args.argmax,
                               kernel=args.kernel)
     dev = torch.device("cuda", local)
-    d_px = torch.from_numpy(px32).to(dev)
+    d_px = torch.from_numpy(pxh).to(dev)
     d_mask = torch.from_numpy(m8).to(dev)
-    d_out = torch.zeros((H, W), dtype=torch.float32, device=dev)
+    d_out = torch.zeros((H, W), dtype=tdt, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
 
-    def step():
-        eng.reconstruct_device(d_px.data_ptr(), W, d_mask.data_ptr(), W, H, W, row0, row1,
-                               d_out.data_ptr(), W, params, stream.cuda_stream)
+    def step(e=eng):
+        e.reconstruct_device(d_px.data_ptr(), W, d_mask.data_ptr(), W, H, W, row0, row1,
+                             d_out.data_ptr(), W, params, stream.cuda_stream, fill=fill, io=io)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else 3):
+    for _ in range(max(args.warmup, 3)):
         step()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -444,26 +481,21 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms = float(np.mean(step_ms))
 
-    # ---- the dominant kernel alone: the timed steps run in row chunks on two
-    # streams (a chunk's fp64 re-run and launch tail overlap the next chunk's main
-    # kernel), so its per-chunk brackets include co-running work.  The roofline
+    # ---- the dominant kernel alone: the timed steps run in row chunks on eight
+    # streams (a chunk's fp64 re-run and launch tail overlap the other chunks' main
+    # kernels), so its per-chunk brackets include co-running work.  The roofline
     # is taken from unchunked calls (one main-kernel launch each), same frame,
     # L2 flushed, CUDA events around the launch on its stream.
     os.environ["FSR_NO_CHUNK"] = "1"
     eng1 = _lib.Engine([local])
     del os.environ["FSR_NO_CHUNK"]
-
-    def step1():
-        eng1.reconstruct_device(d_px.data_ptr(), W, d_mask.data_ptr(), W, H, W, row0, row1,
-                                d_out.data_ptr(), W, params, stream.cuda_stream)
-
-    step1()
+    step(eng1)
     barrier()
     main_chunked = main_ms
     main_ms = []
     for i in range(args.steps):
         flush.fill_(float(i))
-        step1()
+        step(eng1)
         main_ms.append(eng1.last_stats()["main_ms"])
     barrier()
     eng1.close()
@@ -473,44 +505,71 @@ def main():
     ms_max = float(t.item())
     fps = 1000.0 / ms_max
 
-    # ---- end to end through the public C-ABI call with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        hp = torch.from_numpy(px32).pin_memory()
-        hm = torch.from_numpy(m8).pin_memory()
-        ho = torch.zeros((H, W), dtype=torch.float32).pin_memory()
-        hpn, hmn, hon = hp.numpy(), hm.numpy(), ho.numpy()
-        for _ in range(2):
-            eng.reconstruct_rows(hpn, hmn, params, row0, row1, hon)
-        e2e_t = []
-        for _ in range(args.steps):
+    ya, yb = max(0, row0 * B - L), min(H, row1 * B + L)
+    oa, ob = min(H, row0 * B), min(H, row1 * B)
+
+    def timed(fn, reps):
+        fn()
+        fn()
+        ts = []
+        for _ in range(reps):
             barrier()
             t0 = time.perf_counter()
-            eng.reconstruct_rows(hpn, hmn, params, row0, row1, hon)
-            e2e_t.append(time.perf_counter() - t0)
-        e = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device=dev)
+            fn()
+            ts.append(time.perf_counter() - t0)
+        e = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e, op=dist.ReduceOp.MAX)
-        ya, yb = max(0, row0 * B - L), min(H, row1 * B + L)
-        oa, ob = min(H, row0 * B), min(H, row1 * B)
-        e2e = {"value": 1.0 / float(e.item()), "unit": "fps",
-               "h2d_bytes_per_step": int((yb - ya) * W * 5),
-               "d2h_bytes_per_step": int((ob - oa) * W * 4),
-               "ms_per_step": float(e.item()) * 1e3}
-        # quality of this run against the original frame (rank 0 holds its strip only)
-        out_full = ho.numpy()
+        return float(e.item())
+
+    # ---- end to end with HOST buffers, H2D / D2H inside the timed region.
+    # Headline: the reference-facing public API on plain (pageable) numpy arrays
+    # of the reference's own pixel type -- engine.reconstruct (N = 1; the same
+    # C-ABI call, fsr_reconstruct_<io>) or the strip call fsr_reconstruct_rows_<io>
+    # (N > 1) -- staged through the engine's own pinned buffers.  Beside it the
+    # same C-ABI call on buffers the caller pinned.
+    e2e = e2e_pinned = None
+    if not args.no_e2e:
+        h2d = int((yb - ya) * W * (esz + 1))
+        d2h = int((ob - oa) * W * esz)
+        if world == 1:
+            def api():
+                return fsr.reconstruct(pxh, mask, B, N, I, reducer=args.reducer,
+                                       precision=args.precision, argmax=args.argmax)
+        else:
+            hout = np.zeros((H, W), npdt)
+
+            def api():
+                return eng.reconstruct_rows(pxh, m8, params, row0, row1, hout, fill=fill)
+        s_api = timed(api, args.steps)
+        e2e = {"value": 1.0 / s_api, "unit": "fps", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": s_api * 1e3,
+               "call": ("paper_2202_13926_b200.reconstruct(numpy f64 pixels, bool mask) -> "
+                        f"fsr_reconstruct_{io}" if world == 1 else f"fsr_reconstruct_rows_{io}")
+                       + " on pageable numpy buffers (engine-owned pinned staging)"}
+        hp = torch.from_numpy(pxh).pin_memory()
+        hm = torch.from_numpy(m8).pin_memory()
+        ho = torch.zeros((H, W), dtype=tdt).pin_memory()
+        hpn, hmn, hon = hp.numpy(), hm.numpy(), ho.numpy()
+        s_pin = timed(lambda: eng.reconstruct_rows(hpn, hmn, params, row0, row1, hon, fill=fill),
+                      args.steps)
+        e2e_pinned = {"value": 1.0 / s_pin, "unit": "fps", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h, "ms_per_step": s_pin * 1e3,
+                      "call": f"fsr_reconstruct_rows_{io} on caller-pinned host buffers"}
     # ---- N > 1: assemble the frame from the strips once (the only collective)
     gather = None
     if world > 1:
         try:
-            ya, yb, oa, ob = shard.strip_io_rows(row0, row1, B, L, H)
             barrier()
             g0 = time.perf_counter()
             full = shard.gather_strips(d_out[oa:ob], row0, row1, B, H, W, world)
             torch.cuda.synchronize()
             gms = (time.perf_counter() - g0) * 1e3
             ok = bool(torch.equal(full[oa:ob], d_out[oa:ob]))
-            gather = {"ms": gms, "bytes": int(H * W * 4), "collective": "all_gather_into_tensor (NCCL)",
+            gather = {"ms": gms, "bytes": int(H * W * esz),
+                      "collective": f"all_gather_into_tensor ({dist.get_backend()})",
+                      "comm_nranks": dist.get_world_size(),
+                      "comm_nranks_ok": dist.get_world_size() == world,
                       "own_strip_intact": ok}
         except Exception as exc:  # report, never lose the timing line
             gather = {"error": repr(exc)[:200]}
@@ -521,9 +580,7 @@ def main():
     achieved = flop / (mean_main * 1e-3) / 1e12
     clk_hz = pk.get("sm_max_mhz", 1965.0) * 1e6
     fp64 = args.precision == "fp64"
-    lanes = 64 if fp64 else 128  # B200: DFMA at half the FFMA rate
-    peak_fl = 148 * lanes * 2 * clk_hz / 1e12
-    fast = N == 32 and B * B <= 32
+    peak_fl, peak_src = fp_peak(fp64)
     if N == 32 and B * B <= 32:
         kernel = ("warp64_kernel" if args.kernel == "warp" else "pair64_kernel") if fp64 else "warp32_kernel"
     elif N == 16 and B * B <= 32:
@@ -534,13 +591,12 @@ def main():
         kernel = "image_generic_kernel"
     w_bytes = my_blocks * I * N * N * (16 if fp64 else 8)  # W read once per bin per iteration
     smem_peak = 148 * 128 * clk_hz / 1e12  # TB/s, 128 B/clk/SM
-    io_bytes = ((min(H, row1 * B + L) - max(0, row0 * B - L)) * W * 5
-                + (min(H, row1 * B) - min(H, row0 * B)) * W * 4)
+    io_bytes = (yb - ya) * W * (esz + 1) + (ob - oa) * W * esz
     traffic, traffic_src, issue = None, None, None
     # committed ncu captures (tools/profile_round.sh) for the default line of each kernel
-    captured = {("warp32_kernel", "4k"): ("warp32_ncu.json", "void warp32_kernel<4, 1, 2, 1, 0"),
-                ("warp16_kernel", "1080p"): ("warp16_ncu.json", "void warp16_kernel<4, 1, 2, 1, 0"),
-                ("cta64_kernel", "1080p"): ("cta64_ncu.json", "void cta64_kernel<1>")}
+    captured = {("warp32_kernel", "4k"): ("warp32_ncu.json", "void warp32_kernel<"),
+                ("warp16_kernel", "1080p"): ("warp16_ncu.json", "void warp16_kernel<"),
+                ("cta64_kernel", "1080p"): ("cta64_ncu.json", "void cta64_kernel<")}
     cap = captured.get((kernel, args.workload))
     if (cap is not None and world == 1 and args.precision == "fp32" and args.argmax == "redux"
             and I == 100 and B == 4):
@@ -548,7 +604,7 @@ def main():
         issue = ncu_issue(cap[1], cap[0])
         if traffic is not None:
             traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
-                           f"(profiles/r01/{cap[0]}); algorithmic I/O bytes " + str(io_bytes))
+                           f"(profiles/{PROFILE_ROUND}/{cap[0]}); algorithmic I/O bytes " + str(io_bytes))
     line = {
         "metric": METRIC, "value": fps, "unit": "fps", "mpixel_per_s": fps * H * W / 1e6,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
@@ -557,9 +613,10 @@ def main():
         "config": {"workload": f"{W}x{H} quarter-sampled frame, strip-partitioned over "
                                f"{world} GPU(s)", "B": B, "N": N, "iterations": I, "rho": 0.7,
                    "gamma": 0.5, "reducer": args.reducer, "precision": args.precision,
-                   "argmax": args.argmax, "kernel": args.kernel, "image": args.image, "parallelism": f"strips{world}",
+                   "argmax": args.argmax, "kernel": args.kernel, "image": args.image,
+                   "parallelism": f"strips{world}",
                    "guard_tau": effective_guard_tau(N, I) if args.precision == "fp32" else None,
-                   "io": "f32 pixels + u8 mask in, f32 out",
+                   "io": f"{io} pixels + u8 mask in, {io} out",
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,
                      "unit": "TFLOP/s", "frac": achieved / peak_fl, "traffic": traffic,
@@ -569,8 +626,7 @@ def main():
                                        "summed per-chunk brackets in the timed steps: "
                                        f"{float(np.mean(main_chunked)):.3f} ms (overlapping)",
                      "work": "blocks x N^2 (12 I + 30 log2 N) flop (SURVEY 8d)",
-                     "peak_source": f"derived: 148 SM x {lanes} lanes x 2 flop x sm_max_mhz "
-                                    f"({src} MEASURED_PEAKS.json has no non-tensor figure)",
+                     "peak_source": peak_src,
                      "smem": {"achieved_tbs": w_bytes / (mean_main * 1e-3) / 1e12,
                               "peak_tbs": smem_peak,
                               "frac": w_bytes / (mean_main * 1e-3) / 1e12 / smem_peak},
@@ -584,6 +640,7 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+        line["e2e_pinned"] = e2e_pinned
     if gather is not None:
         line["gather"] = gather
     if rank == 0 and world == 1 and not args.no_cpu:

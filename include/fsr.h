@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define FSR_ABI_VERSION 1
+#define FSR_ABI_VERSION 2  /* 2: f64 pixels on every path, explicit empty-support fill for strips */
 
 typedef enum {
     FSR_OK = 0,
@@ -96,6 +96,14 @@ int32_t fsr_abi_version(void);
  * aliases px.  sel (nullable): [n_blocks, iterations] selected flat bins
  * (u*N+v) per block in partition order, -1 after an early stop; done
  * (nullable): [n_blocks] iterations run.  Synchronous.
+ *
+ * Every precision takes either pixel type: _f64 is the reference's own input
+ * contract (core.py:24, f64 pixels), and the fp32-loop kernels read f64 pixels
+ * directly (their gather / weighting / FFT prologue runs in fp64), so FP32 on
+ * _f64 buffers is the production mode on the reference's exact inputs.
+ * The caller's buffers may be pageable: each device's chunks are staged
+ * through engine-owned pinned buffers by a small host thread pool, and the
+ * engine's devices run their strips concurrently (one host thread each).
  */
 int fsr_reconstruct_f64(fsr_engine *eng, const fsr_params *p, const double *px,
                         const uint8_t *mask, int64_t height, int64_t width, double *out,
@@ -105,28 +113,44 @@ int fsr_reconstruct_f32(fsr_engine *eng, const fsr_params *p, const float *px,
                         int32_t *sel, int32_t *done);
 
 /*
- * Strip variant of fsr_reconstruct_f32 for sharded callers (one process per
- * GPU): only target-block rows [row0, row1) are reconstructed; only the image
- * rows their windows touch are copied to the device and only the strip's
- * output rows of `out` (a full H*W host buffer) are written.
+ * Strip variant for sharded callers (one process per GPU): only target-block
+ * rows [row0, row1) are reconstructed; only the image rows their windows touch
+ * (the strip plus L = border rows above and below) are read and only the
+ * strip's output rows of `out` (a full H*W host buffer) are written.
+ * fill: the value of empty-support blocks -- the mean of the known samples of
+ * the WHOLE frame (reconstruction.py:236-237), which a strip holder computes
+ * once (or gets by an all-reduce of sum and count); pass NaN to have it
+ * computed here from px/mask, which then must hold every row of the frame.
  */
 int fsr_reconstruct_rows_f32(fsr_engine *eng, const fsr_params *p, const float *px,
                              const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
-                             int64_t row1, float *out);
+                             int64_t row1, double fill, float *out);
+int fsr_reconstruct_rows_f64(fsr_engine *eng, const fsr_params *p, const double *px,
+                             const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
+                             int64_t row1, double fill, double *out);
 
 /*
  * Device-resident call on the engine's first device, asynchronous on `stream`
  * (a cudaStream_t; NULL = legacy default stream).  d_px/d_mask/d_out are
  * device pointers with row pitches in ELEMENTS.  row0/row1 restrict the work
  * to target-block rows [row0, row1) of the full image (strip partitioning);
- * pass 0 and ceil(H/B) for the whole frame.  The halo (L rows above/below)
- * is read from d_px/d_mask, which must hold the full image rows the strip's
- * windows touch.  f32 I/O; the loop runs in the requested precision.
+ * pass 0 and ceil(H/B) for the whole frame.  Only the image rows the strip's
+ * windows touch (L rows above and below) are read, unless fill is NaN: then
+ * the empty-support fill is the mean of the known samples of all H rows,
+ * summed on the device in a fixed order (deterministic), and all H rows must
+ * be valid.  With no known sample anywhere the call's fsr_last_stats returns
+ * FSR_ENOSAMPLES ("no known samples").  Calls on one engine are serialised in
+ * issue order even across different streams (each waits for the previous
+ * call's end), because they share the engine's per-call scratch.
  */
 int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
                                int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
                                int64_t height, int64_t width, int64_t row0, int64_t row1,
-                               float *d_out, int64_t out_pitch, void *stream);
+                               float *d_out, int64_t out_pitch, double fill, void *stream);
+int fsr_reconstruct_device_f64(fsr_engine *eng, const fsr_params *p, const double *d_px,
+                               int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
+                               int64_t height, int64_t width, int64_t row0, int64_t row1,
+                               double *d_out, int64_t out_pitch, double fill, void *stream);
 
 /*
  * Array-level loop operator (_kernels.reconstruct_batch plus the traces of
@@ -178,7 +202,9 @@ int fsr_sq_error_device(fsr_engine *eng, const float *d_ref, int64_t ref_pitch, 
                         int64_t test_pitch, int64_t height, int64_t width, double *d_sse,
                         void *stream);
 
-/* Statistics of the last image call on the first device. */
+/* Statistics of the last image call (kernel times of the first device).  For
+ * an asynchronous device call this waits for it, and returns FSR_ENOSAMPLES if
+ * the call found an empty-support block but no known sample. */
 typedef struct {
     int64_t blocks;          /* target blocks processed */
     int64_t rerun_blocks;    /* blocks re-run in fp64 by the near-tie guard */
@@ -191,7 +217,7 @@ typedef struct {
 /* fsr_stats.flags: the N=32 fp32 kernel gathered its windows with TMA (2-D
  * tensor maps, zero fill outside the image).  Set FSR_NO_TMA=1 in the
  * environment before fsr_engine_create to force the plain-load gather.
- * Calls over at least 80 block rows run in up to 12 row chunks alternating
+ * Calls over at least 24 block rows run in 3..12 row chunks alternating
  * over up to eight internal streams (forked from / joined into the caller's stream
  * for the device API); results are identical to one launch.  FSR_NO_CHUNK=1
  * at fsr_engine_create makes every call a single launch (kernel timing). */

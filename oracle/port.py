@@ -276,14 +276,17 @@ def block_origins(height: int, width: int, block: int):
 
 
 def reconstruct_image(pixels, mask, block=4, border=14, iterations=100, rho=0.7, gamma=0.5,
-                      reducer="tree", early_stop=False, threads=0, trace=False, block_rows=None):
+                      reducer="tree", early_stop=False, threads=0, trace=False, block_rows=None,
+                      fill_value=None):
     """reconstruction.py:216-290 restated: spans of 128 blocks, numpy FFTs,
     the C loop, inverse FFT, merge and stitch.  With ``trace`` the per-block
     selections/objectives/ties/done are returned as well (they are the
     reference's reconstruct_block_full traces, reconstruction.py:159-203).
     ``block_rows=(r0, r1)`` restricts the work to target-block rows [r0, r1)
     (a strip; other pixels keep the sampled values) -- the per-block result is
-    independent of which other blocks are processed (reconstruction.py:220-226)."""
+    independent of which other blocks are processed (reconstruction.py:220-226).
+    ``fill_value`` overrides the empty-support value (reconstruction.py:236-237)
+    for a strip caller that holds only its halo rows."""
     if reducer not in REDUCERS:
         raise ValueError(f"unknown argmax strategy {reducer!r}, expected one of {REDUCERS}")
     use_tree = reducer == "tree"
@@ -298,7 +301,10 @@ def reconstruct_image(pixels, mask, block=4, border=14, iterations=100, rho=0.7,
     wf_flat = np.ascontiguousarray(frequency_weight(s)).ravel()
     decay = decay_grid(s, rho)
     known = int(np.count_nonzero(mask))
-    fill_value = float(pixels.sum()) / known if known else 0.0
+    if fill_value is None:
+        fill_value = float(pixels.sum()) / known if known else 0.0
+    else:
+        known = max(known, 1)  # the caller vouches for the frame's samples
     out = np.array(pixels)
     n = rows.size
     it = max(iterations, 1)

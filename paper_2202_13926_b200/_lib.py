@@ -87,11 +87,14 @@ def load():
         L.fsr_reconstruct_f64.restype = ctypes.c_int
         L.fsr_reconstruct_f32.argtypes = [P, pp, P, P, i64, i64, P, P, P]
         L.fsr_reconstruct_f32.restype = ctypes.c_int
-        L.fsr_reconstruct_rows_f32.argtypes = [P, pp, P, P, i64, i64, i64, i64, P]
-        L.fsr_reconstruct_rows_f32.restype = ctypes.c_int
-        L.fsr_reconstruct_device_f32.argtypes = [P, pp, P, i64, P, i64, i64, i64, i64, i64, P,
-                                                 i64, P]
-        L.fsr_reconstruct_device_f32.restype = ctypes.c_int
+        dbl = ctypes.c_double
+        for io in ("f32", "f64"):
+            f = getattr(L, f"fsr_reconstruct_rows_{io}")
+            f.argtypes = [P, pp, P, P, i64, i64, i64, i64, dbl, P]
+            f.restype = ctypes.c_int
+            f = getattr(L, f"fsr_reconstruct_device_{io}")
+            f.argtypes = [P, pp, P, i64, P, i64, i64, i64, i64, i64, P, i64, dbl, P]
+            f.restype = ctypes.c_int
         L.fsr_iterate_spectra.argtypes = [P, pp, i64, i32, P, P, P, P, P, P, P, P, P]
         L.fsr_iterate_spectra.restype = ctypes.c_int
         L.fsr_spatial_oracle.argtypes = [P, i32, i32, ctypes.c_double, i64, P, P, P, P, P, P, P, P, P]
@@ -108,7 +111,8 @@ def load():
 
 EXPORTED = ["fsr_params_init", "fsr_params_validate", "fsr_engine_create", "fsr_engine_destroy",
             "fsr_last_error", "fsr_status_string", "fsr_abi_version", "fsr_reconstruct_f64",
-            "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_device_f32", "fsr_iterate_spectra",
+            "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_rows_f64",
+            "fsr_reconstruct_device_f32", "fsr_reconstruct_device_f64", "fsr_iterate_spectra",
             "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats", "fsr_spatial_oracle"]
 
 
@@ -191,22 +195,29 @@ class Engine:
                        _ptr(sel), _ptr(done)))
         return out
 
-    def reconstruct_rows(self, px, mask, params: FsrParamsC, row0: int, row1: int, out):
-        """Strip call on host buffers: block rows [row0, row1) into ``out`` (full size)."""
+    def reconstruct_rows(self, px, mask, params: FsrParamsC, row0: int, row1: int, out,
+                         fill: float = float("nan")):
+        """Strip call on host buffers: block rows [row0, row1) into ``out`` (full size).
+        ``fill``: the empty-support value (the whole frame's mean of the known
+        samples); NaN = computed from ``px``/``mask``, which must then hold every row."""
         h, w = px.shape
-        assert px.dtype == np.float32 and out.dtype == np.float32 and mask.dtype == np.uint8
+        assert px.dtype in (np.float32, np.float64) and out.dtype == px.dtype and mask.dtype == np.uint8
         assert px.flags.c_contiguous and out.flags.c_contiguous and mask.flags.c_contiguous
-        self._check(self._L.fsr_reconstruct_rows_f32(self._h, ctypes.byref(params), _ptr(px),
-                                                     _ptr(mask), h, w, row0, row1, _ptr(out)))
+        fn = self._L.fsr_reconstruct_rows_f64 if px.dtype == np.float64 else self._L.fsr_reconstruct_rows_f32
+        self._check(fn(self._h, ctypes.byref(params), _ptr(px), _ptr(mask), h, w, row0, row1,
+                       float(fill), _ptr(out)))
         return out
 
     def reconstruct_device(self, d_px, px_pitch, d_mask, mask_pitch, height, width, row0, row1,
-                           d_out, out_pitch, params: FsrParamsC, stream=0):
-        """Device pointers (ints), asynchronous on ``stream`` (a cudaStream_t as int)."""
-        self._check(self._L.fsr_reconstruct_device_f32(
-            self._h, ctypes.byref(params), ctypes.c_void_p(d_px), px_pitch,
-            ctypes.c_void_p(d_mask), mask_pitch, height, width, row0, row1,
-            ctypes.c_void_p(d_out), out_pitch, ctypes.c_void_p(stream)))
+                           d_out, out_pitch, params: FsrParamsC, stream=0,
+                           fill: float = float("nan"), io: str = "f32"):
+        """Device pointers (ints), asynchronous on ``stream`` (a cudaStream_t as int).
+        ``io``: pixel type "f32" or "f64"; ``fill`` as in reconstruct_rows (NaN:
+        the device computes the mean from all ``height`` rows of d_px/d_mask)."""
+        fn = {"f32": self._L.fsr_reconstruct_device_f32, "f64": self._L.fsr_reconstruct_device_f64}[io]
+        self._check(fn(self._h, ctypes.byref(params), ctypes.c_void_p(d_px), px_pitch,
+                       ctypes.c_void_p(d_mask), mask_pitch, height, width, row0, row1,
+                       ctypes.c_void_p(d_out), out_pitch, float(fill), ctypes.c_void_p(stream)))
 
     def iterate_spectra(self, R, G, W, wf, params: FsrParamsC, thr=None, sel=None, obj=None,
                         ties=None, done=None):
@@ -258,8 +269,11 @@ class Engine:
             width, ctypes.c_void_p(d_sse), ctypes.c_void_p(stream)))
 
     def last_stats(self) -> dict:
+        """Statistics of the last call (waits for an asynchronous device call);
+        raises ValueError("no known samples") if that call found an empty window
+        in a frame without any known sample."""
         s = FsrStatsC()
-        self._L.fsr_last_stats(self._h, ctypes.byref(s))
+        self._check(self._L.fsr_last_stats(self._h, ctypes.byref(s)))
         return {f: getattr(s, f) for f, _ in FsrStatsC._fields_ if f != "reserved"}
 
 

@@ -19,7 +19,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -28,6 +30,7 @@
 #include <tuple>
 #include <vector>
 
+#define FSR_ABI_TU
 #include "../../include/fsr.h"
 #include "fsr_common.cuh"
 #include "fsr_generic.cuh"
@@ -38,6 +41,7 @@
 #include "fsr_aux.cuh"
 #include "fsr_spatial.cuh"
 #include "fsr_warp64.cuh"
+#include "fsr_launch.cuh"
 
 using namespace fsr;
 
@@ -69,34 +73,137 @@ struct TableSet {
     DevBuf f64, f32;  // decay[N*N] | wf[N*N] | cs[2N]
 };
 
-struct Counters {  // device-side, zeroed per call
-    unsigned int empty_count;
-    unsigned int rerun_count;
-    unsigned int ticket;
-    int status;
-    double acc[2];
-    double fill;
+// Pinned host staging of the host-buffer calls (SURVEY §8b "Ownership": the
+// engine owns device buffers and pinned staging, reused across calls).
+struct HostBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t need) {
+        if (need <= bytes) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        cudaError_t e = cudaHostAlloc(&p, need, cudaHostAllocPortable);
+        if (e == cudaSuccess) bytes = need;
+        return e;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <typename T>
+    T *as() const { return reinterpret_cast<T *>(p); }
 };
+
+struct ChunkCtr {              // device-side, per row chunk, zeroed on the chunk's stream
+    unsigned int rerun_count;  // blocks queued for the fp64 re-run (guarded fp32)
+    unsigned int skip_empty;   // the re-run kernels' empty counter (already counted)
+};
+struct CallCtr {               // device-side, per call and device, zeroed once per call
+    unsigned int empty_count;  // empty-support blocks over all chunks (list: Device::empty_list)
+    int status;                // 2: an empty block but no known sample anywhere
+};
+
+// A small persistent worker pool for the host-side staging copies (parallel
+// memcpy between the caller's pageable buffers and the pinned staging).  All
+// state is under one mutex; tasks are few (a chunk's rows in T pieces) and
+// each is a large memcpy, so the lock is never contended in practice.
+class Pool {
+  public:
+    explicit Pool(int n) {
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : workers_) t.join();
+    }
+    int size() const { return (int)workers_.size() + 1; }
+    // fn(i) for i in [0, n) on the workers and the calling thread; returns when all are done
+    void run(int n, const std::function<void(int)> &fn) {
+        std::unique_lock<std::mutex> lk(m_);
+        job_ = &fn;
+        next_ = 0;
+        total_ = n;
+        pending_ = n;
+        cv_.notify_all();
+        while (next_ < total_) {
+            const int i = next_++;
+            lk.unlock();
+            fn(i);
+            lk.lock();
+            --pending_;
+        }
+        done_.wait(lk, [&] { return pending_ == 0; });
+        job_ = nullptr;
+        total_ = 0;
+    }
+
+  private:
+    void loop() {
+        std::unique_lock<std::mutex> lk(m_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || (job_ && next_ < total_); });
+            if (stop_) return;
+            const int i = next_++;
+            const std::function<void(int)> *f = job_;
+            lk.unlock();
+            (*f)(i);
+            lk.lock();
+            if (--pending_ == 0) done_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    const std::function<void(int)> *job_ = nullptr;
+    int next_ = 0, total_ = 0, pending_ = 0;
+    bool stop_ = false;
+};
+
+// rows [0, rows) of `bytes_per_row` from src to dst, split over the pool
+void pool_copy(Pool *pool, void *dst, const void *src, int64_t rows, size_t bytes_per_row) {
+    const size_t total = (size_t)rows * bytes_per_row;
+    const int parts = (pool && total >= ((size_t)1 << 20)) ? pool->size() : 1;
+    auto piece = [&](int i) {
+        const int64_t r0 = rows * i / parts, r1 = rows * (i + 1) / parts;
+        if (r1 > r0)
+            std::memcpy((char *)dst + r0 * bytes_per_row, (const char *)src + r0 * bytes_per_row,
+                        (size_t)(r1 - r0) * bytes_per_row);
+    };
+    if (parts == 1) piece(0);
+    else pool->run(parts, piece);
+}
 
 struct Device {
     int id = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_mid = nullptr;
-    DevBuf px, mask, out, sel, done, empty_list, rerun_list, counters;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_done = nullptr;  // end of the engine's last call on this device (calls are serialised)
+    DevBuf px, mask, out, sel, done, empty_list, rerun_list, call_ctr, chunk_ctrs, fill_partials;
     DevBuf R, G, W, wf, thr, obj, ties, partials, c64scratch;
+    HostBuf hin, hout;  // pinned staging of a lane's chunk (host-buffer calls)
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
     int launches = 0;
     float *gap_debug = nullptr;  // device buffer for fsr_debug_guard_gaps (null = off)
-    bool tma_enabled = true;     // warp32 window gather by TMA when the rows allow it
+    bool tma_enabled = true;     // window gather by TMA when the rows allow it
     bool chunking = true;        // large calls in row chunks over kLanes streams (FSR_NO_CHUNK=1: off)
-    int used_tma = 0;            // last warp32 launch gathered by TMA
-    // host-buffer calls on large strips are pipelined over kLanes "lanes" (same GPU,
-    // own stream, staging buffers and scratch): H2D of chunk c+1 and D2H of chunk
-    // c-1 overlap the kernels of chunk c
+    int used_tma = 0;            // last fp32-loop launch gathered by TMA
+    // Calls run as K row chunks over kLanes "lanes" (same GPU, own stream, staging
+    // buffers and re-run scratch): one chunk's copies, fp64 re-run and launch
+    // tail overlap the other chunks' main kernels.
     std::vector<std::unique_ptr<Device>> lanes;
-    int dev_chunks = 1;  // chunks of the last device-API call (for its statistics)
+    std::unique_ptr<Pool> pool;  // host staging copies (host-buffer calls)
+    int last_chunks = 0;         // chunks of the last call (for its statistics)
     cudaEvent_t ck0[16] = {}, ck1[16] = {};  // per-chunk main-kernel brackets (K <= 16)
+    // host pipeline: the chunk whose output is still in this lane's pinned staging
+    bool pending = false;
+    int64_t pend_oa = 0, pend_ob = 0;
 };
 
 }  // namespace
@@ -104,6 +211,7 @@ struct Device {
 struct fsr_engine {
     std::vector<std::unique_ptr<Device>> devs;
     std::string err;
+    std::mutex err_mu;  // err is written by the per-device worker threads of a host call
     std::mutex mu;
     fsr_stats stats{};
     bool device_stats_pending = false;
@@ -119,7 +227,10 @@ int fail(fsr_engine *eng, int code, const char *fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
-    if (eng) eng->err = buf;
+    if (eng) {
+        std::lock_guard<std::mutex> lk(eng->err_mu);
+        eng->err = buf;
+    }
     g_err = buf;
     return code;
 }
@@ -250,110 +361,52 @@ int check_params(fsr_engine *eng, const fsr_params *p) {
     return FSR_OK;
 }
 
-size_t generic_smem(int N, size_t real_bytes) { return (size_t)2 * N * N * 2 * real_bytes; }
+// One kernel launch through a launcher of fsr_launch.cuh: count it, map errors.
+#define LAUNCH_TRY(eng, d, expr)                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (expr);                                                                 \
+        if (e_ == kNotBuilt) return fail(eng, FSR_EINVAL, "kernel variant not built: %s", #expr); \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(eng, FSR_ECUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),   \
+                        __FILE__, __LINE__, #expr);                                              \
+        (d).launches++;                                                                          \
+    } while (0)
 
 template <typename Real, typename IO>
-int launch_generic(fsr_engine *eng, Device &d, ImageArgs<Real, IO> a, int grid, cudaStream_t st) {
-    size_t smem = generic_smem(a.N, sizeof(Real));
-    auto k = image_generic_kernel<Real, IO>;
-    if (smem > 48 * 1024) CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    // small supports (N*N <= 256: the paper grid's S = 8, 12) get a CTA sized to
-    // their bin count instead of 256 mostly idle threads, and proportionally
-    // more CTAs; the kernel's per-thread arrays cover 16 strides of the CTA
-    const int n = a.N * a.N;
-    int threads = GEN_THREADS;
-    if (n <= GEN_THREADS && a.B * a.B <= 16 * 64) threads = std::max(64, (n + 31) / 32 * 32);
-    int64_t g = (int64_t)grid * (GEN_THREADS / threads);
-    if (!a.list_count) g = std::min<int64_t>(g, std::max<int64_t>(a.nblocks, 1));
-    grid = (int)g;
-    k<<<grid, threads, smem, st>>>(a);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
+int launch_generic(fsr_engine *eng, Device &d, const ImageArgs<Real, IO> &a, int grid, cudaStream_t st) {
+    LAUNCH_TRY(eng, d, (generic_launch<Real, IO>(a, grid, st)));
     return FSR_OK;
 }
 
-template <int WARPS, bool TREE, int AM, bool GUARD, bool STUDY = false, int OPTS = W32_ALL>
-int launch_warp32_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
-                    cudaStream_t st) {
-    auto k = warp32_kernel<WARPS, TREE, AM, GUARD, STUDY, OPTS>;
-    const size_t smem = sizeof(Warp32Smem<WARPS>);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t want = (a.nblocks + WARPS - 1) / WARPS;
-    int grid = (int)std::min<int64_t>(want, (int64_t)d.sms * per_sm);
-    if (grid < 1) grid = 1;
-    k<<<grid, WARPS * 32, smem, st>>>(a, maps);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
-template <int BPC, bool TREE, int AM, typename IO>
-int launch_pair64_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
-                    cudaStream_t st) {
-    auto k = pair64_kernel<BPC, TREE, AM, IO>;
-    const size_t smem = sizeof(Pair64Smem<BPC>);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BPC * 64, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t want = (want_blocks + BPC - 1) / BPC;
-    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
-    k<<<grid, BPC * 64, smem, st>>>(a);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
-#ifndef FSR_P64_BPC
-#define FSR_P64_BPC 4
-#endif
-constexpr int kPairBPC = FSR_P64_BPC;
-
-template <typename IO>
-int launch_pair64(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
-                  int64_t want_blocks, cudaStream_t st) {
-#define FSR_P64(T, A) \
-    if (tree == T && am == A) return launch_pair64_t<kPairBPC, T, A, IO>(eng, d, a, want_blocks, st);
-    FSR_P64(true, AM_SHFL) FSR_P64(false, AM_SHFL) FSR_P64(true, AM_REDUX)
-    FSR_P64(false, AM_REDUX) FSR_P64(true, AM_SMEM) FSR_P64(false, AM_SMEM)
-#undef FSR_P64
-    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
-}
-
-template <int WARPS, bool TREE, int AM, typename IO>
-int launch_warp64_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
-                    cudaStream_t st) {
-    auto k = warp64_kernel<WARPS, TREE, AM, IO>;
-    const size_t smem = sizeof(Warp64Smem<WARPS>);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t want = (want_blocks + WARPS - 1) / WARPS;
-    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
-    k<<<grid, WARPS * 32, smem, st>>>(a);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
-constexpr int kWarp64Warps = 5;
-
+// N=32 fp64 kernel: auto/pair = two warps per block (pair64), warp = one (warp64)
 template <typename IO>
 int launch_fp64_n32(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, const fsr_params *p,
                     int64_t want_blocks, cudaStream_t st) {
     const bool tree = p->reducer == FSR_REDUCER_TREE;
-    const int am = p->argmax_impl;
-    if (p->kernel != 1) return launch_pair64<IO>(eng, d, a, tree, am, want_blocks, st);  // auto/pair
-#define FSR_W64(T, A) \
-    if (tree == T && am == A) return launch_warp64_t<kWarp64Warps, T, A, IO>(eng, d, a, want_blocks, st);
-    FSR_W64(true, AM_SHFL) FSR_W64(false, AM_SHFL) FSR_W64(true, AM_REDUX)
-    FSR_W64(false, AM_REDUX) FSR_W64(true, AM_SMEM) FSR_W64(false, AM_SMEM)
-#undef FSR_W64
-    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
+    if (p->kernel != 1)
+        LAUNCH_TRY(eng, d, (pair64_launch<IO>(a, tree, p->argmax_impl, want_blocks, d.sms, st)));
+    else
+        LAUNCH_TRY(eng, d, (warp64_launch<IO>(a, tree, p->argmax_impl, want_blocks, d.sms, st)));
+    return FSR_OK;
+}
+
+template <typename IO>
+int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
+                   int64_t want_blocks, cudaStream_t st) {
+    LAUNCH_TRY(eng, d, (warp16d_launch<IO>(a, tree, am, want_blocks, d.sms, st)));
+    return FSR_OK;
+}
+
+template <typename IO>
+int launch_cta64d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
+                  cudaStream_t st) {
+    int grid = 1;
+    CUDA_TRY(eng, cta64d_grid<IO>(want_blocks, d.sms, &grid));
+    CUDA_TRY(eng, d.c64scratch.ensure((size_t)grid * 4096 * sizeof(double2)));
+    Pair64Args<IO> b = a;
+    b.scratch = d.c64scratch.as<double2>();
+    LAUNCH_TRY(eng, d, (cta64d_launch<IO>(b, grid, st)));
+    return FSR_OK;
 }
 
 template <typename IO>
@@ -376,11 +429,6 @@ bool pair64_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 32 && p->block * p->block <= 32;
 }
 
-#ifndef FSR_W32_CTA_WARPS
-#define FSR_W32_CTA_WARPS 4
-#endif
-constexpr int kWarps = FSR_W32_CTA_WARPS;
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -395,13 +443,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-// Tensor maps for the warp32 window gather: 32-row boxes widened to 16-byte
-// aligned starts (W32_BOX_PX / W32_BOX_MK columns), zero fill outside the image.  Returns false when TMA cannot address the buffers (rows not
-// 16-byte aligned); the kernel then gathers with plain loads.
-bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t mask_pitch,
-                 int64_t H, int64_t W, Warp32Maps *m, int box_px = W32_BOX_PX, int box_mk = W32_BOX_MK,
-                 int box_rows = 32) {
-    if ((reinterpret_cast<uintptr_t>(px) & 15) || ((px_pitch * 4) & 15) ||
+// Tensor maps for the fp32-loop kernels' window gather: box_rows-row boxes
+// widened to 16-byte aligned starts (TmaBox<IO, ROWS, N> columns), zero fill
+// outside the image, for f32 or f64 pixels.  Returns false when TMA cannot
+// address the buffers (rows not 16-byte aligned); the kernel then gathers
+// with plain loads.
+template <typename IO>
+bool window_maps(const IO *px, int64_t px_pitch, const uint8_t *mask, int64_t mask_pitch,
+                 int64_t H, int64_t W, Warp32Maps *m, int N) {
+    const int box_px = N + 16 / (int)sizeof(IO), box_mk = N + 16, box_rows = N;
+    if ((reinterpret_cast<uintptr_t>(px) & 15) || ((px_pitch * (int64_t)sizeof(IO)) & 15) ||
         (reinterpret_cast<uintptr_t>(mask) & 15) || (mask_pitch & 15) || H < 1 || W < 1 ||
         H > (int64_t)INT32_MAX || W > (int64_t)INT32_MAX)
         return false;
@@ -410,8 +461,10 @@ bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t
     const cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)H};
     const cuuint32_t bpx[2] = {(cuuint32_t)box_px, (cuuint32_t)box_rows},
                      bmk[2] = {(cuuint32_t)box_mk, (cuuint32_t)box_rows}, estr[2] = {1, 1};
-    const cuuint64_t spx[1] = {(cuuint64_t)px_pitch * 4}, smk[1] = {(cuuint64_t)mask_pitch};
-    if (enc(&m->px, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(px), dims, spx, bpx, estr,
+    const cuuint64_t spx[1] = {(cuuint64_t)px_pitch * sizeof(IO)}, smk[1] = {(cuuint64_t)mask_pitch};
+    const CUtensorMapDataType dt =
+        sizeof(IO) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    if (enc(&m->px, dt, 2, const_cast<IO *>(px), dims, spx, bpx, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -422,116 +475,6 @@ bool warp32_maps(const float *px, int64_t px_pitch, const uint8_t *mask, int64_t
     return true;
 }
 
-int launch_warp32(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps, bool tree,
-                  int am, bool guard, cudaStream_t st) {
-    if (a.gap_out) {  // guard study (tools/guard_study.py): redux argmax only
-        if (am != AM_REDUX) return fail(eng, FSR_EINVAL, "guard study needs argmax=redux");
-        return tree ? launch_warp32_t<kWarps, true, AM_REDUX, true, true>(eng, d, a, maps, st)
-                    : launch_warp32_t<kWarps, false, AM_REDUX, true, true>(eng, d, a, maps, st);
-    }
-    // production argmax: variants without the trace / early-stop checks
-    const int opts = (a.sel ? W32_TRACE : 0) | (a.early_stop ? W32_EARLY : 0);
-#define FSR_W32R(T, G, O) \
-    if (am == AM_REDUX && tree == T && guard == G && opts == O) \
-        return launch_warp32_t<kWarps, T, AM_REDUX, G, false, O>(eng, d, a, maps, st);
-    FSR_W32R(true, true, 0) FSR_W32R(true, false, 0) FSR_W32R(false, true, 0) FSR_W32R(false, false, 0)
-    FSR_W32R(true, true, 1) FSR_W32R(true, false, 1) FSR_W32R(false, true, 1) FSR_W32R(false, false, 1)
-    FSR_W32R(true, true, 2) FSR_W32R(true, false, 2) FSR_W32R(false, true, 2) FSR_W32R(false, false, 2)
-#undef FSR_W32R
-#define FSR_W32(T, A, G) \
-    if (tree == T && am == A && guard == G) return launch_warp32_t<kWarps, T, A, G>(eng, d, a, maps, st);
-    FSR_W32(true, AM_SHFL, true) FSR_W32(true, AM_SHFL, false)
-    FSR_W32(false, AM_SHFL, true) FSR_W32(false, AM_SHFL, false)
-    FSR_W32(true, AM_REDUX, true) FSR_W32(true, AM_REDUX, false)
-    FSR_W32(false, AM_REDUX, true) FSR_W32(false, AM_REDUX, false)
-    FSR_W32(true, AM_SMEM, true) FSR_W32(true, AM_SMEM, false)
-    FSR_W32(false, AM_SMEM, true) FSR_W32(false, AM_SMEM, false)
-#undef FSR_W32
-    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
-}
-
-template <int WARPS, bool TREE, int AM, bool GUARD, int OPTS = W32_ALL>
-int launch_warp16_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
-                    cudaStream_t st) {
-    auto k = warp16_kernel<WARPS, TREE, AM, GUARD, OPTS>;
-    const size_t smem = sizeof(Warp16Smem<WARPS>);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t want = (a.nblocks + WARPS - 1) / WARPS;
-    int grid = (int)std::min<int64_t>(want, (int64_t)d.sms * per_sm);
-    if (grid < 1) grid = 1;
-    k<<<grid, WARPS * 32, smem, st>>>(a, maps);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
-int launch_warp16(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps, bool tree,
-                  int am, bool guard, cudaStream_t st) {
-    if (am == AM_REDUX && !a.sel && !a.early_stop) {  // production: no trace / early-stop checks
-        if (tree) return guard ? launch_warp16_t<kWarps, true, AM_REDUX, true, 0>(eng, d, a, maps, st)
-                               : launch_warp16_t<kWarps, true, AM_REDUX, false, 0>(eng, d, a, maps, st);
-        return guard ? launch_warp16_t<kWarps, false, AM_REDUX, true, 0>(eng, d, a, maps, st)
-                     : launch_warp16_t<kWarps, false, AM_REDUX, false, 0>(eng, d, a, maps, st);
-    }
-#define FSR_W16(T, A, G) \
-    if (tree == T && am == A && guard == G) return launch_warp16_t<kWarps, T, A, G>(eng, d, a, maps, st);
-    FSR_W16(true, AM_SHFL, true) FSR_W16(true, AM_SHFL, false)
-    FSR_W16(false, AM_SHFL, true) FSR_W16(false, AM_SHFL, false)
-    FSR_W16(true, AM_REDUX, true) FSR_W16(true, AM_REDUX, false)
-    FSR_W16(false, AM_REDUX, true) FSR_W16(false, AM_REDUX, false)
-    FSR_W16(true, AM_SMEM, true) FSR_W16(true, AM_SMEM, false)
-    FSR_W16(false, AM_SMEM, true) FSR_W16(false, AM_SMEM, false)
-#undef FSR_W16
-    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
-}
-
-template <int WARPS, bool TREE, int AM, typename IO>
-int launch_warp16d_t(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
-                     cudaStream_t st) {
-    auto k = warp16d_kernel<WARPS, TREE, AM, IO>;
-    const size_t smem = sizeof(Warp16dSmem<WARPS>);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, WARPS * 32, smem));
-    if (per_sm < 1) per_sm = 1;
-    int64_t want = (want_blocks + WARPS - 1) / WARPS;
-    int grid = (int)std::min<int64_t>(std::max<int64_t>(want, 1), (int64_t)d.sms * per_sm);
-    k<<<grid, WARPS * 32, smem, st>>>(a);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
-template <typename IO>
-int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tree, int am,
-                   int64_t want_blocks, cudaStream_t st) {
-#define FSR_W16D(T, A) \
-    if (tree == T && am == A) return launch_warp16d_t<kWarps, T, A, IO>(eng, d, a, want_blocks, st);
-    FSR_W16D(true, AM_SHFL) FSR_W16D(false, AM_SHFL) FSR_W16D(true, AM_REDUX)
-    FSR_W16D(false, AM_REDUX) FSR_W16D(true, AM_SMEM) FSR_W16D(false, AM_SMEM)
-#undef FSR_W16D
-    return fail(eng, FSR_EINVAL, "unknown argmax implementation");
-}
-
-template <bool GUARD>
-int launch_cta64_t(fsr_engine *eng, Device &d, const Warp32Args &a, const Warp32Maps &maps,
-                   cudaStream_t st) {
-    auto k = cta64_kernel<GUARD>;
-    const size_t smem = sizeof(C64Smem);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C64_THREADS, smem));
-    if (per_sm < 1) per_sm = 1;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(a.nblocks, (int64_t)d.sms * per_sm));
-    k<<<grid, C64_THREADS, smem, st>>>(a, maps);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
-}
-
 bool cta64_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 64 && p->block * p->block <= C64_THREADS &&
            p->reducer == FSR_REDUCER_LINEAR && p->precision != FSR_PREC_FP64;
@@ -540,25 +483,6 @@ bool cta64_eligible(const fsr_params *p) {
 bool cta64d_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 64 && p->block * p->block <= C64_THREADS &&
            p->reducer == FSR_REDUCER_LINEAR;
-}
-
-template <typename IO>
-int launch_cta64d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
-                  cudaStream_t st) {
-    auto k = cta64d_kernel<IO>;
-    const size_t smem = sizeof(C64dSmem);
-    CUDA_TRY(eng, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CUDA_TRY(eng, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, C64_THREADS, smem));
-    if (per_sm < 1) per_sm = 1;
-    const int grid = (int)std::min<int64_t>(std::max<int64_t>(want_blocks, 1), (int64_t)d.sms * per_sm);
-    CUDA_TRY(eng, d.c64scratch.ensure((size_t)grid * 4096 * sizeof(double2)));
-    Pair64Args<IO> b = a;
-    b.scratch = d.c64scratch.as<double2>();
-    k<<<grid, C64_THREADS, smem, st>>>(b);
-    d.launches++;
-    CUDA_TRY(eng, cudaGetLastError());
-    return FSR_OK;
 }
 
 bool warp16d_eligible(const fsr_params *p) {
@@ -590,18 +514,19 @@ double guard_tau_for(const fsr_params *p) {
     return std::min(0.25, 5e-5 * kn * std::pow(it, 1.25));
 }
 
-// Enqueue the whole image path for target-block rows [row0, row1) on device d.
+// Enqueue the image path for target-block rows [row0, row1) on lane d, stream st:
+// the main kernel, then (guarded fp32) the fp64 re-run of the flagged blocks.
 // px/mask/out are "virtual" row-0 pointers (absolute row y at ptr + y*pitch).
-// device_fill: compute the empty-support fill value on the device from rows [0, H).
+// Empty-support blocks are appended to the call's list (call->empty_count,
+// empty_list); the caller fills them once all chunks are done (enqueue_fill or
+// on the host).  ev_main0/1 bracket the main kernel.
 template <typename IO>
 int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, int64_t px_pitch,
                   const uint8_t *mask, int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H,
-                  int64_t W, int64_t row0, int64_t row1, int32_t *sel, int32_t *done,
-                  bool device_fill, double host_fill, cudaStream_t st,
-                  Counters *ctr_in = nullptr, int32_t *empty_in = nullptr,
-                  cudaEvent_t ev_main0 = nullptr, cudaEvent_t ev_main1 = nullptr) {
-    // ev_main0/1 (chunked calls): bracket the main kernel; otherwise d.ev_mid marks its end
-    cudaEvent_t ev_end = ev_main1 ? ev_main1 : d.ev_mid;
+                  int64_t W, int64_t row0, int64_t row1, int32_t *sel, int32_t *done, cudaStream_t st,
+                  ChunkCtr *cc, CallCtr *call, int32_t *empty_list, cudaEvent_t ev_main0,
+                  cudaEvent_t ev_main1) {
+    const cudaEvent_t ev_end = ev_main1;
     const int N = p->block + 2 * p->border;
     const int64_t bcols = (W + p->block - 1) / p->block;
     const int64_t first = row0 * bcols, nblocks = (row1 - row0) * bcols;
@@ -612,30 +537,24 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     fsr_params pl = *p;
     if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
     p = &pl;
-    Counters *ctr = ctr_in;
-    int32_t *empty_list = empty_in;
-    if (!ctr) {  // the device's own scratch (otherwise the caller's per-chunk slot)
-        CUDA_TRY(eng, d.counters.ensure(sizeof(Counters)));
-        CUDA_TRY(eng, d.empty_list.ensure((size_t)nblocks * sizeof(int32_t)));
-        ctr = d.counters.as<Counters>();
-        empty_list = d.empty_list.as<int32_t>();
-    }
-    CUDA_TRY(eng, cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
-    if (ev_main0) CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
+    CUDA_TRY(eng, cudaMemsetAsync(cc, 0, sizeof(ChunkCtr), st));
+    CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
     const int gen_grid = d.sms * 8;
     int rc = FSR_OK;
-    const bool fast32 = std::is_same<IO, float>::value && warp32_eligible(p);
-    const bool fast16 = std::is_same<IO, float>::value && warp16_eligible(p);
-    const bool fast64 = std::is_same<IO, float>::value && cta64_eligible(p);
+    // the fp32-loop kernels take f32 or f64 pixels (the reference's own input
+    // type); their prologue (gather, weights, FFT, split) runs in fp64 either way
+    const bool fast32 = warp32_eligible(p);
+    const bool fast16 = warp16_eligible(p);
+    const bool fast64 = cta64_eligible(p);
     if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16 || fast64)) {
         if (p->precision == FSR_PREC_FP64 && pair64_eligible(p)) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
-                                               &ctr->empty_count, empty_list);
+                                               &call->empty_count, empty_list);
             if ((rc = launch_fp64_n32<IO>(eng, d, a, p, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64 && warp16d_eligible(p)) {
@@ -643,7 +562,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
-                                               &ctr->empty_count, empty_list);
+                                               &call->empty_count, empty_list);
             if ((rc = launch_warp16d<IO>(eng, d, a, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          nblocks, st)))
                 return rc;
@@ -653,7 +572,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, first, nblocks, tab, sel, done,
-                                               &ctr->empty_count, empty_list);
+                                               &call->empty_count, empty_list);
             if ((rc = launch_cta64d<IO>(eng, d, a, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64) {
@@ -662,7 +581,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             ImageArgs<double, IO> a{px, px_pitch, mask, mask_pitch, out, out_pitch, H, W,
                                     p->block, p->border, N, p->iterations, bcols, first, nblocks,
                                     nullptr, nullptr, p->gamma, p->reducer == FSR_REDUCER_TREE,
-                                    p->early_stop, tab, sel, done, &ctr->empty_count,
+                                    p->early_stop, tab, sel, done, &call->empty_count,
                                     empty_list};
             if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(ev_end, st));
@@ -678,7 +597,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                        p->block, p->border, N, p->iterations, bcols, first,
                                        nblocks, nullptr, nullptr, (float)p->gamma,
                                        p->reducer == FSR_REDUCER_TREE, p->early_stop, tf, sel,
-                                       done, &ctr->empty_count, empty_list};
+                                       done, &call->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
                 CUDA_TRY(eng, cudaEventRecord(ev_end, st));
             } else {
@@ -686,7 +605,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                         p->block, p->border, N, p->iterations, bcols, first,
                                         nblocks, nullptr, nullptr, p->gamma,
                                         p->reducer == FSR_REDUCER_TREE, p->early_stop, tab, sel,
-                                        done, &ctr->empty_count, empty_list};
+                                        done, &call->empty_count, empty_list};
                 if ((rc = launch_generic(eng, d, a, (int)std::min<int64_t>(nblocks, gen_grid), st))) return rc;
                 CUDA_TRY(eng, cudaEventRecord(ev_end, st));
             }
@@ -698,11 +617,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         if ((rc = get_tables<double>(eng, d, N, p->rho, td))) return rc;
         Warp32Args a{};
         a.decay64 = td.decay;
-        a.px = (const float *)px;
+        a.px = px;
         a.px_pitch = px_pitch;
         a.mask = mask;
         a.mask_pitch = mask_pitch;
-        a.out = (float *)out;
+        a.out = out;
         a.out_pitch = out_pitch;
         a.H = H;
         a.W = W;
@@ -719,9 +638,9 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.wf = tf.wf;
         a.sel = sel;
         a.done = done;
-        a.empty_count = &ctr->empty_count;
+        a.empty_count = &call->empty_count;
         a.empty_list = empty_list;
-        a.rerun_count = &ctr->rerun_count;
+        a.rerun_count = &cc->rerun_count;
         a.rerun_list = guarded ? d.rerun_list.as<int32_t>() : nullptr;
         a.gap_out = d.gap_debug ? d.gap_debug - 2 * first : nullptr;
         a.key_mask = 0xffffffe0u;
@@ -735,28 +654,26 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         const int64_t ty0 = std::max<int64_t>(0, row0 * p->block - p->border);
         const int64_t ty1 = std::min<int64_t>(H, row1 * p->block + p->border);
         a.tma_y0 = (int)ty0;
-        const float *tpx = a.px + ty0 * px_pitch;
+        const IO *tpx = px + ty0 * px_pitch;
         const uint8_t *tmk = mask + ty0 * mask_pitch;
+        const bool tree = p->reducer == FSR_REDUCER_TREE;
+        // trace / early-stop code only in the launches that need it
+        const int opts = (sel ? LOPT_TRACE : 0) | (p->early_stop ? LOPT_EARLY : 0);
+        const int nsup = fast64 ? 64 : fast16 ? 16 : 32;
+        a.use_tma = (d.tma_enabled &&
+                     window_maps<IO>(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps, nsup)) ? 1 : 0;
+        d.used_tma = a.use_tma;
         if (fast64) {
             a.key_mask = 0xffffffc0u;  // 6 rank bits (row u of 64)
-            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps,
-                                                      C64_BOX_PX, C64_BOX_MK, 64)) ? 1 : 0;
-            d.used_tma = a.use_tma;
-            rc = guarded ? launch_cta64_t<true>(eng, d, a, maps, st) : launch_cta64_t<false>(eng, d, a, maps, st);
-            if (rc) return rc;
+            LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, d.sms, st)));
         } else if (fast16) {
-            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps,
-                                                      W16_BOX_PX, W16_BOX_MK, 16)) ? 1 : 0;
-            d.used_tma = a.use_tma;
-            if ((rc = launch_warp16(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
-                                    guarded, st)))
-                return rc;
+            LAUNCH_TRY(eng, d, (warp16_any<IO>(a, maps, tree, p->argmax_impl, guarded, opts, d.sms, st)));
         } else {
-            a.use_tma = (d.tma_enabled && warp32_maps(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps)) ? 1 : 0;
-            d.used_tma = a.use_tma;
-            if ((rc = launch_warp32(eng, d, a, maps, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
-                                    guarded || d.gap_debug != nullptr, st)))
-                return rc;
+            const bool study = d.gap_debug != nullptr;
+            if (study && p->argmax_impl != FSR_ARGMAX_REDUX)
+                return fail(eng, FSR_EINVAL, "guard study needs argmax=redux");
+            LAUNCH_TRY(eng, d, (warp32_any<IO>(a, maps, tree, p->argmax_impl, guarded || study, study,
+                                               opts, d.sms, st)));
         }
         CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         if (guarded && fast64) {
@@ -765,9 +682,9 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, 0, 0, tab, sel, done,
-                                               &ctr->ticket /* empties already counted */, nullptr);
+                                               &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
-            r.list_count = &ctr->rerun_count;
+            r.list_count = &cc->rerun_count;
             if ((rc = launch_cta64d<IO>(eng, d, r, (int64_t)d.sms, st))) return rc;
         } else if (guarded && fast16) {
             // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)
@@ -775,9 +692,9 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, 0, 0, tab, sel, done,
-                                               &ctr->ticket /* empties already counted */, nullptr);
+                                               &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
-            r.list_count = &ctr->rerun_count;
+            r.list_count = &cc->rerun_count;
             if ((rc = launch_warp16d<IO>(eng, d, r, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          (int64_t)d.sms * 16, st)))
                 return rc;
@@ -787,30 +704,42 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
             Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
                                                W, bcols, 0, 0, tab, sel, done,
-                                               &ctr->ticket /* empties already counted */, nullptr);
+                                               &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
-            r.list_count = &ctr->rerun_count;
+            r.list_count = &cc->rerun_count;
             if ((rc = launch_fp64_n32<IO>(eng, d, r, p, (int64_t)d.sms * 16, st))) return rc;
         }
     }
-    if (device_fill) {
-        mean_known_kernel<IO><<<d.sms * 4, 256, 0, st>>>(px, px_pitch, mask, mask_pitch, H, W,
-                                                         &ctr->empty_count, ctr->acc, &ctr->ticket,
-                                                         &ctr->fill, &ctr->status);
-        d.launches++;
+    return FSR_OK;
+}
+
+// Empty-support fallback for a whole call (reconstruction.py:236-237, 272-275),
+// enqueued after every chunk: the listed blocks get `fill`, or (fill = NaN) the
+// mean of the known samples of rows [0, H) of px/mask, summed on the device in
+// a fixed order (deterministic).  Both kernels return at once when no block was
+// empty; an empty block without any known sample sets call->status = 2.
+template <typename IO>
+int enqueue_fill(fsr_engine *eng, Device &d, const IO *px, int64_t px_pitch, const uint8_t *mask,
+                 int64_t mask_pitch, IO *out, int64_t out_pitch, int64_t H, int64_t W, int B,
+                 CallCtr *call, const int32_t *list, double fill, cudaStream_t st) {
+    const int64_t bcols = (W + B - 1) / B;
+    const double2 *parts = nullptr;
+    int nparts = 0;
+    if (fill != fill) {
+        nparts = d.sms * 2;
+        CUDA_TRY(eng, d.fill_partials.ensure((size_t)nparts * sizeof(double2)));
+        mean_partial_kernel<IO><<<nparts, 256, 0, st>>>(px, px_pitch, mask, mask_pitch, H, W,
+                                                         &call->empty_count,
+                                                         d.fill_partials.as<double2>());
         CUDA_TRY(eng, cudaGetLastError());
-        fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
-                                                      empty_list,
-                                                      &ctr->empty_count, &ctr->fill, 0.0);
         d.launches++;
-        CUDA_TRY(eng, cudaGetLastError());
-    } else if (host_fill == host_fill) {  // not NaN: fill value known on the host
-        fill_blocks_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, p->block, bcols,
-                                                      empty_list,
-                                                      &ctr->empty_count, nullptr, host_fill);
-        d.launches++;
-        CUDA_TRY(eng, cudaGetLastError());
+        parts = d.fill_partials.as<double2>();
     }
+    fill_empty_kernel<IO><<<d.sms, 128, 0, st>>>(out, out_pitch, H, W, B, bcols, list,
+                                                 &call->empty_count, parts, nparts, fill,
+                                                 &call->status);
+    CUDA_TRY(eng, cudaGetLastError());
+    d.launches++;
     return FSR_OK;
 }
 
@@ -819,9 +748,11 @@ int select_device(fsr_engine *eng, Device &d) {
     return FSR_OK;
 }
 
-// Large calls run in K row chunks alternating over kLanes lanes (same GPU, own
+// Calls run in K row chunks alternating over kLanes lanes (same GPU, own
 // stream, staging and scratch): one chunk's copies, fp64 re-run and launch tail
-// overlap the next chunk's main kernel.
+// overlap the other chunks' main kernels.  K = block_rows / 40, at least 3 for
+// any call of 24 block rows or more (so a 4K strip at 8 GPUs, 67 rows, still
+// overlaps its re-run) and at most 12.
 int chunk_count(const Device &d, int64_t block_rows) {
 #ifndef FSR_CHUNK_ROWS
 #define FSR_CHUNK_ROWS 40  // block rows per chunk (at least); 1080p: 40 rows is +0.5-1 % over 64
@@ -829,15 +760,22 @@ int chunk_count(const Device &d, int64_t block_rows) {
 #ifndef FSR_MAX_CHUNKS
 #define FSR_MAX_CHUNKS 12  // 4K (540 block rows): 12 chunks (e2e: 4 -> 8 +0.4 %, 8 -> 12 +0.2 %)
 #endif
-    return (d.gap_debug || !d.chunking)
-               ? 1
-               : (int)std::min<int64_t>(FSR_MAX_CHUNKS, std::max<int64_t>(1, block_rows / FSR_CHUNK_ROWS));
+#ifndef FSR_MIN_CHUNKS
+#define FSR_MIN_CHUNKS 3
+#endif
+    if (d.gap_debug || !d.chunking || block_rows < 8 * FSR_MIN_CHUNKS) return 1;
+    return (int)std::min<int64_t>(FSR_MAX_CHUNKS,
+                                  std::max<int64_t>(FSR_MIN_CHUNKS, block_rows / FSR_CHUNK_ROWS));
 }
 
 #ifndef FSR_LANES
 #define FSR_LANES 8  // one stream per chunk at 4K (2 lanes: e2e 37.6, 4: 38.2, 8: 38.4 fps; device 38.8)
 #endif
 constexpr int kLanes = FSR_LANES;  // streams a chunked call alternates over
+
+#ifndef FSR_STAGE_THREADS
+#define FSR_STAGE_THREADS 4  // host threads per device for the staging copies (incl. the caller)
+#endif
 
 int ensure_lanes(fsr_engine *eng, Device &d) {
     while ((int)d.lanes.size() < kLanes) {
@@ -848,7 +786,6 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
         CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
         CUDA_TRY(eng, cudaEventCreateWithFlags(&ln->ev0, cudaEventDisableTiming));
         CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
-        CUDA_TRY(eng, cudaEventCreate(&ln->ev_mid));
         d.lanes.push_back(std::move(ln));
     }
     for (int c = 0; c < 16; ++c)
@@ -859,175 +796,301 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
     return FSR_OK;
 }
 
-// Host-buffer whole-image call: split block rows over devices, H2D strip+halo,
-// enqueue, D2H target rows.  The empty-support fill value is computed on the
-// host (from the caller's full image) only if some block had an empty window.
+// Chunk c of K over block rows [row0, row1)
+inline void chunk_rows(int64_t row0, int64_t row1, int c, int K, int64_t &r0, int64_t &r1) {
+    r0 = row0 + (row1 - row0) * c / K;
+    r1 = row0 + (row1 - row0) * (c + 1) / K;
+}
+
+// Per-call scratch of device d: the call counter, K chunk counters and the empty
+// list (capacity nb blocks), zeroed on d.stream after the engine's previous call.
+int begin_call(fsr_engine *eng, Device &d, int K, int64_t nb, cudaStream_t st) {
+    CUDA_TRY(eng, d.call_ctr.ensure(sizeof(CallCtr)));
+    CUDA_TRY(eng, d.chunk_ctrs.ensure((size_t)std::max(K, 1) * sizeof(ChunkCtr)));
+    CUDA_TRY(eng, d.empty_list.ensure((size_t)std::max<int64_t>(nb, 1) * sizeof(int32_t)));
+    // calls on one engine are serialised: the scratch above is reused by the next call
+    CUDA_TRY(eng, cudaStreamWaitEvent(st, d.ev_done, 0));
+    CUDA_TRY(eng, cudaMemsetAsync(d.call_ctr.p, 0, sizeof(CallCtr), st));
+    CUDA_TRY(eng, cudaEventRecord(d.ev0, st));
+    d.launches = 0;
+    d.last_chunks = K;
+    return FSR_OK;
+}
+
+// Kernel-side statistics of the last call on device d (waits for it).
+int read_call_stats(fsr_engine *eng, Device &d, CallCtr &call, int64_t &reruns, float &ms, float &main_ms) {
+    CUDA_TRY(eng, cudaEventSynchronize(d.ev1));
+    ms = 0.f;
+    main_ms = 0.f;
+    if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+    for (int c = 0; c < d.last_chunks; ++c) {  // the chunks' main-kernel brackets
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) main_ms += t;
+    }
+    (void)cudaGetLastError();
+    CUDA_TRY(eng, cudaMemcpy(&call, d.call_ctr.p, sizeof(CallCtr), cudaMemcpyDeviceToHost));
+    std::vector<ChunkCtr> cc(std::max(d.last_chunks, 1));
+    CUDA_TRY(eng, cudaMemcpy(cc.data(), d.chunk_ctrs.p, cc.size() * sizeof(ChunkCtr),
+                             cudaMemcpyDeviceToHost));
+    reruns = 0;
+    for (const ChunkCtr &c : cc) reruns += c.rerun_count;
+    return FSR_OK;
+}
+
+// Device-resident call on device d, asynchronous on st: K chunks forked onto the
+// lanes from st and joined back into it, then the empty-support fill.
+template <typename IO>
+int device_call(fsr_engine *eng, Device &d, const fsr_params *p, const IO *d_px, int64_t px_pitch,
+                const uint8_t *d_mask, int64_t mask_pitch, int64_t H, int64_t W, int64_t row0,
+                int64_t row1, IO *d_out, int64_t out_pitch, double fill, cudaStream_t st) {
+    const int64_t bcols = (W + p->block - 1) / p->block;
+    const int K = chunk_count(d, row1 - row0);
+    int rc = ensure_lanes(eng, d);
+    if (rc) return rc;
+    if ((rc = begin_call(eng, d, K, (row1 - row0) * bcols, st))) return rc;
+    CallCtr *call = d.call_ctr.as<CallCtr>();
+    const int nl = std::min(K, kLanes);
+    for (int l = 0; l < nl; ++l) {
+        d.lanes[l]->launches = 0;
+        d.lanes[l]->gap_debug = d.gap_debug;
+        CUDA_TRY(eng, cudaStreamWaitEvent(d.lanes[l]->stream, d.ev0, 0));
+    }
+    for (int c = 0; c < K; ++c) {
+        Device &ld = *d.lanes[c % kLanes];
+        int64_t r0, r1;
+        chunk_rows(row0, row1, c, K, r0, r1);
+        rc = enqueue_image<IO>(eng, ld, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch, H, W,
+                               r0, r1, nullptr, nullptr, ld.stream, d.chunk_ctrs.as<ChunkCtr>() + c,
+                               call, d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
+        if (rc) return rc;
+        d.used_tma = ld.used_tma;
+    }
+    for (int l = 0; l < nl; ++l) {
+        Device &ld = *d.lanes[l];
+        d.launches += ld.launches;
+        CUDA_TRY(eng, cudaEventRecord(ld.ev1, ld.stream));
+        CUDA_TRY(eng, cudaStreamWaitEvent(st, ld.ev1, 0));
+    }
+    if ((rc = enqueue_fill<IO>(eng, d, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch, H, W,
+                               p->block, call, d.empty_list.as<int32_t>(), fill, st)))
+        return rc;
+    CUDA_TRY(eng, cudaEventRecord(d.ev1, st));
+    CUDA_TRY(eng, cudaEventRecord(d.ev_done, st));
+    return FSR_OK;
+}
+
+// Result of one device's share of a host-buffer call.
+struct HostPart {
+    int64_t row0 = 0, row1 = 0;
+    int rc = FSR_OK;
+    CallCtr call{};
+    int64_t reruns = 0;
+    float ms = 0.f, main_ms = 0.f;
+    std::vector<int32_t> empty;  // empty-support block ids (host fill)
+};
+
+// One device's strip of a host-buffer call, run by its own host thread when the
+// engine has several devices.  Chunk c goes to lane c % kLanes: its pixel and
+// mask rows (strip + halo) are copied by the staging pool into the lane's pinned
+// buffer, sent H2D, reconstructed, and its output rows come back D2H into pinned
+// staging, copied to the caller's buffer once the lane is reused or the call
+// drains -- so the caller's pageable buffers never block the pipeline.
+template <typename IO>
+int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, const uint8_t *mask,
+               int64_t H, int64_t W, IO *out, int32_t *sel, int32_t *done, HostPart &hp) {
+    const int B = p->block, L = p->border;
+    const int64_t bcols = (W + B - 1) / B, rows = hp.row1 - hp.row0;
+    const int64_t it_stride = std::max(p->iterations, 1);
+    int rc = select_device(eng, d);
+    if (rc) return rc;
+    if (!d.pool) d.pool = std::make_unique<Pool>(FSR_STAGE_THREADS - 1);
+    const int K = chunk_count(d, rows);
+    if ((rc = ensure_lanes(eng, d))) return rc;
+    if ((rc = begin_call(eng, d, K, rows * bcols, d.stream))) return rc;
+    CallCtr *call = d.call_ctr.as<CallCtr>();
+    const int nl = std::min(K, kLanes);
+    for (int l = 0; l < nl; ++l) {
+        Device &ld = *d.lanes[l];
+        ld.launches = 0;
+        ld.pending = false;
+        ld.gap_debug = d.gap_debug;
+        CUDA_TRY(eng, cudaStreamWaitEvent(ld.stream, d.ev0, 0));
+    }
+    auto drain = [&](Device &ld) -> int {  // the lane's finished chunk -> caller's buffer
+        if (!ld.pending) return FSR_OK;
+        CUDA_TRY(eng, cudaEventSynchronize(ld.ev1));
+        pool_copy(d.pool.get(), out + ld.pend_oa * W, ld.hout.p, ld.pend_ob - ld.pend_oa,
+                  (size_t)W * sizeof(IO));
+        ld.pending = false;
+        return FSR_OK;
+    };
+    for (int c = 0; c < K; ++c) {
+        Device &ld = *d.lanes[c % kLanes];
+        if ((rc = drain(ld))) return rc;
+        int64_t r0, r1;
+        chunk_rows(hp.row0, hp.row1, c, K, r0, r1);
+        const int64_t ya = std::max<int64_t>(0, r0 * B - L), yb = std::min<int64_t>(H, r1 * B + L);
+        const int64_t oa = std::min<int64_t>(H, r0 * B), ob = std::min<int64_t>(H, r1 * B);
+        const int64_t rows_in = yb - ya, rows_out = ob - oa, nb = (r1 - r0) * bcols;
+        const size_t px_bytes = (size_t)rows_in * W * sizeof(IO), mk_bytes = (size_t)rows_in * W;
+        CUDA_TRY(eng, ld.px.ensure(px_bytes));
+        CUDA_TRY(eng, ld.mask.ensure(mk_bytes));
+        CUDA_TRY(eng, ld.out.ensure((size_t)rows_out * W * sizeof(IO)));
+        CUDA_TRY(eng, ld.hin.ensure(px_bytes + mk_bytes));
+        CUDA_TRY(eng, ld.hout.ensure((size_t)rows_out * W * sizeof(IO)));
+        if (sel) CUDA_TRY(eng, ld.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
+        if (done) CUDA_TRY(eng, ld.done.ensure((size_t)nb * sizeof(int32_t)));
+        pool_copy(d.pool.get(), ld.hin.p, px + ya * W, rows_in, (size_t)W * sizeof(IO));
+        pool_copy(d.pool.get(), ld.hin.as<char>() + px_bytes, mask + ya * W, rows_in, (size_t)W);
+        CUDA_TRY(eng, cudaMemcpyAsync(ld.px.p, ld.hin.p, px_bytes, cudaMemcpyHostToDevice, ld.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(ld.mask.p, ld.hin.as<char>() + px_bytes, mk_bytes,
+                                      cudaMemcpyHostToDevice, ld.stream));
+        const IO *vpx = ld.px.as<IO>() - ya * W;
+        const uint8_t *vmask = ld.mask.as<uint8_t>() - ya * W;
+        IO *vout = ld.out.as<IO>() - oa * W;
+        int32_t *vsel = sel ? ld.sel.as<int32_t>() - r0 * bcols * it_stride : nullptr;
+        int32_t *vdone = done ? ld.done.as<int32_t>() - r0 * bcols : nullptr;
+        rc = enqueue_image<IO>(eng, ld, p, vpx, W, vmask, W, vout, W, H, W, r0, r1, vsel, vdone,
+                               ld.stream, d.chunk_ctrs.as<ChunkCtr>() + c, call,
+                               d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
+        if (rc) return rc;
+        CUDA_TRY(eng, cudaMemcpyAsync(ld.hout.p, ld.out.p, (size_t)rows_out * W * sizeof(IO),
+                                      cudaMemcpyDeviceToHost, ld.stream));
+        // traces (validation only) go straight to the caller's buffers
+        if (sel)
+            CUDA_TRY(eng, cudaMemcpyAsync(sel + r0 * bcols * it_stride, ld.sel.p,
+                                          (size_t)nb * it_stride * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, ld.stream));
+        if (done)
+            CUDA_TRY(eng, cudaMemcpyAsync(done + r0 * bcols, ld.done.p, (size_t)nb * sizeof(int32_t),
+                                          cudaMemcpyDeviceToHost, ld.stream));
+        CUDA_TRY(eng, cudaEventRecord(ld.ev1, ld.stream));
+        ld.pending = true;
+        ld.pend_oa = oa;
+        ld.pend_ob = ob;
+        d.used_tma = ld.used_tma;
+    }
+    for (int l = 0; l < nl; ++l) {
+        Device &ld = *d.lanes[l];
+        if ((rc = drain(ld))) return rc;
+        d.launches += ld.launches;
+        CUDA_TRY(eng, cudaStreamWaitEvent(d.stream, ld.ev1, 0));
+    }
+    CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
+    CUDA_TRY(eng, cudaEventRecord(d.ev_done, d.stream));
+    if ((rc = read_call_stats(eng, d, hp.call, hp.reruns, hp.ms, hp.main_ms))) return rc;
+    if (hp.call.empty_count > 0) {
+        hp.empty.resize(hp.call.empty_count);
+        CUDA_TRY(eng, cudaMemcpy(hp.empty.data(), d.empty_list.p, hp.empty.size() * sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost));
+    }
+    return FSR_OK;
+}
+
+// Host-buffer whole-image call: block rows [rbeg, rend) split into contiguous
+// strips over the engine's first max_devs devices, each run by host_strip
+// (concurrently, one host thread per device).  Empty-support blocks get
+// `fill`, or (fill = NaN) the mean of the known samples of the caller's full
+// image (reconstruction.py:236-237; "no known samples" if there is none).
 template <typename IO>
 int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const uint8_t *mask,
                      int64_t H, int64_t W, IO *out, int32_t *sel, int32_t *done,
-                     int64_t rbeg = 0, int64_t rend = -1) {
+                     int64_t rbeg = 0, int64_t rend = -1, double fill = NAN, int max_devs = 0) {
     if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
     std::lock_guard<std::mutex> lock(eng->mu);
     int rc = check_params(eng, p);
     if (rc) return rc;
     if (H < 1 || W < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
     if (!px || !mask || !out) return fail(eng, FSR_EINVAL, "null image buffer");
-    const int B = p->block, L = p->border;
+    const int B = p->block;
     const int64_t brows_all = (H + B - 1) / B, bcols = (W + B - 1) / B;
     if (rend < 0) rend = brows_all;
     if (rbeg < 0 || rend > brows_all || rbeg > rend)
         return fail(eng, FSR_EINVAL, "block-row range out of bounds");
     const int64_t brows = rend - rbeg;
-    const int nd = (int)eng->devs.size();
-    const int64_t it_stride = std::max(p->iterations, 1);
+    const int nd = max_devs > 0 ? std::min<int>(max_devs, (int)eng->devs.size()) : (int)eng->devs.size();
     eng->stats = fsr_stats{};
     eng->device_stats_pending = false;
     eng->stats.blocks = brows * bcols;
-    struct Part { int64_t row0, row1, ya, yb, oa, ob; };
-    std::vector<Part> parts(nd);
+    std::vector<HostPart> parts(nd);
     for (int g = 0; g < nd; ++g) {
-        Part &q = parts[g];
-        q.row0 = rbeg + brows * g / nd;
-        q.row1 = rbeg + brows * (g + 1) / nd;
-        q.ya = std::max<int64_t>(0, q.row0 * B - L);          // halo above
-        q.yb = std::min<int64_t>(H, q.row1 * B + L);          // halo below
-        q.oa = std::min<int64_t>(H, q.row0 * B);
-        q.ob = std::min<int64_t>(H, q.row1 * B);
+        parts[g].row0 = rbeg + brows * g / nd;
+        parts[g].row1 = rbeg + brows * (g + 1) / nd;
     }
-    // per device: the strip's block rows in K chunks (K = 1 for small strips), chunk c
-    // on lane c % kLanes -- copies of one chunk overlap the kernels of the others
-    std::vector<int> nchunks(nd, 0);
-    for (int g = 0; g < nd; ++g) {
-        Device &d = *eng->devs[g];
-        const Part &q = parts[g];
-        if (q.row1 <= q.row0) continue;
-        if ((rc = select_device(eng, d))) return rc;
-        const int64_t prow = q.row1 - q.row0;
-        const int K = chunk_count(d, prow);
-        nchunks[g] = K;
-        if (K > 1 && (rc = ensure_lanes(eng, d))) return rc;
-        d.launches = 0;
-        const int64_t nb_part = prow * bcols;
-        CUDA_TRY(eng, d.counters.ensure((size_t)K * sizeof(Counters)));
-        CUDA_TRY(eng, d.empty_list.ensure((size_t)nb_part * sizeof(int32_t)));
-        // the first lane's stream starts the clock for the whole strip
-        cudaStream_t st0 = K > 1 ? d.lanes[0]->stream : d.stream;
-        CUDA_TRY(eng, cudaEventRecord(d.ev0, st0));
-        for (int c = 0; c < K; ++c) {
-            Device &ld = K > 1 ? *d.lanes[c % kLanes] : d;
-            if (K > 1) ld.launches = c < kLanes ? 0 : ld.launches;
-            const int64_t r0 = q.row0 + prow * c / K, r1 = q.row0 + prow * (c + 1) / K;
-            const int64_t ya = std::max<int64_t>(0, r0 * B - L), yb = std::min<int64_t>(H, r1 * B + L);
-            const int64_t oa = std::min<int64_t>(H, r0 * B), ob = std::min<int64_t>(H, r1 * B);
-            const int64_t rows_in = yb - ya, rows_out = ob - oa, nb = (r1 - r0) * bcols;
-            CUDA_TRY(eng, ld.px.ensure((size_t)rows_in * W * sizeof(IO)));
-            CUDA_TRY(eng, ld.mask.ensure((size_t)rows_in * W));
-            CUDA_TRY(eng, ld.out.ensure((size_t)rows_out * W * sizeof(IO)));
-            if (sel) CUDA_TRY(eng, ld.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
-            if (done) CUDA_TRY(eng, ld.done.ensure((size_t)nb * sizeof(int32_t)));
-            CUDA_TRY(eng, cudaMemcpyAsync(ld.px.p, px + ya * W, (size_t)rows_in * W * sizeof(IO),
-                                          cudaMemcpyHostToDevice, ld.stream));
-            CUDA_TRY(eng, cudaMemcpyAsync(ld.mask.p, mask + ya * W, (size_t)rows_in * W,
-                                          cudaMemcpyHostToDevice, ld.stream));
-            if (K > 1) CUDA_TRY(eng, cudaEventRecord(ld.ev0, ld.stream));
-            const IO *vpx = ld.px.as<IO>() - ya * W;
-            const uint8_t *vmask = ld.mask.as<uint8_t>() - ya * W;
-            IO *vout = ld.out.as<IO>() - oa * W;
-            int32_t *vsel = sel ? ld.sel.as<int32_t>() - r0 * bcols * it_stride : nullptr;
-            int32_t *vdone = done ? ld.done.as<int32_t>() - r0 * bcols : nullptr;
-            rc = enqueue_image<IO>(eng, ld, p, vpx, W, vmask, W, vout, W, H, W, r0, r1, vsel, vdone,
-                                   false, NAN, ld.stream, d.counters.as<Counters>() + c,
-                                   d.empty_list.as<int32_t>() + (r0 - q.row0) * bcols,
-                                   K > 1 ? d.ck0[c] : nullptr, K > 1 ? d.ck1[c] : nullptr);
-            if (rc) return rc;
-            if (K == 1) CUDA_TRY(eng, cudaEventRecord(d.ev1, d.stream));
-            CUDA_TRY(eng, cudaMemcpyAsync(out + oa * W, ld.out.p, (size_t)rows_out * W * sizeof(IO),
-                                          cudaMemcpyDeviceToHost, ld.stream));
-            if (sel)
-                CUDA_TRY(eng, cudaMemcpyAsync(sel + r0 * bcols * it_stride, ld.sel.p,
-                                              (size_t)nb * it_stride * sizeof(int32_t),
-                                              cudaMemcpyDeviceToHost, ld.stream));
-            if (done)
-                CUDA_TRY(eng, cudaMemcpyAsync(done + r0 * bcols, ld.done.p, (size_t)nb * sizeof(int32_t),
-                                              cudaMemcpyDeviceToHost, ld.stream));
-            if (K > 1) CUDA_TRY(eng, cudaEventRecord(ld.ev1, ld.stream));
-            if (K > 1 && c + kLanes >= K) d.launches += ld.launches;  // the lane's last chunk
-            d.used_tma = ld.used_tma;
-        }
+    auto run = [&](int g) {
+        if (parts[g].row1 > parts[g].row0)
+            parts[g].rc = host_strip<IO>(eng, *eng->devs[g], p, px, mask, H, W, out, sel, done, parts[g]);
+    };
+    int busy = 0;
+    for (int g = 0; g < nd; ++g) busy += parts[g].row1 > parts[g].row0;
+    if (busy <= 1) {
+        for (int g = 0; g < nd; ++g) run(g);
+    } else {
+        std::vector<std::thread> th;
+        for (int g = 0; g < nd; ++g) th.emplace_back(run, g);
+        for (auto &t : th) t.join();
     }
-    unsigned empty_total = 0;
-    std::vector<std::vector<Counters>> ctrs(nd);
+    for (int g = 0; g < nd; ++g)
+        if (parts[g].rc) return parts[g].rc;  // eng->err holds the message
+    int64_t empty_total = 0;
     for (int g = 0; g < nd; ++g) {
-        Device &d = *eng->devs[g];
-        const int K = nchunks[g];
-        if (K == 0) continue;
-        if ((rc = select_device(eng, d))) return rc;
-        float ms = 0.f, mm = 0.f;
-        if (K > 1) {
-            for (auto &ln : d.lanes) {
-                CUDA_TRY(eng, cudaStreamSynchronize(ln->stream));
-                float t = 0.f;
-                if (cudaEventElapsedTime(&t, d.ev0, ln->ev1) == cudaSuccess) ms = std::max(ms, t);
-            }
-            for (int c = 0; c < K; ++c) {  // the chunks' main-kernel brackets
-                float t = 0.f;
-                if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) mm += t;
-            }
-        } else {
-            CUDA_TRY(eng, cudaStreamSynchronize(d.stream));
-            if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
-            if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) mm = 0.f;
-        }
-        (void)cudaGetLastError();
-        ctrs[g].resize(K);
-        CUDA_TRY(eng, cudaMemcpy(ctrs[g].data(), d.counters.p, (size_t)K * sizeof(Counters),
-                                 cudaMemcpyDeviceToHost));
-        for (const Counters &c : ctrs[g]) {
-            empty_total += c.empty_count;
-            eng->stats.rerun_blocks += c.rerun_count;
-        }
-        eng->stats.kernel_launches += d.launches;
+        const HostPart &hp = parts[g];
+        empty_total += hp.call.empty_count;
+        eng->stats.rerun_blocks += hp.reruns;
+        eng->stats.kernel_launches += eng->devs[g]->launches;
         if (g == 0) {
-            eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
-            eng->stats.kernel_ms = ms;
-            eng->stats.main_ms = mm;
+            eng->stats.flags = eng->devs[0]->used_tma ? FSR_STATS_TMA_GATHER : 0;
+            eng->stats.kernel_ms = hp.ms;
+            eng->stats.main_ms = hp.main_ms;
         }
     }
     eng->stats.empty_blocks = empty_total;
     if (empty_total > 0) {
         // reconstruction.py:236-237, 272-275
-        double s = 0.0;
-        int64_t known = 0;
-        for (int64_t i = 0; i < H * W; ++i)
-            if (mask[i]) {
-                s += (double)px[i];
-                ++known;
-            }
-        if (known == 0) return fail(eng, FSR_ENOSAMPLES, "no known samples");
-        const double fill = s / (double)known;
-        const int64_t bc = bcols;
-        for (int g = 0; g < nd; ++g) {
-            Device &d = *eng->devs[g];
-            const Part &q = parts[g];
-            const int K = nchunks[g];
-            if ((rc = select_device(eng, d))) return rc;
-            for (int c = 0; c < K; ++c) {
-                if (ctrs[g][c].empty_count == 0) continue;
-                // host-side fill of the listed blocks (rare path); chunk c's list
-                // sits at its first block's offset in the strip's empty list
-                const int64_t prow = q.row1 - q.row0, r0c = q.row0 + prow * c / K;
-                std::vector<int32_t> list(ctrs[g][c].empty_count);
-                CUDA_TRY(eng, cudaMemcpy(list.data(), d.empty_list.as<int32_t>() + (r0c - q.row0) * bc,
-                                         list.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
-                for (int32_t bid : list) {
-                    int64_t r0 = (bid / bc) * B, c0 = (bid % bc) * B;
-                    for (int64_t y = r0; y < std::min<int64_t>(H, r0 + B); ++y)
-                        for (int64_t x = c0; x < std::min<int64_t>(W, c0 + B); ++x) out[y * W + x] = (IO)fill;
+        if (fill != fill) {
+            double s = 0.0;
+            int64_t known = 0;
+            for (int64_t i = 0; i < H * W; ++i)
+                if (mask[i]) {
+                    s += (double)px[i];
+                    ++known;
                 }
-            }
+            if (known == 0) return fail(eng, FSR_ENOSAMPLES, "no known samples");
+            fill = s / (double)known;
         }
+        for (const HostPart &hp : parts)
+            for (int32_t bid : hp.empty) {
+                const int64_t r0 = (bid / bcols) * B, c0 = (bid % bcols) * B;
+                for (int64_t y = r0; y < std::min<int64_t>(H, r0 + B); ++y)
+                    for (int64_t x = c0; x < std::min<int64_t>(W, c0 + B); ++x) out[y * W + x] = (IO)fill;
+            }
     }
     return FSR_OK;
+}
+
+template <typename IO>
+int reconstruct_device(fsr_engine *eng, const fsr_params *p, const IO *d_px, int64_t px_pitch,
+                       const uint8_t *d_mask, int64_t mask_pitch, int64_t height, int64_t width,
+                       int64_t row0, int64_t row1, IO *d_out, int64_t out_pitch, double fill,
+                       void *stream) {
+    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
+    std::lock_guard<std::mutex> lock(eng->mu);
+    int rc = check_params(eng, p);
+    if (rc) return rc;
+    if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
+    if (!d_px || !d_mask || !d_out) return fail(eng, FSR_EINVAL, "null image buffer");
+    const int64_t brows = (height + p->block - 1) / p->block;
+    if (row0 < 0 || row1 > brows || row0 > row1) return fail(eng, FSR_EINVAL, "block-row range out of bounds");
+    Device &d = *eng->devs[0];
+    if ((rc = select_device(eng, d))) return rc;
+    rc = device_call<IO>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, height, width, row0, row1,
+                         d_out, out_pitch, fill, (cudaStream_t)stream);
+    eng->stats = fsr_stats{};
+    eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
+    eng->stats.kernel_launches = d.launches;
+    eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
+    eng->device_stats_pending = rc == FSR_OK;
+    return rc;
 }
 
 }  // namespace
@@ -1101,7 +1164,8 @@ int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **ou
         CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));
-        CUDA_TRY(nullptr, cudaEventCreate(&d->ev_mid));
+        CUDA_TRY(nullptr, cudaEventCreateWithFlags(&d->ev_done, cudaEventDisableTiming));
+        CUDA_TRY(nullptr, cudaEventRecord(d->ev_done, d->stream));
         eng->devs.push_back(std::move(d));
     }
     *out = eng.release();
@@ -1114,26 +1178,29 @@ void fsr_engine_destroy(fsr_engine *eng) {
         Device &d = *dp;
         cudaSetDevice(d.id);
         cudaStreamSynchronize(d.stream);
-        for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list,
-                          &d.counters, &d.R, &d.G, &d.W, &d.wf, &d.thr, &d.obj, &d.ties, &d.c64scratch})
-            b->release();
-        for (auto &kv : d.tables) {
-            kv.second->f64.release();
-            kv.second->f32.release();
-        }
+        d.pool.reset();
         for (auto &ln : d.lanes) {
             cudaStreamSynchronize(ln->stream);
-            for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->empty_list,
-                              &ln->rerun_list, &ln->counters, &ln->c64scratch, &ln->partials})
+            for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->rerun_list,
+                              &ln->c64scratch})
                 b->release();
+            ln->hin.release();
+            ln->hout.release();
             for (auto &kv : ln->tables) {
                 kv.second->f64.release();
                 kv.second->f32.release();
             }
             cudaEventDestroy(ln->ev0);
             cudaEventDestroy(ln->ev1);
-            cudaEventDestroy(ln->ev_mid);
             cudaStreamDestroy(ln->stream);
+        }
+        for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list,
+                          &d.call_ctr, &d.chunk_ctrs, &d.fill_partials, &d.R, &d.G, &d.W, &d.wf,
+                          &d.thr, &d.obj, &d.ties, &d.partials, &d.c64scratch})
+            b->release();
+        for (auto &kv : d.tables) {
+            kv.second->f64.release();
+            kv.second->f32.release();
         }
         for (int c = 0; c < 16; ++c)
             if (d.ck0[c]) {
@@ -1142,7 +1209,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
             }
         cudaEventDestroy(d.ev0);
         cudaEventDestroy(d.ev1);
-        cudaEventDestroy(d.ev_mid);
+        cudaEventDestroy(d.ev_done);
         cudaStreamDestroy(d.stream);
     }
     delete eng;
@@ -1162,72 +1229,39 @@ int fsr_reconstruct_f32(fsr_engine *eng, const fsr_params *p, const float *px,
 
 int fsr_reconstruct_rows_f32(fsr_engine *eng, const fsr_params *p, const float *px,
                              const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
-                             int64_t row1, float *out) {
+                             int64_t row1, double fill, float *out) {
     return reconstruct_host<float>(eng, p, px, mask, height, width, out, nullptr, nullptr, row0,
-                                   row1);
+                                   row1, fill);
+}
+
+int fsr_reconstruct_rows_f64(fsr_engine *eng, const fsr_params *p, const double *px,
+                             const uint8_t *mask, int64_t height, int64_t width, int64_t row0,
+                             int64_t row1, double fill, double *out) {
+    return reconstruct_host<double>(eng, p, px, mask, height, width, out, nullptr, nullptr, row0,
+                                    row1, fill);
 }
 
 int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
                                int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
                                int64_t height, int64_t width, int64_t row0, int64_t row1,
-                               float *d_out, int64_t out_pitch, void *stream) {
-    if (!eng) return fail(nullptr, FSR_EINVAL, "null engine");
-    std::lock_guard<std::mutex> lock(eng->mu);
-    int rc = check_params(eng, p);
-    if (rc) return rc;
-    if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
-    const int64_t brows = (height + p->block - 1) / p->block;
-    if (row0 < 0 || row1 > brows || row0 > row1) return fail(eng, FSR_EINVAL, "block-row range out of bounds");
-    Device &d = *eng->devs[0];
-    if ((rc = select_device(eng, d))) return rc;
-    cudaStream_t st = (cudaStream_t)stream;
-    d.launches = 0;
-    const int K = chunk_count(d, row1 - row0);
-    d.dev_chunks = K;
-    CUDA_TRY(eng, cudaEventRecord(d.ev0, st));
-    if (K == 1) {
-        rc = enqueue_image<float>(eng, d, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
-                                  height, width, row0, row1, nullptr, nullptr, true, NAN, st);
-    } else {
-        // chunks alternate over the lanes, forked from and joined back into the
-        // caller's stream; chunk c uses counter slot c and its own empty-list region
-        if ((rc = ensure_lanes(eng, d))) return rc;
-        const int64_t bcols = (width + p->block - 1) / p->block;
-        CUDA_TRY(eng, d.counters.ensure((size_t)K * sizeof(Counters)));
-        CUDA_TRY(eng, d.empty_list.ensure((size_t)(row1 - row0) * bcols * sizeof(int32_t)));
-        for (auto &ln : d.lanes) {
-            ln->launches = 0;
-            CUDA_TRY(eng, cudaStreamWaitEvent(ln->stream, d.ev0, 0));
-        }
-        for (int c = 0; c < K && rc == FSR_OK; ++c) {
-            Device &ld = *d.lanes[c % kLanes];
-            const int64_t r0 = row0 + (row1 - row0) * c / K, r1 = row0 + (row1 - row0) * (c + 1) / K;
-            rc = enqueue_image<float>(eng, ld, p, d_px, px_pitch, d_mask, mask_pitch, d_out, out_pitch,
-                                      height, width, r0, r1, nullptr, nullptr, true, NAN, ld.stream,
-                                      d.counters.as<Counters>() + c,
-                                      d.empty_list.as<int32_t>() + (r0 - row0) * bcols,
-                                      d.ck0[c], d.ck1[c]);
-            d.used_tma = ld.used_tma;
-        }
-        for (auto &ln : d.lanes) {
-            d.launches += ln->launches;
-            CUDA_TRY(eng, cudaEventRecord(ln->ev1, ln->stream));
-            CUDA_TRY(eng, cudaStreamWaitEvent(st, ln->ev1, 0));
-        }
-    }
-    CUDA_TRY(eng, cudaEventRecord(d.ev1, st));
-    eng->stats = fsr_stats{};
-    eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
-    eng->stats.kernel_launches = d.launches;
-    eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
-    eng->device_stats_pending = rc == FSR_OK;
-    return rc;
+                               float *d_out, int64_t out_pitch, double fill, void *stream) {
+    return reconstruct_device<float>(eng, p, d_px, px_pitch, d_mask, mask_pitch, height, width, row0,
+                                     row1, d_out, out_pitch, fill, stream);
+}
+
+int fsr_reconstruct_device_f64(fsr_engine *eng, const fsr_params *p, const double *d_px,
+                               int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
+                               int64_t height, int64_t width, int64_t row0, int64_t row1,
+                               double *d_out, int64_t out_pitch, double fill, void *stream) {
+    return reconstruct_device<double>(eng, p, d_px, px_pitch, d_mask, mask_pitch, height, width, row0,
+                                      row1, d_out, out_pitch, fill, stream);
 }
 
 // Not part of include/fsr.h: development hook for the guard study
-// (tools/guard_study.py).  Runs the N=32 fp32 kernel on one device with the
-// top-2 tracking on but no re-run, returning each block's minimum relative
-// top-2 objective gap over its iterations and the first iteration whose gap is below guard_tau, plus the selection trace.
+// (tools/guard_study.py).  Runs the N=32 fp32 kernel on the first device with
+// the top-2 tracking on but no re-run, returning each block's minimum relative
+// top-2 gap over its iterations and the first iteration whose gap is below
+// guard_tau, plus the selection trace.
 int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *px,
                          const uint8_t *mask, int64_t H, int64_t W, float *out, float *gaps,
                          int32_t *sel) {
@@ -1241,13 +1275,17 @@ int fsr_debug_guard_gaps(fsr_engine *eng, const fsr_params *p_in, const float *p
     if (rc) return rc;
     DevBuf g;
     CUDA_TRY(eng, g.ensure((size_t)nb * 2 * sizeof(float)));
-    d.gap_debug = g.as<float>();
-    std::vector<std::unique_ptr<Device>> others;
-    // single-device run so the gap buffer indexes every block
-    while (eng->devs.size() > 1) { others.push_back(std::move(eng->devs.back())); eng->devs.pop_back(); }
-    rc = reconstruct_host<float>(eng, &p, px, mask, H, W, out, sel, nullptr);
-    while (!others.empty()) { eng->devs.push_back(std::move(others.back())); others.pop_back(); }
-    d.gap_debug = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(eng->mu);
+        d.gap_debug = g.as<float>();
+    }
+    // first device only (max_devs = 1) and one launch (chunk_count is 1 with
+    // gap_debug set), so the gap buffer indexes every block
+    rc = reconstruct_host<float>(eng, &p, px, mask, H, W, out, sel, nullptr, 0, -1, NAN, 1);
+    {
+        std::lock_guard<std::mutex> lock(eng->mu);
+        d.gap_debug = nullptr;
+    }
     if (rc == FSR_OK)
         CUDA_TRY(eng, cudaMemcpy(gaps, g.p, (size_t)nb * 2 * sizeof(float), cudaMemcpyDeviceToHost));
     g.release();
@@ -1263,30 +1301,19 @@ int fsr_last_stats(const fsr_engine *eng_c, fsr_stats *out) {
         Device &d = *eng->devs[0];
         int rc = select_device(eng, d);
         if (rc) return rc;
-        CUDA_TRY(eng, cudaEventSynchronize(d.ev1));
+        CallCtr call{};
+        int64_t reruns = 0;
         float ms = 0.f, mm = 0.f;
-        if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
-        if (d.dev_chunks > 1) {  // sum of the chunks' main-kernel brackets
-            for (int c = 0; c < d.dev_chunks; ++c) {
-                float t = 0.f;
-                if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) mm += t;
-            }
-        } else if (cudaEventElapsedTime(&mm, d.ev0, d.ev_mid) != cudaSuccess) {
-            mm = 0.f;
-        }
-        (void)cudaGetLastError();
-        std::vector<Counters> cs(std::max(d.dev_chunks, 1));
-        CUDA_TRY(eng, cudaMemcpy(cs.data(), d.counters.p, cs.size() * sizeof(Counters),
-                                 cudaMemcpyDeviceToHost));
+        if ((rc = read_call_stats(eng, d, call, reruns, ms, mm))) return rc;
         eng->stats.kernel_ms = ms;
         eng->stats.main_ms = mm;
-        eng->stats.rerun_blocks = 0;
-        eng->stats.empty_blocks = 0;
-        for (const Counters &c : cs) {
-            eng->stats.rerun_blocks += c.rerun_count;
-            eng->stats.empty_blocks += c.empty_count;
-        }
+        eng->stats.rerun_blocks = reruns;
+        eng->stats.empty_blocks = call.empty_count;
         eng->device_stats_pending = false;
+        *out = eng->stats;
+        // the device API's "no known samples" (reconstruction.py:273-274)
+        if (call.status == 2) return fail(eng, FSR_ENOSAMPLES, "no known samples");
+        return FSR_OK;
     }
     *out = eng->stats;
     return FSR_OK;
@@ -1413,6 +1440,7 @@ int fsr_iterate_spectra(fsr_engine *eng, const fsr_params *p, int64_t count, int
     if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
     (void)cudaGetLastError();
     eng->stats = fsr_stats{};
+    eng->device_stats_pending = false;
     eng->stats.blocks = count;
     eng->stats.kernel_launches = 1;
     eng->stats.kernel_ms = ms;

@@ -35,9 +35,8 @@ namespace fsr {
 
 constexpr int C64_THREADS = 128;
 constexpr int C64_TS = 65;  // fp64 tile row stride (double2)
-constexpr int C64_BOX_PX = 68, C64_BOX_MK = 80;
-constexpr int C64_STAGE_MK = 64 * C64_BOX_PX * 4;                 // 17408
-constexpr int C64_STAGE_BYTES = C64_STAGE_MK + 64 * C64_BOX_MK;   // 22528
+constexpr int C64_BOX_PX = TmaBox<float, 64, 64>::PX, C64_BOX_MK = TmaBox<float, 64, 64>::MK;
+// staging 22528 B (f32 pixels) / 38912 B (f64 pixels), inside the 65 KiB region
 constexpr int C64_REGION = 64 * C64_TS * 16;                      // 66560 >= 64 KiB U table
 
 struct __align__(16) C64Slot {
@@ -165,7 +164,7 @@ __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const
 #ifndef FSR_C64_PAIRKEY
 #define FSR_C64_PAIRKEY 1
 #endif
-template <bool GUARD>
+template <typename IO, int ARGMAX, bool GUARD>
 __global__ void __launch_bounds__(C64_THREADS, 3)
     cta64_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     // pair keys in guarded mode (every near-tie is re-run in fp64, see warp32)
@@ -205,32 +204,34 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         const int64_t r0 = brow * a.B, c0 = bcol * a.B;
         const int64_t wr0 = r0 - a.L, wc0 = c0 - a.L;
         // ---- gather: thread owns window column v, rows 32h .. 32h + 31
-        float pf[32];
-        uint32_t pm[32];
+        using Box = TmaBox<IO, 64, 64>;
+        IO pf[32];
+        uint32_t mbits = 0;
         if (a.use_tma) {
-            const int x0 = (int)wc0, xp = x0 & ~3, xm = x0 & ~15;
-            const float *spx = reinterpret_cast<const float *>(sm.region);
-            const uint8_t *smk = sm.region + C64_STAGE_MK;
+            const int x0 = (int)wc0, xp = x0 & ~(Box::ALIGN - 1), xm = x0 & ~15;
+            const IO *spx = reinterpret_cast<const IO *>(sm.region);
+            const uint8_t *smk = sm.region + Box::STAGE_MK;
             if (wid == 0)
-                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, C64_STAGE_BYTES);
+                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::STAGE_BYTES);
             mbar_wait(bar, phase);
             phase ^= 1u;
-            const float *cpx = spx + 32 * h * C64_BOX_PX + (x0 - xp) + v;
-            const uint8_t *cmk = smk + 32 * h * C64_BOX_MK + (x0 - xm) + v;
+            const IO *cpx = spx + 32 * h * Box::PX + (x0 - xp) + v;
+            const uint8_t *cmk = smk + 32 * h * Box::MK + (x0 - xm) + v;
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
-                pf[k] = cpx[k * C64_BOX_PX];
-                pm[k] = cmk[k * C64_BOX_MK];
+                pf[k] = cpx[k * Box::PX];
+                mbits |= (uint32_t)(cmk[k * Box::MK] != 0) << k;
             }
         } else {
             const int64_t x = wc0 + v;
             const bool xin = x >= 0 && x < a.W;
+            const IO *px = static_cast<const IO *>(a.px);
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const int64_t y = wr0 + 32 * h + k;
                 const bool in = xin && y >= 0 && y < a.H;
-                pf[k] = in ? __ldg(a.px + y * a.px_pitch + x) : 0.f;
-                pm[k] = in ? (uint32_t)__ldg(a.mask + y * a.mask_pitch + x) : 0u;
+                pf[k] = in ? __ldg(px + y * a.px_pitch + x) : (IO)0;
+                mbits |= (uint32_t)(in && __ldg(a.mask + y * a.mask_pitch + x) != 0) << k;
             }
         }
         __syncthreads();  // staging fully read before the tile overwrites it
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         for (int k = 0; k < 32; ++k) {
             const int r = 32 * h + k;
             double f = 0.0, w = 0.0;
-            if (pm[k]) {
+            if ((mbits >> k) & 1u) {
                 f = (double)pf[k];
                 w = __ldg(a.decay64 + r * 64 + v);
             }
@@ -321,9 +322,11 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 swap ? pass64<GUARD, H, true, true, PK>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2)
                      : pass64<GUARD, H, true, false, PK>(re, im, wf2, up, gr, gi, canon, h, a.key_mask, m1, m2);
             // phase 1: in-warp argmax, coefficient of the warp's best bin
-            const uint32_t kw = __reduce_max_sync(0xffffffffu, m1);
-            const uint32_t bal = __ballot_sync(0xffffffffu, m1 == kw);
-            const int wl = PK ? 31 - __clz(bal) : __ffs(bal) - 1;
+            // (ARGMAX: the paper's __shfl_xor_sync butterfly, redux.sync + ballot,
+            // or the shared-memory tree -- the same cross-lane step as warp32)
+            uint32_t kw;
+            int wl;
+            cross_lane_best<ARGMAX, PK>(m1, kw, wl, sm.red_key[wid], sm.red_rank[wid]);
             uint32_t k1w = kw, k2w = 0u;
             float cre, cim;
             if (PK) {
@@ -432,7 +435,8 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const int m = tid / a.B, n = tid % a.B;
             const int64_t y = r0 + m, xx = c0 + n;
             if (y < a.H && xx < a.W)
-                a.out[y * a.out_pitch + xx] = a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+                static_cast<IO *>(a.out)[y * a.out_pitch + xx] =
+                    a.mask[y * a.mask_pitch + xx] ? static_cast<const IO *>(a.px)[y * a.px_pitch + xx] : (IO)acc;
         }
         __syncthreads();  // the region is rewritten by the next block's gather
     }

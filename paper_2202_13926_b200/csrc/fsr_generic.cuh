@@ -181,6 +181,7 @@ struct IterateArgs {
     int32_t *done;         // [count] or null
 };
 
+#ifdef FSR_ABI_TU  // non-template kernel: defined in fsr_abi.cu's translation unit only
 __global__ void __launch_bounds__(GEN_THREADS) iterate_spectra_kernel(IterateArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int n = a.N * a.N;
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(GEN_THREADS) iterate_spectra_kernel(IterateArg
         __syncthreads();
     }
 }
+#endif
 
 // ---------------------------------------------------------------------------
 // Image path, CTA per block: gather -> w = decay*mask -> packed 2-D DFT ->
@@ -391,37 +393,26 @@ __global__ void __launch_bounds__(GEN_THREADS) image_generic_kernel(ImageArgs<Re
     }
 }
 
-// Empty-support fallback (reconstruction.py:272-275): the listed blocks get
-// the global mean of the known samples.
+// Empty-support fallback (reconstruction.py:236-237, 272-275).
+//
+// mean_partial_kernel: per-CTA (sum of known pixels, count of known pixels)
+// over rows [0, H), each thread striding over the pixels in a fixed order and
+// the CTA combining its threads by a fixed tree -- so, for a fixed grid, the
+// partials (and the mean fill_empty_kernel forms from them) are bitwise
+// reproducible.  A no-op unless some block of the call was empty.
 template <typename IO>
-__global__ void fill_blocks_kernel(IO *out, int64_t out_pitch, int64_t H, int64_t W, int B,
-                                   int64_t bcols, const int32_t *list,
-                                   const unsigned int *count, const double *fill_ptr,
-                                   double fill_value) {
-    const double fill = fill_ptr ? *fill_ptr : fill_value;
-    for (int i = blockIdx.x; i < (int)*count; i += gridDim.x) {
-        int64_t bid = list[i];
-        int64_t r0 = (bid / bcols) * B, c0 = (bid % bcols) * B;
-        int h = (int)min((int64_t)B, H - r0), w = (int)min((int64_t)B, W - c0);
-        for (int p = threadIdx.x; p < h * w; p += blockDim.x)
-            out[(r0 + p / w) * out_pitch + c0 + p % w] = (IO)fill;
-    }
-}
-
-// Mean of the known samples over rows [0, H) (reconstruction.py:236-237:
-// sum of all pixels / count of known); a no-op unless a block was empty.
-// acc[0] = sum, acc[1] = count, *fill = sum / count (written by the last CTA).
-template <typename IO>
-__global__ void mean_known_kernel(const IO *px, int64_t px_pitch, const uint8_t *mask,
-                                  int64_t mask_pitch, int64_t H, int64_t W,
-                                  const unsigned int *empty_count, double *acc,
-                                  unsigned int *ticket, double *fill, int *status) {
+__global__ void __launch_bounds__(256) mean_partial_kernel(const IO *px, int64_t px_pitch,
+                                                           const uint8_t *mask, int64_t mask_pitch,
+                                                           int64_t H, int64_t W,
+                                                           const unsigned int *empty_count,
+                                                           double2 *partials) {
     if (*empty_count == 0) return;
+    __shared__ double2 ws[8];
     double s = 0.0, c = 0.0;
     const int64_t total = H * W;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t y = i / W, x = i - y * W;
+        const int64_t y = i / W, x = i - y * W;
         if (mask[y * mask_pitch + x]) {
             s += (double)px[y * px_pitch + x];
             c += 1.0;
@@ -429,23 +420,59 @@ __global__ void mean_known_kernel(const IO *px, int64_t px_pitch, const uint8_t 
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, off);
-        c += __shfl_xor_sync(0xffffffffu, c, off);
+        s += __shfl_down_sync(0xffffffffu, s, off);
+        c += __shfl_down_sync(0xffffffffu, c, off);
     }
-    if (lane_id() == 0) {
-        atomicAdd(&acc[0], s);
-        atomicAdd(&acc[1], c);
-    }
-    __threadfence();
+    if (lane_id() == 0) ws[warp_id()] = make_double2(s, c);
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned t = atomicAdd(ticket, 1u);
-        if (t == gridDim.x - 1) {
-            __threadfence();
-            double S = atomicAdd(&acc[0], 0.0), C = atomicAdd(&acc[1], 0.0);
-            if (C == 0.0) *status = 2;  // "no known samples"
-            *fill = C > 0.0 ? S / C : 0.0;
+        double2 t = ws[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            t.x += ws[w].x;
+            t.y += ws[w].y;
         }
+        partials[blockIdx.x] = t;
+    }
+}
+
+// fill_empty_kernel: the listed blocks get `fill_value`, or (partials != null)
+// sum/count of the nparts partials, summed by one warp in a fixed order (every
+// CTA forms the same value).  status = 2 if a block was empty but the image
+// holds no known sample ("no known samples", reconstruction.py:273-274).
+template <typename IO>
+__global__ void fill_empty_kernel(IO *out, int64_t out_pitch, int64_t H, int64_t W, int B,
+                                  int64_t bcols, const int32_t *list, const unsigned int *count,
+                                  const double2 *partials, int nparts, double fill_value,
+                                  int *status) {
+    const int n = (int)*count;
+    if (n == 0) return;
+    __shared__ double fill_s;
+    if (threadIdx.x < 32) {
+        double fill = fill_value;
+        if (partials) {
+            double S = 0.0, C = 0.0;
+            for (int i = threadIdx.x; i < nparts; i += 32) {
+                S += partials[i].x;
+                C += partials[i].y;
+            }
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+                S += __shfl_xor_sync(0xffffffffu, S, off);
+                C += __shfl_xor_sync(0xffffffffu, C, off);
+            }
+            if (C == 0.0 && blockIdx.x == 0 && threadIdx.x == 0) *status = 2;
+            fill = C > 0.0 ? S / C : 0.0;
+        }
+        if (threadIdx.x == 0) fill_s = fill;
+    }
+    __syncthreads();
+    const double fill = fill_s;
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t bid = list[i];
+        const int64_t r0 = (bid / bcols) * B, c0 = (bid % bcols) * B;
+        const int h = (int)min((int64_t)B, H - r0), w = (int)min((int64_t)B, W - c0);
+        for (int q = threadIdx.x; q < h * w; q += blockDim.x)
+            out[(r0 + q / w) * out_pitch + c0 + q % w] = (IO)fill;
     }
 }
 

@@ -30,9 +30,8 @@ namespace fsr {
 
 constexpr int W16_US = 20;  // U16 row stride (float4)
 constexpr int W16_TS = 17;  // fp64 tile row stride (double2)
-constexpr int W16_BOX_PX = 20, W16_BOX_MK = 32;
-constexpr int W16_STAGE_MK = 16 * W16_BOX_PX * 4;                 // 1280
-constexpr int W16_STAGE_BYTES = W16_STAGE_MK + 16 * W16_BOX_MK;   // 1792
+constexpr int W16_BOX_PX = TmaBox<float, 16, 16>::PX, W16_BOX_MK = TmaBox<float, 16, 16>::MK;
+// staging: 1792 B (f32 pixels), 2816 B (f64 pixels) -- both inside the 5 KiB per warp
 
 template <int WARPS>
 struct Warp16Smem {
@@ -111,39 +110,41 @@ __device__ __forceinline__ void pass16_update(float2 (&re)[4], float2 (&im)[4], 
 // Gather + fp64 2-D FFT + split for one N = 16 window.  Lane l gathers window
 // column l & 15, rows (l >> 4) * 8 .. + 7; lanes 0..15 each transform one row,
 // then one column; lane (v, p) then keeps rows p + 2j of spectral column v.
-template <bool TREE>
+template <typename IO, bool TREE>
 __device__ __forceinline__ double w16_prologue(const Warp32Args &a, const Warp32Maps &maps, float4 *ub,
                                                uint32_t bar, uint32_t &phase, float2 (&re)[4],
                                                float2 (&im)[4], int64_t wr0, int64_t wc0, int lane,
                                                int v, int p) {
+    using Box = TmaBox<IO, 16, 16>;
     double2 *t = reinterpret_cast<double2 *>(ub);
     const int cl = lane & 15, rh = lane >> 4;
-    float pf[8];
+    IO pf[8];
     uint32_t pm[8];
     if (a.use_tma) {
         const int x0 = (int)wc0;
-        const int xp = x0 & ~3, xm = x0 & ~15;
-        const float *spx = reinterpret_cast<const float *>(ub);
-        const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + W16_STAGE_MK;
-        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, W16_STAGE_BYTES);
+        const int xp = x0 & ~(Box::ALIGN - 1), xm = x0 & ~15;
+        const IO *spx = reinterpret_cast<const IO *>(ub);
+        const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + Box::STAGE_MK;
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::STAGE_BYTES);
         mbar_wait(bar, phase);
         phase ^= 1u;
-        const float *cpx = spx + rh * 8 * W16_BOX_PX + (x0 - xp) + cl;
-        const uint8_t *cmk = smk + rh * 8 * W16_BOX_MK + (x0 - xm) + cl;
+        const IO *cpx = spx + rh * 8 * Box::PX + (x0 - xp) + cl;
+        const uint8_t *cmk = smk + rh * 8 * Box::MK + (x0 - xm) + cl;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            pf[k] = cpx[k * W16_BOX_PX];
-            pm[k] = cmk[k * W16_BOX_MK];
+            pf[k] = cpx[k * Box::PX];
+            pm[k] = cmk[k * Box::MK];
         }
         __syncwarp();
     } else {
         const int64_t x = wc0 + cl;
         const bool xin = x >= 0 && x < a.W;
+        const IO *px = static_cast<const IO *>(a.px);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int64_t y = wr0 + rh * 8 + k;
             const bool in = xin && y >= 0 && y < a.H;
-            pf[k] = in ? __ldg(a.px + y * a.px_pitch + x) : 0.f;
+            pf[k] = in ? __ldg(px + y * a.px_pitch + x) : (IO)0;
             pm[k] = in ? (uint32_t)__ldg(a.mask + y * a.mask_pitch + x) : 0u;
         }
     }
@@ -218,7 +219,7 @@ __device__ __forceinline__ double w16_prologue(const Warp32Args &a, const Warp32
 #ifndef FSR_W16_WARPS_PER_SM
 #define FSR_W16_WARPS_PER_SM 24  // resident warps (blocks) per SM the register budget targets (measured at 1080p: 20 -> 24 is +3 %, 28 and 32 are slower)
 #endif
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD, int OPTS = W32_ALL>
+template <typename IO, int WARPS, bool TREE, int ARGMAX, bool GUARD, int OPTS = W32_ALL>
 __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
     warp16_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
         const int64_t r0 = brow * a.B, c0 = bcol * a.B;
         float2 re[4], im[4];
         const float energy =
-            (float)w16_prologue<LT>(a, maps, ub, bar, phase, re, im, r0 - a.L, c0 - a.L, lane, v, p);
+            (float)w16_prologue<IO, LT>(a, maps, ub, bar, phase, re, im, r0 - a.L, c0 - a.L, lane, v, p);
         const float w00 = ub[8 * W16_US].x;  // U16[8][0].x = Wx[0][0] = sum of the weights
         int32_t *sel_b = (TRACE && a.sel) ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
         if (!(w00 > 0.f)) {  // empty support (reconstruction.py:272-275)
@@ -376,7 +377,8 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             const int m = lane / a.B, n = lane % a.B;
             const int64_t y = r0 + m, xx = c0 + n;
             if (y < a.H && xx < a.W)
-                a.out[y * a.out_pitch + xx] = a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+                static_cast<IO *>(a.out)[y * a.out_pitch + xx] =
+                    a.mask[y * a.mask_pitch + xx] ? static_cast<const IO *>(a.px)[y * a.px_pitch + xx] : (IO)acc;
         }
         __syncwarp();
     }

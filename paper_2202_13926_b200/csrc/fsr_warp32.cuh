@@ -58,11 +58,11 @@ namespace fsr {
 enum ArgmaxImpl { AM_SHFL = 0, AM_SMEM = 1, AM_REDUX = 2 };
 
 struct Warp32Args {
-    const float *px;
+    const void *px;        // IO pixels (float or double: the kernels are templated on IO)
     int64_t px_pitch;
     const uint8_t *mask;
     int64_t mask_pitch;
-    float *out;
+    void *out;             // IO output
     int64_t out_pitch;
     int64_t H, W;
     int B, L, iterations, early_stop;
@@ -90,9 +90,21 @@ struct Warp32Args {
 // on a 16-byte boundary in the innermost dimension, so the boxes are widened
 // (pixels 36 = 32 + 4 columns from x0 rounded down to a multiple of 4, mask
 // 48 = 32 + 16 from a multiple of 16) and each lane reads at its offset.
-constexpr int W32_BOX_PX = 36, W32_BOX_MK = 48;
-constexpr int W32_STAGE_MK = 32 * W32_BOX_PX * 4;                    // mask staging offset (bytes)
-constexpr int W32_STAGE_BYTES = W32_STAGE_MK + 32 * W32_BOX_MK;      // 6144
+// The same holds for f64 pixels (the reference's own input type, core.py:24):
+// 16 bytes are 2 doubles, so the pixel box is N + 2 columns from an even start.
+// TmaBox<IO, ROWS, N> gives the box and staging layout of an N-column window of
+// ROWS rows for pixel type IO (the mask box is always N + 16 bytes wide).
+template <typename IO, int ROWS, int N>
+struct TmaBox {
+    static constexpr int ALIGN = 16 / (int)sizeof(IO);             // pixels per 16 bytes
+    static constexpr int PX = N + ALIGN;                           // pixel box columns
+    static constexpr int MK = N + 16;                              // mask box columns
+    static constexpr int STAGE_MK = ROWS * PX * (int)sizeof(IO);   // mask staging offset (bytes)
+    static constexpr int STAGE_BYTES = STAGE_MK + ROWS * MK;
+    static_assert(STAGE_MK % 128 == 0, "TMA destinations must be 128-byte aligned");
+};
+constexpr int W32_BOX_PX = TmaBox<float, 32, 32>::PX, W32_BOX_MK = TmaBox<float, 32, 32>::MK;
+constexpr int W32_STAGE_BYTES = TmaBox<float, 32, 32>::STAGE_BYTES;  // 6144 (f32), 10240 (f64)
 struct alignas(64) Warp32Maps {
     CUtensorMap px;
     CUtensorMap mask;
@@ -360,38 +372,40 @@ __device__ __forceinline__ void pass_update(float2 (&re)[16], float2 (&im)[16], 
 // fp64 prologue: gather, weights, 2-D FFT and Hermitian split in double
 // precision, then R (registers, packed row pairs) and W (U table in shared
 // memory) rounded to fp32 once.  Returns the early-stop energy sum f^2 w.
-template <bool TREE>
+template <typename IO, bool TREE>
 __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Warp32Maps &maps,
                                                    float4 *ub, uint32_t bar, uint32_t &phase,
                                                    float2 (&re)[16], float2 (&im)[16], int64_t wr0,
                                                    int64_t x, bool xin, int lane, int v) {
+    using Box = TmaBox<IO, 32, 32>;
     double2 *t = reinterpret_cast<double2 *>(ub);  // 32 x 33 double2 (16.5 KiB)
     // ---- gather: every row's pixel and mask load is issued before any is used.
     // Window rows k in [k0, k1) lie inside the image; outside rows and columns
-    // are unknown (sampling.py:93-107).
-    float pf[32];
-    uint32_t pm[32];
+    // are unknown (sampling.py:93-107).  The mask is kept as one bit per row.
+    IO pf[32];
+    uint32_t mbits = 0;
     if (a.use_tma) {
-        // the 32 x 32 window of pixels (4 KiB) and mask (1 KiB) lands in the
-        // tile region by TMA; lane l then reads window column l
+        // the 32 x 32 window of pixels (4 KiB f32 / 8 KiB f64) and mask (1 KiB)
+        // lands in the tile region by TMA; lane l then reads window column l
         const int x0 = (int)(x - lane);
-        const int xp = x0 & ~3, xm = x0 & ~15;  // floor to 16-byte boundaries
-        const float *spx = reinterpret_cast<const float *>(ub);
-        const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + W32_STAGE_MK;
-        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0);
+        const int xp = x0 & ~(Box::ALIGN - 1), xm = x0 & ~15;  // floor to 16-byte boundaries
+        const IO *spx = reinterpret_cast<const IO *>(ub);
+        const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + Box::STAGE_MK;
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0,
+                   Box::STAGE_BYTES);
         mbar_wait(bar, phase);
         phase ^= 1u;
-        const float *cpx = spx + (x0 - xp) + lane;
+        const IO *cpx = spx + (x0 - xp) + lane;
         const uint8_t *cmk = smk + (x0 - xm) + lane;
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-            pf[k] = cpx[k * W32_BOX_PX];
-            pm[k] = cmk[k * W32_BOX_MK];
+            pf[k] = cpx[k * Box::PX];
+            mbits |= (uint32_t)(cmk[k * Box::MK] != 0) << k;
         }
         __syncwarp();
     } else {
         const int64_t xc = xin ? x : 0;
-        const float *pp = a.px + wr0 * a.px_pitch + xc;
+        const IO *pp = static_cast<const IO *>(a.px) + wr0 * a.px_pitch + xc;
         const uint8_t *mp = a.mask + wr0 * a.mask_pitch + xc;
         const int k0 = wr0 < 0 ? (int)-wr0 : 0;
         const int k1 = a.H - wr0 < 32 ? (int)(a.H - wr0) : 32;
@@ -399,8 +413,8 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
             const bool in = xin && k >= k0 && k < k1;
-            pf[k] = in ? __ldg(pp + k * ppitch) : 0.f;
-            pm[k] = in ? (uint32_t)__ldg(mp + k * mpitch) : 0u;
+            pf[k] = in ? __ldg(pp + k * ppitch) : (IO)0;
+            mbits |= (uint32_t)(in && __ldg(mp + k * mpitch) != 0) << k;
         }
     }
     double2 *tl = t + lane;  // column `lane` of the tile
@@ -408,7 +422,7 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
         double f = 0.0, w = 0.0;
-        if (pm[k]) {
+        if ((mbits >> k) & 1u) {
             f = (double)pf[k];
             w = __ldg(a.decay64 + k * 32 + lane);
         }
@@ -506,7 +520,7 @@ constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_ALL = 3;
 #ifndef FSR_W32_WARPS_PER_SM
 #define FSR_W32_WARPS_PER_SM 12  // resident warps (blocks) per SM the register budget targets
 #endif
-template <int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY, int OPTS = W32_ALL>
+template <typename IO, int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY, int OPTS = W32_ALL>
 __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
@@ -553,7 +567,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         const int64_t wr0 = r0 - a.L, x = c0 - a.L + lane;
         const bool xin = x >= 0 && x < a.W;
         float2 re[16], im[16];
-        const float energy = (float)w32_prologue_f64<LT>(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane, v);
+        const float energy = (float)w32_prologue_f64<IO, LT>(a, maps, ub, bar, phase, re, im, wr0, x, xin, lane, v);
         const float w00 = ub[16 * 32].x;  // U[16][0].x = Wx[0][0] = sum of the weights
         // frequency prior of this column for the row pairs (i, i+16) (weights.py:40-56);
         // re-read per block (L1-resident) so it is not live across the prologue
@@ -743,8 +757,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             const int m = lane / a.B, n = lane % a.B;
             const int64_t y = r0 + m, xx = c0 + n;
             if (y < a.H && xx < a.W)
-                a.out[y * a.out_pitch + xx] =
-                    a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : acc;
+                static_cast<IO *>(a.out)[y * a.out_pitch + xx] =
+                    a.mask[y * a.mask_pitch + xx] ? static_cast<const IO *>(a.px)[y * a.px_pitch + xx]
+                                                  : (IO)acc;
         }
         }
         __syncwarp();

@@ -69,9 +69,10 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
 
     ``support`` is the FFT size N = block + 2*border; N - block must be even
     (reference cli.py:186-188).  Supports up to 64 are accepted (the tree
-    reducer is limited to N*N <= 1024, like the reference).  Returns an array of
-    the compute precision's I/O type (float32 for fp32 modes, float64 for fp64),
-    or ``(array, Trace)`` with ``return_trace``.  ``argmax`` picks the warp
+    reducer is limited to N*N <= 1024, like the reference).  Returns float64 for
+    float64 input (the reference's pixel type, in every precision: the fp32 loop
+    reads the f64 pixels directly) and float32 for float32 input in the fp32
+    modes; or ``(array, Trace)`` with ``return_trace``.  ``argmax`` picks the warp
     argmax implementation -- "redux" (redux.sync + ballot, the fastest on
     B200), "shfl" (the paper's shuffle butterfly) or "smem" (the paper's
     shared-memory comparison point); all three give bitwise-identical results.
@@ -86,7 +87,9 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
         raise ValueError("image must be a 2D grid with at least one pixel")
     if m.shape != img.shape:
         raise ValueError("image and mask dimensions differ")
-    io = np.float64 if precision == "fp64" else np.float32
+    # every precision takes the reference's f64 pixels as they are (the fp32
+    # kernels' prologue reads and transforms them in fp64); f32 input stays f32
+    io = np.float32 if (img.dtype == np.float32 and precision != "fp64") else np.float64
     img = np.ascontiguousarray(img, dtype=io)
     m = np.ascontiguousarray(m, dtype=bool)
     params = _lib.make_params(block, border, iterations, rho, gamma, reducer, early_stop,

@@ -12,6 +12,12 @@ shards with no collective on the data path:
   devices it is given (fsr_abi.cu, reconstruct_host).
 * frames: a stream of frames is dealt round-robin (``frame_shard``), no halo.
 
+The one frame-wide quantity is the empty-support fill (reconstruction.py:
+236-237: the mean of ALL known samples of the frame).  A rank that holds the
+whole frame computes it exactly as the reference does (``frame_fill``); the
+strips then receive it as an argument, so a rank's blocks never depend on
+which rows it happens to hold.
+
 The only collective is the final assembly of a frame on one rank
 (``gather_strips``): every rank contributes its output rows with one
 ``all_gather_into_tensor`` (NCCL over NVLink on GPUs, gloo on CPU).  Output
@@ -81,38 +87,53 @@ def gather_strips(local_rows, row0: int, row1: int, block: int, height: int, wid
     return out
 
 
+def frame_fill(pixels: np.ndarray, mask: np.ndarray) -> float:
+    """The reference's empty-support value (reconstruction.py:236-237): the sum of
+    the frame's pixels over the number of known samples, in the same numpy
+    arithmetic (so the bits match); NaN when the frame has no known sample (the
+    engine then raises "no known samples" if a block needs the fill)."""
+    known = int(np.count_nonzero(mask))
+    return float(np.asarray(pixels, dtype=np.float64).sum()) / known if known else float("nan")
+
+
 def reconstruct_strip_host(pixels: np.ndarray, mask: np.ndarray, block: int, border: int,
                            rank: int, world: int,
-                           strip_fn: Callable[[np.ndarray, np.ndarray, int, int, int], np.ndarray]):
+                           strip_fn: Callable[..., np.ndarray], fill: float | None = None):
     """Run ``strip_fn`` on this rank's halo rows and return (row0, row1, out_rows).
 
-    ``strip_fn(px_rows, mask_rows, ya, row0, row1)`` reconstructs block rows
-    [row0, row1) of the frame given the image rows [ya, ya + len(px_rows)) and
-    returns the full-width output rows [row0*B, row1*B) clipped to the frame.
+    ``strip_fn(px_rows, mask_rows, ya, row0, row1, fill)`` reconstructs block
+    rows [row0, row1) of the frame given the image rows [ya, ya + len(px_rows))
+    and the frame-wide empty-support value ``fill``, and returns the full-width
+    output rows [row0*B, row1*B) clipped to the frame.  ``fill`` defaults to
+    ``frame_fill(pixels, mask)`` (every rank holds the frame here).
     """
     height = pixels.shape[0]
     row0, row1 = strip_rows(block_rows(height, block), rank, world)
     ya, yb, oa, ob = strip_io_rows(row0, row1, block, border, height)
-    out = strip_fn(pixels[ya:yb], mask[ya:yb], ya, row0, row1)
+    if fill is None:
+        fill = frame_fill(pixels, mask)
+    out = strip_fn(pixels[ya:yb], mask[ya:yb], ya, row0, row1, fill)
     if out.shape[0] != ob - oa:
         raise ValueError(f"strip_fn returned {out.shape[0]} rows, expected {ob - oa}")
     return row0, row1, out
 
 
 def engine_strip_fn(params, height: int, width: int, engine=None):
-    """strip_fn backed by the CUDA engine (fsr_reconstruct_rows_f32: only the
-    strip's halo rows travel to the device), for ``reconstruct_strip_host``."""
+    """strip_fn backed by the CUDA engine (fsr_reconstruct_rows_f32/_f64: only
+    the strip's halo rows are read and travel to the device; the empty-support
+    value comes in as ``fill``), for ``reconstruct_strip_host``."""
     from . import _lib
 
     eng = engine or _lib.default_engine()
 
-    def run(px_rows, mask_rows, ya, row0, row1):
-        full_px = np.zeros((height, width), np.float32)
+    def run(px_rows, mask_rows, ya, row0, row1, fill):
+        io = np.float32 if px_rows.dtype == np.float32 else np.float64
+        full_px = np.zeros((height, width), io)
         full_mk = np.zeros((height, width), np.uint8)
         full_px[ya:ya + px_rows.shape[0]] = px_rows
         full_mk[ya:ya + mask_rows.shape[0]] = mask_rows
-        out = np.zeros((height, width), np.float32)
-        eng.reconstruct_rows(full_px, full_mk, params, row0, row1, out)
+        out = np.zeros((height, width), io)
+        eng.reconstruct_rows(full_px, full_mk, params, row0, row1, out, fill=fill)
         oa, ob = min(height, row0 * params.block), min(height, row1 * params.block)
         return out[oa:ob]
 

@@ -1,0 +1,70 @@
+"""Whole-frame parity at BASELINE configs[1] (1920x1080 quarter-sampled,
+B=4, N=32, I=100, rho=0.7, gamma=0.5, tree): every one of the 129,600 blocks
+of the GPU engine against the CPU restatement of the reference (oracle/port.py,
+pinned bitwise to fsrkit by tests/golden), in both precisions:
+
+  * fp64 validation -- per-block selection sequences equal to the reference's
+    modulo the conjugate mirror; any other divergence must be a
+    proven co-maximal split (pkg/tests/test_acceptance.py:73-87); known pixels
+    bitwise; PSNR within 1e-6 dB;
+  * fp32 production on the reference's own f64 pixels -- max |d| <= 1e-3 on
+    the 0..1 scale and |dPSNR| <= 0.01 dB (north_star tolerance).
+
+The CPU side takes ~10-15 s on the GPU box's 16 host cores.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import port as oracle
+
+pytestmark = pytest.mark.gpu
+
+fsr = pytest.importorskip("paper_2202_13926_b200")
+
+H, W, B, N, I = 1080, 1920, 4, 32, 100
+L = (N - B) // 2
+
+
+@pytest.fixture(scope="module")
+def frame():
+    img = oracle.synthetic_frame(H, W, 7)
+    sampled, mask = oracle.quarter_sample(img, 42)
+    ref, rtr = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, "tree", trace=True)
+    return img, sampled, mask, ref, rtr
+
+
+def test_fullframe_1080p_fp64_sequences(frame):
+    img, sampled, mask, ref, rtr = frame
+    out, tr = fsr.reconstruct(sampled, mask, B, N, I, precision="fp64", return_trace=True)
+    counts, div = oracle.compare_sequences(tr.selections[:, :I].astype(np.int64),
+                                           rtr["sel"][:, :I].astype(np.int64), N)
+    nb = tr.selections.shape[0]
+    assert counts["equal"] + counts["mirror"] + counts["diverged"] == nb == 129600
+    print(f"fp64 1080p: equal {counts['equal']}, mirror {counts['mirror']}, "
+          f"diverged {counts['diverged']} of {nb}")
+    assert counts["diverged"] <= nb // 1000  # mirror-equal for >= 99.9 % of the blocks
+    for b in np.nonzero(div)[0]:
+        ok, f, gap = oracle.coemaximal_split(sampled, mask, B, L, I, 0.7, 0.5, "tree", int(b),
+                                             tr.selections[b])
+        assert ok, f"block {b}: diverges at iteration {f}, objective gap {gap:.3e}"
+    # outside proven splits the pixels agree to fp64 rounding
+    err = np.abs(out - ref)
+    bc = W // B
+    bad = {(int(y) // B) * bc + int(x) // B for y, x in np.argwhere(err > 1e-9 * 255)}
+    assert bad <= set(np.nonzero(div)[0].tolist())
+    assert np.array_equal(out[mask], sampled[mask])
+    assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= 1e-6
+
+
+def test_fullframe_1080p_fp32_production(frame):
+    img, sampled, mask, ref, _ = frame
+    out, tr = fsr.reconstruct(sampled, mask, B, N, I, precision="fp32", return_trace=True)
+    assert out.dtype == np.float64
+    err = float(np.abs(out - ref).max())
+    dpsnr = oracle.psnr(img, out) - oracle.psnr(img, ref)
+    print(f"fp32 1080p: max|d| {err / 255:.3e} (0..1), dPSNR {dpsnr:+.2e} dB, "
+          f"re-runs {tr.stats['rerun_blocks']}")
+    assert err <= 1e-3 * 255, err
+    assert abs(dpsnr) <= 0.01
+    assert np.array_equal(out[mask], sampled[mask])

@@ -145,8 +145,7 @@ def test_image_production_tolerance(name, precision):
         assert err <= FP32_TOL, f"{name}/{red}: max|d| {err:.4f}"
         assert dpsnr <= PSNR_TOL, f"{name}/{red}: dPSNR {dpsnr:.4f}"
         known = d["mask"]
-        io = np.float64 if precision == "fp64" else np.float32
-        assert np.array_equal(out[known], d["sampled"][known].astype(io).astype(np.float64))
+        assert np.array_equal(out[known], d["sampled"][known])  # f64 pixels in every precision
 
 
 @pytest.mark.parametrize("name", ["c1_natural", "c1_uniform"])
@@ -236,18 +235,21 @@ def test_device_api_matches_host_api():
     assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
 
 
+@pytest.mark.parametrize("io", ["f32", "f64"])
 @pytest.mark.parametrize("support", [32, 16, 64])
 @pytest.mark.parametrize("shape", [(96, 128), (1080 // 8, 1920 // 8)])
-def test_tma_gather_matches_plain_loads(monkeypatch, shape, support):
-    """The N=32 fp32 kernel gathers each 32x32 window with 2-D TMA (zero fill
-    outside the image = the reference's outside-is-unknown rule,
-    sampling.py:93-107).  It must give bitwise the same image as the
-    plain-load gather, on frames whose windows cross all four edges."""
+def test_tma_gather_matches_plain_loads(monkeypatch, shape, support, io):
+    """The fp32-loop kernels gather each window with 2-D TMA (zero fill outside
+    the image = the reference's outside-is-unknown rule, sampling.py:93-107),
+    for f32 and f64 pixels (f64: 16-byte aligned boxes of N + 2 columns).  It
+    must give bitwise the same image as the plain-load gather, on frames whose
+    windows cross all four edges."""
     from paper_2202_13926_b200 import _lib
     H, W = shape
     img = oracle.synthetic_frame(H, W, 11)
     sampled, mask = oracle.quarter_sample(img, 5)
-    px, m8 = sampled.astype(np.float32), mask.astype(np.uint8)
+    px = sampled.astype(np.float32 if io == "f32" else np.float64)
+    m8 = mask.astype(np.uint8)
     outs = {}
     for no_tma in ("0", "1"):
         monkeypatch.setenv("FSR_NO_TMA", no_tma)
@@ -263,6 +265,101 @@ def test_tma_gather_matches_plain_loads(monkeypatch, shape, support):
         assert outs["0", precision][1] & 1, "TMA gather not used"
         assert not outs["1", precision][1] & 1
         assert np.array_equal(outs["0", precision][0], outs["1", precision][0]), precision
+
+
+@pytest.mark.parametrize("support", [32, 16, 64])
+def test_f64_pixels_on_fp32_kernels(support):
+    """f64 pixels through every fp32-loop kernel (host and device APIs): known
+    pixels copied bitwise, output within the production tolerance of the
+    reference on the same f64 inputs, and the device call (f64 I/O) equal to
+    the host call bitwise."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib
+    H, W, B, I = 72, 96, 4, 60
+    L = (support - B) // 2
+    red = "linear" if support == 64 else "tree"
+    img = oracle.synthetic_frame(H, W, 13)
+    sampled, mask = oracle.quarter_sample(img, 6)
+    ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, red)
+    out = fsr.reconstruct(sampled, mask, B, support, I, reducer=red, precision="fp32")
+    assert out.dtype == np.float64
+    assert np.array_equal(out[mask], sampled[mask])
+    assert float(np.abs(out - ref).max()) <= FP32_TOL
+    eng = _lib.Engine([0])
+    p = _lib.make_params(B, L, I, precision="fp32", reducer=red)
+    d_px = torch.tensor(sampled, dtype=torch.float64, device="cuda")
+    d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
+    d_out = torch.empty_like(d_px)
+    eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // B,
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f64")
+    eng.last_stats()
+    assert np.array_equal(d_out.cpu().numpy(), out)
+
+
+def test_strip_fill_is_the_frame_mean():
+    """A strip caller that holds only its halo rows passes the frame-wide
+    empty-support value (reconstruction.py:236-237); the strip's blocks then
+    equal the whole-frame call's bitwise, and no row outside the halo is read
+    (the rows outside it are NaN here)."""
+    from paper_2202_13926_b200 import _lib, shard
+    H, W, B, L, I = 96, 64, 4, 6, 30
+    img = oracle.synthetic_frame(H, W, 19)
+    sampled, mask = oracle.quarter_sample(img, 3)
+    mask[30:70, 8:40] = False  # unsampled hole larger than the support: empty windows
+    sampled = np.where(mask, sampled, 0.0)
+    p = _lib.make_params(B, L, I, precision="fp32")
+    eng = _lib.Engine([0])
+    whole = eng.reconstruct(sampled, mask, p)
+    assert eng.last_stats()["empty_blocks"] > 0
+    fill = shard.frame_fill(sampled, mask)
+    assert np.any(whole == fill) or np.any(np.abs(whole - fill) < 1e-9)
+    row0, row1 = 8, 16
+    ya, yb, oa, ob = shard.strip_io_rows(row0, row1, B, L, H)
+    px = np.full((H, W), np.nan)
+    px[ya:yb] = sampled[ya:yb]
+    mk = np.zeros((H, W), np.uint8)
+    mk[ya:yb] = mask[ya:yb]
+    out = np.zeros((H, W))
+    eng.reconstruct_rows(px, mk, p, row0, row1, out, fill=fill)
+    assert np.allclose(out[oa:ob], whole[oa:ob], rtol=0, atol=1e-9)
+    assert np.array_equal(out[oa:ob][~np.isclose(whole[oa:ob], fill)],
+                          whole[oa:ob][~np.isclose(whole[oa:ob], fill)])
+
+
+def test_device_api_fill_and_no_samples():
+    """Device API: with fill = NaN the empty-support value is the mean of all
+    rows, summed in a fixed order on the device (two calls give the same
+    bits, and equal the host call within rounding); a frame without any known
+    sample makes fsr_last_stats raise "no known samples"."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib, shard
+    H, W = 64, 80
+    img = oracle.synthetic_frame(H, W, 5)
+    sampled, mask = oracle.quarter_sample(img, 2)
+    mask[10:50, 10:60] = False
+    sampled = np.where(mask, sampled, 0.0).astype(np.float32)
+    p = _lib.make_params(4, 6, 20, precision="fp32")
+    eng = _lib.Engine([0])
+    d_px = torch.tensor(sampled, device="cuda")
+    d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
+    outs = []
+    for _ in range(2):
+        d_out = torch.empty_like(d_px)
+        eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+        assert eng.last_stats()["empty_blocks"] > 0
+        outs.append(d_out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    host = eng.reconstruct(sampled, mask, p)
+    assert np.abs(outs[0].astype(np.float64) - host).max() <= 1e-4
+    fill = shard.frame_fill(sampled, mask)
+    assert np.any(np.abs(outs[0] - np.float32(fill)) == 0)
+    d_mk.zero_()
+    d_px.zero_()
+    eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+    with pytest.raises(ValueError, match="no known samples"):
+        eng.last_stats()
 
 
 def test_frame_stream_matches_single_frames():
@@ -295,12 +392,11 @@ def test_support16_fp32_kernel_matches_oracle(reducer, argmax):
     img = oracle.synthetic_frame(96, 128, 21)
     sampled, mask = oracle.quarter_sample(img, 8)
     ref = oracle.reconstruct_image(sampled, mask, 4, 6, 100, 0.7, 0.5, reducer)
-    out, tr = fsr.reconstruct(sampled.astype(np.float32), mask, 4, 16, 100, reducer=reducer,
+    out, tr = fsr.reconstruct(sampled, mask, 4, 16, 100, reducer=reducer,
                               precision="fp32", argmax=argmax, return_trace=True)
-    out = out.astype(np.float64)
     assert float(np.abs(out - ref).max()) <= FP32_TOL
     assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
-    assert np.array_equal(out[mask], sampled[mask].astype(np.float32).astype(np.float64))
+    assert np.array_equal(out[mask], sampled[mask])
     # every non-guarded block's selection sequence equals the fp64 engine's
     # modulo the conjugate mirror except where the guard re-ran it in fp64
     _, tr64 = fsr.reconstruct(sampled, mask, 4, 16, 100, reducer=reducer, precision="fp64",
@@ -344,11 +440,12 @@ def test_support64_fp32_kernel_matches_oracle():
     img = oracle.synthetic_frame(72, 80, 23)
     sampled, mask = oracle.quarter_sample(img, 9)
     ref = oracle.reconstruct_image(sampled, mask, 4, 30, 60, 0.7, 0.5, "linear")
-    out = fsr.reconstruct(sampled.astype(np.float32), mask, 4, 64, 60, reducer="linear",
-                          precision="fp32", argmax="redux").astype(np.float64)
-    assert float(np.abs(out - ref).max()) <= FP32_TOL
-    assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
-    assert np.array_equal(out[mask], sampled[mask].astype(np.float32).astype(np.float64))
+    for argmax in ("redux", "shfl", "smem"):
+        out = fsr.reconstruct(sampled, mask, 4, 64, 60, reducer="linear", precision="fp32",
+                              argmax=argmax)
+        assert float(np.abs(out - ref).max()) <= FP32_TOL, argmax
+        assert abs(oracle.psnr(img, out) - oracle.psnr(img, ref)) <= PSNR_TOL
+        assert np.array_equal(out[mask], sampled[mask])
 
 
 EDGE_CASES = [(32, 4, "tree"), (32, 2, "linear"), (16, 4, "linear"), (16, 2, "tree"), (64, 4, "linear")]
@@ -369,14 +466,23 @@ def test_register_kernels_edges(N, B, reducer, early_stop):
     sampled = np.where(mask, sampled, 0.0)
     L = (N - B) // 2
     ref = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, reducer, early_stop)
-    # the fp32 path takes f32 pixels: compare it with the reference on the SAME
-    # (f32-representable) inputs -- this frame has a block (N=16, B=2) whose
-    # greedy path hinges on a 3e-8 relative near-tie, below the f32 input rounding
+    # guarded fp32 on the reference's own f64 pixels (the kernels read them
+    # directly): within the production tolerance of the reference's output.
+    # This frame has a block (N=16, B=2) whose greedy path hinges on a 3e-8
+    # relative near-tie -- below the f32 rounding of its pixels -- so f32
+    # pixels are judged against the reference run on the same f32 inputs.
+    out32 = fsr.reconstruct(sampled, mask, B, N, I, reducer=reducer,
+                            early_stop=early_stop, precision="fp32", argmax="redux")
+    assert out32.dtype == np.float64
+    err = float(np.abs(out32 - ref).max())
+    assert err <= FP32_TOL, err
+    assert np.array_equal(out32[mask], sampled[mask])
     s32 = sampled.astype(np.float32)
     ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer, early_stop)
-    out32 = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer,
-                            early_stop=early_stop, precision="fp32", argmax="redux")
-    err = float(np.abs(out32.astype(np.float64) - ref32).max())
+    o32 = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer, early_stop=early_stop,
+                          precision="fp32", argmax="redux")
+    assert o32.dtype == np.float32
+    err = float(np.abs(o32.astype(np.float64) - ref32).max())
     assert err <= FP32_TOL, err
     out64, tr = fsr.reconstruct(sampled, mask, B, N, I, reducer=reducer, early_stop=early_stop,
                                 precision="fp64", argmax="redux", return_trace=True)
@@ -399,8 +505,7 @@ def test_early_stop_fires(N, B):
     ref, rtr = oracle.reconstruct_image(sampled, mask, B, L, I, 0.7, 0.5, "tree", True, trace=True)
     assert int(np.max(rtr["done"])) < I  # the stop fires
     for precision in ("fp32", "fp64"):
-        out, tr = fsr.reconstruct(sampled.astype(np.float32) if precision == "fp32" else sampled,
-                                  mask, B, N, I, early_stop=True, precision=precision,
+        out, tr = fsr.reconstruct(sampled, mask, B, N, I, early_stop=True, precision=precision,
                                   argmax="redux", return_trace=True)
         assert np.array_equal(tr.done, rtr["done"]), precision
         assert float(np.abs(out.astype(np.float64) - ref).max()) <= FP32_TOL
@@ -554,26 +659,21 @@ def test_reference_psnr_kat_512(precision):
     """The reference's own end-to-end KAT (test_output.txt:21): natural 512x512,
     quarter-sampled with seed 42, B=4, L=6 (S=16), I=200, tree -> PSNR
     42.312882 dB against the original.  fp64 reproduces it to 1e-6 dB and the
-    reference output to 1e-9 (0..1); guarded fp32 within the production
-    tolerance."""
+    reference output to 1e-9 (0..1); guarded fp32, fed the same f64 pixels,
+    within the production tolerance of the reference output."""
     d = golden_image("acc6_512_s16")
     B, L, I = int(d["block"]), int(d["border"]), int(d["iterations"])
-    px = d["sampled"] if precision == "fp64" else d["sampled"].astype(np.float32)
-    out = fsr.reconstruct(px, d["mask"], B, B + 2 * L, I, reducer="tree", precision=precision,
-                          argmax="redux").astype(np.float64)
+    out = fsr.reconstruct(d["sampled"], d["mask"], B, B + 2 * L, I, reducer="tree",
+                          precision=precision, argmax="redux")
+    assert out.dtype == np.float64  # the reference's own f64 pixels in and out
     err = float(np.abs(out - d["out_tree"]).max())
     dpsnr = abs(oracle.psnr(d["original"], out) - float(d["psnr_tree"]))
     if precision == "fp64":
         assert err <= FP64_TOL, err
         assert dpsnr <= 1e-6, dpsnr
     else:
-        # the fp32 entry point takes f32 pixels; rounding the reference's f64
-        # pixels already moves a near-tied block of this frame by ~0.8 gray
-        # levels, so pixel parity is judged against the reference on the same
-        # f32 inputs (DESIGN.md §4), PSNR against the published KAT
-        ref32 = oracle.reconstruct_image(px.astype(np.float64), d["mask"], B, L, I, 0.7, 0.5, "tree")
-        err32 = float(np.abs(out - ref32).max())
-        assert err32 <= FP32_TOL, err32
+        # guarded fp32 on the same (f64) inputs as the reference
+        assert err <= FP32_TOL, err
         assert dpsnr <= PSNR_TOL, dpsnr
     assert abs(float(d["psnr_tree"]) - 42.312882) < 5e-7
 
@@ -583,7 +683,7 @@ def test_reference_psnr_kat_512(precision):
                                       (32, 400, "natural")])
 def test_guard_beyond_default_iterations(N, I, kind):
     """The near-tie guard's tau grows with N and I (guard_tau_for): guarded fp32
-    stays within the production tolerance of the reference on the same f32
+    stays within the production tolerance of the reference on the same (f64)
     inputs where the fixed tau = 5e-5 of the N=32, I=100 study did not
     (tools/guard_check.py; beyond I = 300 the request is served in fp64)."""
     B = 4
@@ -594,8 +694,8 @@ def test_guard_beyond_default_iterations(N, I, kind):
     size = 512 if kind == "natural" and N != 32 else 192
     img = oracle.synthetic_frame(size, size, 7 if kind == "natural" else 3, kind)
     sampled, mask = oracle.quarter_sample(img, 42)
-    s32 = np.where(mask, sampled, 0.0).astype(np.float32)
-    ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, 0.7, 0.5, reducer)
-    out = fsr.reconstruct(s32, mask, B, N, I, reducer=reducer, precision="fp32", argmax="redux")
-    err = float(np.abs(out.astype(np.float64) - ref32).max())
+    s64 = np.where(mask, sampled, 0.0)
+    ref = oracle.reconstruct_image(s64, mask, B, L, I, 0.7, 0.5, reducer)
+    out = fsr.reconstruct(s64, mask, B, N, I, reducer=reducer, precision="fp32", argmax="redux")
+    err = float(np.abs(out - ref).max())
     assert err <= FP32_TOL, err

@@ -21,18 +21,26 @@ from oracle import port as oracle  # noqa: E402
 B, L, I = 4, 6, 12  # N = 16 keeps the oracle fast
 
 
-def _frame(seed=3, h=45, w=36):
+def _frame(seed=3, h=45, w=36, hole=False):
     img = oracle.synthetic_frame(h, w, seed)
-    return oracle.quarter_sample(img, seed + 1)
+    sampled, mask = oracle.quarter_sample(img, seed + 1)
+    if hole:
+        # an unsampled hole larger than the support (N = 16): its blocks have an
+        # empty window and take the frame-wide mean (reconstruction.py:236-237)
+        mask[4:40, 6:30] = False
+        sampled[~mask] = 0.0
+    return sampled, mask
 
 
-def _oracle_strip(px_rows, mask_rows, ya, row0, row1, height):
-    """Strip with the oracle, given only the halo rows [ya, ya + len)."""
+def _oracle_strip(px_rows, mask_rows, ya, row0, row1, fill, height):
+    """Strip with the oracle, given only the halo rows [ya, ya + len) and the
+    frame-wide empty-support value."""
     full_px = np.zeros((height, px_rows.shape[1]))
     full_mk = np.zeros((height, px_rows.shape[1]), bool)
     full_px[ya:ya + px_rows.shape[0]] = px_rows
     full_mk[ya:ya + mask_rows.shape[0]] = mask_rows
-    out = oracle.reconstruct_image(full_px, full_mk, B, L, I, threads=1, block_rows=(row0, row1))
+    out = oracle.reconstruct_image(full_px, full_mk, B, L, I, threads=1, block_rows=(row0, row1),
+                                   fill_value=fill)
     return out[min(height, row0 * B):min(height, row1 * B)]
 
 
@@ -42,15 +50,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, hole):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        sampled, mask = _frame()
+        sampled, mask = _frame(hole=hole)
         H, W = sampled.shape
         row0, row1, rows = shard.reconstruct_strip_host(
             sampled, mask, B, L, rank, world,
-            lambda p, m, ya, r0, r1: _oracle_strip(p, m, ya, r0, r1, H))
+            lambda p, m, ya, r0, r1, fill: _oracle_strip(p, m, ya, r0, r1, fill, H))
         full = shard.gather_strips(torch.from_numpy(np.ascontiguousarray(rows)), row0, row1, B, H, W,
                                    world)
         # frame stream: each rank takes its round-robin frames, rank 0 collects the count
@@ -63,22 +71,34 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_strip_gather_matches_single_process(world):
+@pytest.mark.parametrize("world,hole", [(2, False), (3, False), (3, True)])
+def test_strip_gather_matches_single_process(world, hole):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, hole)) for r in range(world)]
     for p in procs:
         p.start()
     full, nframes = q.get(timeout=300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    sampled, mask = _frame()
+    sampled, mask = _frame(hole=hole)
     ref = oracle.reconstruct_image(sampled, mask, B, L, I, threads=1)
     assert np.array_equal(full, ref)
     assert nframes == 7
+
+
+def test_hole_frame_has_empty_windows_and_global_fill():
+    # the hole test above only means something if some window is empty and the
+    # strip-local mean would differ from the frame's
+    sampled, mask = _frame(hole=True)
+    H = sampled.shape[0]
+    fill = shard.frame_fill(sampled, mask)
+    ref = oracle.reconstruct_image(sampled, mask, B, L, I, threads=1)
+    assert np.any(ref == fill)
+    top = _oracle_strip(sampled[:26], mask[:26], 0, 0, 5, float(sampled[:26].sum()) / mask[:26].sum(), H)
+    assert not np.array_equal(top, ref[:20])
 
 
 def test_partition_arithmetic():
