@@ -30,7 +30,8 @@
 extern "C" {
 #endif
 
-#define FSR_ABI_VERSION 2  /* 2: f64 pixels on every path, explicit empty-support fill for strips */
+#define FSR_ABI_VERSION 3  /* 2: f64 pixels on every path, explicit empty-support fill for strips;
+                              3: guard_kappa */
 
 typedef enum {
     FSR_OK = 0,
@@ -66,8 +67,12 @@ typedef struct {
     int32_t kernel;      /* N=32 fp64 kernel: 0 auto (= warp pair), 1 one warp per block, 2 warp pair */
     double rho;          /* (0, 1) */
     double gamma;        /* (0, 1] */
-    double guard_tau;    /* fp32 near-tie guard: relative top-2 gap that forces an fp64 re-run;
-                            0 (default) = chosen from N and I */
+    double guard_tau;    /* fp32 near-tie guard, relative term: a block is re-run in fp64 when
+                            some iteration's top-2 objectives satisfy
+                            b1 - b2 <= guard_tau * b1 + guard_kappa * sqrt(b1 * B0)
+                            (B0 = the block's first maximum); 0 (default) = auto */
+    double guard_kappa;  /* fp32 near-tie guard, scale term (the fp32 residual's absolute error
+                            follows B0, not b1); 0 (default) = auto, < 0 = off */
 } fsr_params;
 
 typedef struct fsr_engine fsr_engine;

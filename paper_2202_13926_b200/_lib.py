@@ -37,6 +37,7 @@ class FsrParamsC(ctypes.Structure):
         ("rho", ctypes.c_double),
         ("gamma", ctypes.c_double),
         ("guard_tau", ctypes.c_double),
+        ("guard_kappa", ctypes.c_double),
     ]
 
 
@@ -126,7 +127,7 @@ def _ptr(a):
 
 def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer="tree",
                 early_stop=False, precision="fp64", argmax="redux", guard_tau=0.0,
-                kernel="auto") -> FsrParamsC:
+                kernel="auto", guard_kappa=0.0) -> FsrParamsC:
     p = FsrParamsC()
     load().fsr_params_init(ctypes.byref(p))
     if reducer not in REDUCER:
@@ -142,6 +143,7 @@ def make_params(block=4, border=14, iterations=100, rho=0.7, gamma=0.5, reducer=
         raise ValueError(f"unknown kernel variant {kernel!r}, expected one of {tuple(KERNEL)}")
     p.precision, p.argmax_impl, p.guard_tau = PRECISION[precision], ARGMAX[argmax], float(guard_tau)
     p.kernel = KERNEL[kernel]
+    p.guard_kappa = float(guard_kappa)
     return p
 
 

@@ -55,6 +55,13 @@ struct Tables {
     const Real *cs;     // [2*N] interleaved cos, sin of 2*pi*j/N
 };
 
+// sqrt for the guard's scale term (one MUFU; ~2 ulp is immaterial there).
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

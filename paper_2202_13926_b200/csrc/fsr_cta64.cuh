@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         const int pm_ = a.L + tid / a.B, pn_ = a.L + tid % a.B;
         float acc = 0.f, gr = 0.f, gi = 0.f;
         bool herm = true, flagged = false;
+        float ks = 0.f;  // kappa sqrt(B0) (see warp32)
         int pu = 0, pv = 0, it = 0;
         // one iteration; H: Hermitian phase, run as its own loop (see warp32)
         auto step = [&](auto hconst) -> bool {
@@ -406,7 +407,9 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             pv = bv;
             if (GUARD) {
                 const float b2 = __uint_as_float(second & ~63u);
-                flagged |= b2 >= b1 * one_minus_tau;
+                const float sb1 = sqrt_approx(b1);  // scale term (see warp32)
+                if (H && it == 0) ks = a.kappa * sb1;
+                flagged |= b2 >= fmaf(-ks, sb1, b1 * one_minus_tau);
                 flagged |= b1 * one_minus_tau < thr;
             }
             if (H) herm = ((bu & 31) == 0) && ((bv & 31) == 0);

@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
         int pu = 0, pv = 0;
         int it = 0;
         float fl = -1.f;  // guard test as a float max (see warp32): flagged iff fl >= 0
+        float ks = 0.f;   // kappa sqrt(B0) (see warp32)
         // one iteration; H: Hermitian phase (run as its own loop, see warp32)
         // synthesis deferred by one iteration (see warp32)
         int sidx = 0;
@@ -343,7 +344,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             if (GUARD) {
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));
+                const float sb1 = sqrt_approx(b1);  // scale term (see warp32)
+                if (H && it == 0) ks = a.kappa * sb1;
+                fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
                 if (EARLY) flagged |= b1 * a.omt < thr;
             }
             if (H) herm = ((bu & 7) == 0) && ((bv & 7) == 0);

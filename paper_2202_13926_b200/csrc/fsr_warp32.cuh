@@ -82,6 +82,7 @@ struct Warp32Args {
     int use_tma;           // gather the window with TMA (needs 16 B aligned rows)
     int tma_y0;            // image row of the tensor maps' row 0 (maps span only the rows the call reads)
     float omt;             // 1 - tau in fp32 (a parameter operand rather than a live register)
+    float kappa;           // guard: scale term, near-tie iff b1 - b2 <= tau b1 + kappa sqrt(b1 B0)
 };
 
 // 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
@@ -610,6 +611,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         // the guard's main test accumulated as a float: flagged iff fl >= 0
         // (b2 >= b1 (1 - tau) <=> b2 - b1 (1 - tau) >= 0, exact in float)
         float fl = -1.f;
+        float ks = 0.f;  // kappa sqrt(B0), B0 = the block's first maximum (set at it = 0)
         // One greedy iteration; H: the state is still exactly Hermitian.  The
         // Hermitian phase (a few iterations at most) and the rest run as two
         // loops, so the main loop carries no Hermitian bookkeeping.
@@ -700,7 +702,10 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu,
                                                       ((int)(tid & 31u) == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));  // no FMA contraction: same test
+                // near-tie iff b2 >= b1 (1 - tau) - ks sqrt(b1), ks = kappa sqrt(B0)
+                const float sb1 = sqrt_approx(b1);
+                if (H && it == 0) ks = a.kappa * sb1;
+                fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
                 // a continue decision within tau of the stop threshold is ambiguous too
                 if (EARLY) flagged |= b1 * a.omt < thr;
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)

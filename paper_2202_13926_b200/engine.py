@@ -34,15 +34,26 @@ from .spectra import WeightSet
 REDUCERS = ("tree", "linear")
 EARLY_STOP_RELATIVE = 1e-12
 DEFAULT_GUARD_TAU = 0.0  # 0: chosen by the engine from N and I (fsr.h)
+DEFAULT_GUARD_KAPPA = 0.0  # 0: the engine's default scale term (fsr.h)
 
 
 def effective_guard_tau(support: int, iterations: int, guard_tau: float = DEFAULT_GUARD_TAU) -> float:
-    """The near-tie guard's tau as the engine applies it (fsr_abi.cu guard_tau_for):
-    an explicit tau > 0 as given, else 5e-5 * k_N * max(1, I/100)^1.25, k_N = 2 for N=64."""
+    """The near-tie guard's relative term as the engine applies it (fsr_abi.cu
+    guard_tau_for): an explicit tau > 0 as given, else 5e-5 (1e-4 for N=64)."""
     if guard_tau > 0.0:
         return float(guard_tau)
-    kn = 2.0 if support >= 64 else 1.0
-    return min(0.25, 5e-5 * kn * max(1.0, iterations / 100.0) ** 1.25)
+    return 1e-4 if support >= 64 else 5e-5
+
+
+def effective_guard_kappa(iterations: int, guard_kappa: float = DEFAULT_GUARD_KAPPA) -> float:
+    """The guard's scale term (fsr_abi.cu guard_kappa_for): a block is re-run in
+    fp64 when b1 - b2 <= tau b1 + kappa sqrt(b1 B0) at some iteration; explicit
+    kappa > 0 as given, < 0 off, else 1e-7 * max(0, I/100 - 1)."""
+    if guard_kappa > 0.0:
+        return float(guard_kappa)
+    if guard_kappa < 0.0:
+        return 0.0
+    return 1e-7 * max(0.0, iterations / 100.0 - 1.0)
 
 
 def _check_reducer(reducer: str) -> bool:
@@ -64,7 +75,7 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
                 rho: float = 0.7, gamma: float = 0.5, *, reducer: str = "tree",
                 early_stop: bool = False, precision: str = "fp64", devices=None,
                 argmax: str = "redux", guard_tau: float = DEFAULT_GUARD_TAU,
-                return_trace: bool = False):
+                guard_kappa: float = DEFAULT_GUARD_KAPPA, return_trace: bool = False):
     """Reconstruct the unknown pixels of ``image`` (0..255 scale) given ``mask``.
 
     ``support`` is the FFT size N = block + 2*border; N - block must be even
@@ -93,7 +104,7 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
     img = np.ascontiguousarray(img, dtype=io)
     m = np.ascontiguousarray(m, dtype=bool)
     params = _lib.make_params(block, border, iterations, rho, gamma, reducer, early_stop,
-                              precision, argmax, guard_tau)
+                              precision, argmax, guard_tau, guard_kappa=guard_kappa)
     eng = _lib.default_engine(devices)
     sel = done = None
     if return_trace:

@@ -638,7 +638,7 @@ def test_full_size_properties(H, W, N, reducer):
                            d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
     st = eng.last_stats()
     out = d_out.cpu().numpy()
-    assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.2  # tau grows with N (guard_tau_for)
+    assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.2  # tau doubles at N=64 (guard_tau_for)
     strips = np.zeros_like(px)
     c1, c2 = brows // 3, 2 * brows // 3 + 7  # uneven strips
     for r0, r1 in ((0, c1), (c1, c2), (c2, brows)):
@@ -682,10 +682,11 @@ def test_reference_psnr_kat_512(precision):
                                       (64, 100, "natural"), (64, 200, "uniform"),
                                       (32, 400, "natural")])
 def test_guard_beyond_default_iterations(N, I, kind):
-    """The near-tie guard's tau grows with N and I (guard_tau_for): guarded fp32
-    stays within the production tolerance of the reference on the same (f64)
-    inputs where the fixed tau = 5e-5 of the N=32, I=100 study did not
-    (tools/guard_check.py; beyond I = 300 the request is served in fp64)."""
+    """Beyond the default 100 iterations the guard's scale term kappa sqrt(b1 B0)
+    switches on (guard_kappa_for): guarded fp32 stays within the production
+    tolerance of the reference on the same (f64) inputs where a relative tau
+    alone did not (tools/flip_errors.py; beyond I = 300 the request is served
+    in fp64)."""
     B = 4
     L = (N - B) // 2
     reducer = "linear" if N == 64 else "tree"

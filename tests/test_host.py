@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(L, name), name
     assert set(names) == set(_lib.EXPORTED)
-    assert L.fsr_abi_version() == 2
+    assert L.fsr_abi_version() == 3
 
 
 def test_params_validation_messages():
