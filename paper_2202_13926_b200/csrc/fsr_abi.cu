@@ -670,7 +670,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         const uint8_t *tmk = mask + ty0 * mask_pitch;
         const bool tree = p->reducer == FSR_REDUCER_TREE;
         // trace / early-stop code only in the launches that need it
-        const int opts = (sel ? LOPT_TRACE : 0) | (p->early_stop ? LOPT_EARLY : 0);
+        const int opts = (sel ? LOPT_TRACE : 0) | (p->early_stop ? LOPT_EARLY : 0) |
+                         (guarded && a.kappa > 0.f ? LOPT_KAPPA : 0);
         const int nsup = fast64 ? 64 : fast16 ? 16 : 32;
         a.use_tma = (d.tma_enabled &&
                      window_maps<IO>(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps, nsup)) ? 1 : 0;

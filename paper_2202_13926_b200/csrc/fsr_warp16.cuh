@@ -223,6 +223,7 @@ template <typename IO, int WARPS, bool TREE, int ARGMAX, bool GUARD, int OPTS = 
 __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
     warp16_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
+    constexpr bool KAPPA = (OPTS & W32_KAPPA) != 0;
     // lane order as in warp32: tie-rank order only where the kernel breaks exact
     // ties itself; guarded, every near-tie is re-run in fp64, so natural order
     // (no bit reversals in the argmax tail) and any maximal lane may win
@@ -344,9 +345,13 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             if (GUARD) {
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
-                const float sb1 = sqrt_approx(b1);  // scale term (see warp32)
-                if (H && it == 0) ks = a.kappa * sb1;
-                fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                if (KAPPA) {  // scale term (see warp32)
+                    const float sb1 = sqrt_approx(b1);
+                    if (H && it == 0) ks = a.kappa * sb1;
+                    fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                } else {
+                    fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));
+                }
                 if (EARLY) flagged |= b1 * a.omt < thr;
             }
             if (H) herm = ((bu & 7) == 0) && ((bv & 7) == 0);

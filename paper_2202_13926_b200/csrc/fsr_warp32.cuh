@@ -514,9 +514,10 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 }
 
 // STUDY: record per-block minimum top-2 gaps (tools/guard_study.py only).
-// OPTS: W32_TRACE compiles the selection trace in, W32_EARLY the early stop;
-// production launches without them carry no per-iteration checks for either.
-constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_ALL = 3;
+// OPTS: W32_TRACE compiles the selection trace in, W32_EARLY the early stop,
+// W32_KAPPA the guard's scale term; production launches without them carry no
+// per-iteration work for either (the scale term's sqrt costs ~1 % of the loop).
+constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_KAPPA = 4, W32_ALL = 7;
 
 #ifndef FSR_W32_WARPS_PER_SM
 #define FSR_W32_WARPS_PER_SM 12  // resident warps (blocks) per SM the register budget targets
@@ -525,6 +526,7 @@ template <typename IO, int WARPS, bool TREE, int ARGMAX, bool GUARD, bool STUDY,
 __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
+    constexpr bool KAPPA = (OPTS & W32_KAPPA) != 0;
     // pair keys (one key per row pair, half resolved after the argmax): exact ties
     // between bins are ordered differently than the reference, so only where the
     // guard re-runs every near-tie in fp64 anyway
@@ -703,9 +705,13 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                                                       ((int)(tid & 31u) == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 // near-tie iff b2 >= b1 (1 - tau) - ks sqrt(b1), ks = kappa sqrt(B0)
-                const float sb1 = sqrt_approx(b1);
-                if (H && it == 0) ks = a.kappa * sb1;
-                fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                if (KAPPA) {
+                    const float sb1 = sqrt_approx(b1);
+                    if (H && it == 0) ks = a.kappa * sb1;
+                    fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                } else {
+                    fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));  // no FMA contraction: same test
+                }
                 // a continue decision within tau of the stop threshold is ambiguous too
                 if (EARLY) flagged |= b1 * a.omt < thr;
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)

@@ -35,6 +35,8 @@ cudaError_t warp16_launch(const Warp32Args &a, const Warp32Maps &maps, bool tree
         if (tree) return guard ? go<IO, AM, true, true, 0>(a, maps, sms, st) : go<IO, AM, true, false, 0>(a, maps, sms, st);
         return guard ? go<IO, AM, false, true, 0>(a, maps, sms, st) : go<IO, AM, false, false, 0>(a, maps, sms, st);
     }
+    if (opts == LOPT_KAPPA && guard)
+        return tree ? go<IO, AM, true, true, W32_KAPPA>(a, maps, sms, st) : go<IO, AM, false, true, W32_KAPPA>(a, maps, sms, st);
     if (tree) return guard ? go<IO, AM, true, true, W32_ALL>(a, maps, sms, st) : go<IO, AM, true, false, W32_ALL>(a, maps, sms, st);
     return guard ? go<IO, AM, false, true, W32_ALL>(a, maps, sms, st) : go<IO, AM, false, false, W32_ALL>(a, maps, sms, st);
 }

@@ -36,6 +36,8 @@ cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_
 template <typename IO, int AM, bool TREE, bool GUARD>
 cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, int opts, int sms, cudaStream_t st) {
     if (opts == 0) return go<IO, AM, TREE, GUARD, false, 0>(a, maps, sms, st);
+    if constexpr (GUARD)
+        if (opts == LOPT_KAPPA) return go<IO, AM, TREE, GUARD, false, LOPT_KAPPA>(a, maps, sms, st);
     if constexpr (AM == AM_REDUX) {
         if (opts == LOPT_TRACE) return go<IO, AM, TREE, GUARD, false, LOPT_TRACE>(a, maps, sms, st);
         if (opts == LOPT_EARLY) return go<IO, AM, TREE, GUARD, false, LOPT_EARLY>(a, maps, sms, st);
