@@ -24,6 +24,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -836,10 +837,18 @@ int read_call_stats(fsr_engine *eng, Device &d, CallCtr &call, int64_t &reruns, 
     ms = 0.f;
     main_ms = 0.f;
     if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
+    static const bool trace = std::getenv("FSR_CHUNK_TRACE") != nullptr;  // pipeline timeline (stderr)
     for (int c = 0; c < d.last_chunks; ++c) {  // the chunks' main-kernel brackets
         float t = 0.f;
         if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) main_ms += t;
+        if (trace) {
+            float t0 = 0.f, t1 = 0.f;
+            cudaEventElapsedTime(&t0, d.ev0, d.ck0[c]);
+            cudaEventElapsedTime(&t1, d.ev0, d.ck1[c]);
+            fprintf(stderr, "chunk %2d: main kernel %7.3f .. %7.3f ms\n", c, t0, t1);
+        }
     }
+    if (trace) fprintf(stderr, "call: %.3f ms\n", ms);
     (void)cudaGetLastError();
     CUDA_TRY(eng, cudaMemcpy(&call, d.call_ctr.p, sizeof(CallCtr), cudaMemcpyDeviceToHost));
     std::vector<ChunkCtr> cc(std::max(d.last_chunks, 1));
@@ -929,8 +938,14 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         ld.gap_debug = d.gap_debug;
         CUDA_TRY(eng, cudaStreamWaitEvent(ld.stream, d.ev0, 0));
     }
-    auto drain = [&](Device &ld) -> int {  // the lane's finished chunk -> caller's buffer
-        if (!ld.pending) return FSR_OK;
+    // Finished chunks are copied to the caller's buffer in chunk (= completion)
+    // order: the persistent grids of the lanes' kernels run nearly one after the
+    // other, so chunk c's copy-out overlaps chunks c+1.. on the GPU and only the
+    // last chunk's is exposed.
+    std::deque<Device *> fifo;  // lanes with a pending chunk, oldest first
+    auto drain_one = [&]() -> int {  // the oldest pending chunk -> caller's buffer
+        Device &ld = *fifo.front();
+        fifo.pop_front();
         CUDA_TRY(eng, cudaEventSynchronize(ld.ev1));
         pool_copy(d.pool.get(), out + ld.pend_oa * W, ld.hout.p, ld.pend_ob - ld.pend_oa,
                   (size_t)W * sizeof(IO));
@@ -939,7 +954,8 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
     };
     for (int c = 0; c < K; ++c) {
         Device &ld = *d.lanes[c % kLanes];
-        if ((rc = drain(ld))) return rc;
+        while (ld.pending)
+            if ((rc = drain_one())) return rc;
         int64_t r0, r1;
         chunk_rows(hp.row0, hp.row1, c, K, r0, r1);
         const int64_t ya = std::max<int64_t>(0, r0 * B - L), yb = std::min<int64_t>(H, r1 * B + L);
@@ -981,11 +997,13 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         ld.pending = true;
         ld.pend_oa = oa;
         ld.pend_ob = ob;
+        fifo.push_back(&ld);
         d.used_tma = ld.used_tma;
     }
+    while (!fifo.empty())
+        if ((rc = drain_one())) return rc;
     for (int l = 0; l < nl; ++l) {
         Device &ld = *d.lanes[l];
-        if ((rc = drain(ld))) return rc;
         d.launches += ld.launches;
         CUDA_TRY(eng, cudaStreamWaitEvent(d.stream, ld.ev1, 0));
     }
