@@ -276,7 +276,9 @@ class Engine:
         in a frame without any known sample."""
         s = FsrStatsC()
         self._check(self._L.fsr_last_stats(self._h, ctypes.byref(s)))
-        return {f: getattr(s, f) for f, _ in FsrStatsC._fields_ if f != "reserved"}
+        d = {f: getattr(s, f) for f, _ in FsrStatsC._fields_ if f != "reserved"}
+        d["served_fp64"] = bool(s.flags & 2)  # FSR_STATS_SERVED_FP64
+        return d
 
 
 _default = {}

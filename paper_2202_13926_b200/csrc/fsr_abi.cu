@@ -195,6 +195,7 @@ struct Device {
     bool tma_enabled = true;     // window gather by TMA when the rows allow it
     bool chunking = true;        // large calls in row chunks over kLanes streams (FSR_NO_CHUNK=1: off)
     int used_tma = 0;            // last fp32-loop launch gathered by TMA
+    int served_fp64 = 0;         // last launch: a guarded fp32 request served by the fp64 kernels
     // Calls run as K row chunks over kLanes "lanes" (same GPU, own stream, staging
     // buffers and re-run scratch): one chunk's copies, fp64 re-run and launch
     // tail overlap the other chunks' main kernels.
@@ -400,6 +401,13 @@ int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tre
 }
 
 template <typename IO>
+int launch_warpnd(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int N, int am,
+                  int64_t want_blocks, cudaStream_t st) {
+    LAUNCH_TRY(eng, d, (warpnd_launch<IO>(a, N, am, want_blocks, d.sms, st)));
+    return FSR_OK;
+}
+
+template <typename IO>
 int launch_cta64d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int64_t want_blocks,
                   cudaStream_t st) {
     int grid = 1;
@@ -424,6 +432,7 @@ Pair64Args<IO> pair64_args(const fsr_params *p, const IO *px, int64_t px_pitch, 
     a.bcols = bcols; a.first = first; a.nblocks = nblocks; a.list = nullptr; a.list_count = nullptr;
     a.gamma = p->gamma; a.decay = tab.decay; a.wf = tab.wf; a.sel = sel; a.done = done;
     a.empty_count = empty_count; a.empty_list = empty_list;
+    a.tree = p->reducer == FSR_REDUCER_TREE;
     return a;
 }
 
@@ -432,6 +441,7 @@ bool pair64_eligible(const fsr_params *p) {
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+// (declared early: warpn launchers below)
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -453,7 +463,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 template <typename IO>
 bool window_maps(const IO *px, int64_t px_pitch, const uint8_t *mask, int64_t mask_pitch,
                  int64_t H, int64_t W, Warp32Maps *m, int N) {
-    const int box_px = N + 16 / (int)sizeof(IO), box_mk = N + 16, box_rows = N;
+    const int box_px = N + 16 / (int)sizeof(IO), box_mk = (N + 30) / 16 * 16, box_rows = N;
     if ((reinterpret_cast<uintptr_t>(px) & 15) || ((px_pitch * (int64_t)sizeof(IO)) & 15) ||
         (reinterpret_cast<uintptr_t>(mask) & 15) || (mask_pitch & 15) || H < 1 || W < 1 ||
         H > (int64_t)INT32_MAX || W > (int64_t)INT32_MAX)
@@ -486,6 +496,13 @@ bool cta64d_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 64 && p->block * p->block <= C64_THREADS &&
            p->reducer == FSR_REDUCER_LINEAR;
 }
+
+// the paper grid's other supports (fsr_warpn.cuh): one warp per block, N in {4, 8, 24}
+bool warpn_support(int N) { return N == 4 || N == 8 || N == 24; }
+bool warpnd_eligible(const fsr_params *p) {
+    return warpn_support(p->block + 2 * p->border) && p->block * p->block <= 32;
+}
+bool warpn_eligible(const fsr_params *p) { return warpnd_eligible(p) && p->precision != FSR_PREC_FP64; }
 
 bool warp16d_eligible(const fsr_params *p) {
     return p->block + 2 * p->border == 16 && p->block * p->block <= 32;
@@ -546,8 +563,12 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     // Beyond ~300 iterations the guard re-runs most blocks (tau grows with I,
     // tools/guard_check.py: 90-99 % at I = 500), so the guarded fp32 request is
     // served by the fp64 kernels directly -- faster, and exact.
+    const fsr_params *p_req = p;
     fsr_params pl = *p;
     if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
+    // N = 4 (L = 0 at B = 4: the window is the block) flags ~40 % of the blocks
+    // and its fp64 kernel is faster than fp32 + re-runs (1080p: 378 vs 349 fps)
+    if (pl.precision == FSR_PREC_FP32 && N == 4) pl.precision = FSR_PREC_FP64;
     p = &pl;
     CUDA_TRY(eng, cudaMemsetAsync(cc, 0, sizeof(ChunkCtr), st));
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
@@ -560,7 +581,10 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     const bool fast32 = warp32_eligible(p);
     const bool fast16 = warp16_eligible(p);
     const bool fast64 = cta64_eligible(p);
-    if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16 || fast64)) {
+    const bool fastn = warpn_eligible(p);
+    d.served_fp64 = p_req->precision == FSR_PREC_FP32 &&
+                    (p->precision == FSR_PREC_FP64 || !(fast32 || fast16 || fast64 || fastn));
+    if (p->precision == FSR_PREC_FP64 || !(fast32 || fast16 || fast64 || fastn)) {
         if (p->precision == FSR_PREC_FP64 && pair64_eligible(p)) {
             Tables<double> tab;
             if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
@@ -586,6 +610,14 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                W, bcols, first, nblocks, tab, sel, done,
                                                &call->empty_count, empty_list);
             if ((rc = launch_cta64d<IO>(eng, d, a, nblocks, st))) return rc;
+            CUDA_TRY(eng, cudaEventRecord(ev_end, st));
+        } else if (p->precision == FSR_PREC_FP64 && warpnd_eligible(p)) {
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> a = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, first, nblocks, tab, sel, done,
+                                               &call->empty_count, empty_list);
+            if ((rc = launch_warpnd<IO>(eng, d, a, N, p->argmax_impl, nblocks, st))) return rc;
             CUDA_TRY(eng, cudaEventRecord(ev_end, st));
         } else if (p->precision == FSR_PREC_FP64) {
             Tables<double> tab;
@@ -648,6 +680,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.tau = (float)guard_tau_for(p);
         a.omt = 1.f - a.tau;
         a.kappa = (float)guard_kappa_for(p);
+        a.tree = p->reducer == FSR_REDUCER_TREE;
         a.wf = tf.wf;
         a.sel = sel;
         a.done = done;
@@ -673,7 +706,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         // trace / early-stop code only in the launches that need it
         const int opts = (sel ? LOPT_TRACE : 0) | (p->early_stop ? LOPT_EARLY : 0) |
                          (guarded && a.kappa > 0.f ? LOPT_KAPPA : 0);
-        const int nsup = fast64 ? 64 : fast16 ? 16 : 32;
+        const int nsup = fast64 ? 64 : fast16 ? 16 : fastn ? N : 32;
         a.use_tma = (d.tma_enabled &&
                      window_maps<IO>(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps, nsup)) ? 1 : 0;
         d.used_tma = a.use_tma;
@@ -682,6 +715,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, d.sms, st)));
         } else if (fast16) {
             LAUNCH_TRY(eng, d, (warp16_any<IO>(a, maps, tree, p->argmax_impl, guarded, opts, d.sms, st)));
+        } else if (fastn) {
+            LAUNCH_TRY(eng, d, (warpn_any<IO>(a, maps, N, p->argmax_impl, guarded, opts, d.sms, st)));
         } else {
             const bool study = d.gap_debug != nullptr;
             if (study && p->argmax_impl != FSR_ARGMAX_REDUX)
@@ -700,6 +735,16 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &cc->rerun_count;
             if ((rc = launch_cta64d<IO>(eng, d, r, (int64_t)d.sms, st))) return rc;
+        } else if (guarded && fastn) {
+            // fp64 re-run of ambiguous blocks on the fp64 one-warp kernel (list mode)
+            Tables<double> tab;
+            if ((rc = get_tables<double>(eng, d, N, p->rho, tab))) return rc;
+            Pair64Args<IO> r = pair64_args<IO>(p, px, px_pitch, mask, mask_pitch, out, out_pitch, H,
+                                               W, bcols, 0, 0, tab, sel, done,
+                                               &cc->skip_empty /* empties already counted */, nullptr);
+            r.list = d.rerun_list.as<int32_t>();
+            r.list_count = &cc->rerun_count;
+            if ((rc = launch_warpnd<IO>(eng, d, r, N, p->argmax_impl, (int64_t)d.sms * 16, st))) return rc;
         } else if (guarded && fast16) {
             // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)
             Tables<double> tab;
@@ -886,6 +931,7 @@ int device_call(fsr_engine *eng, Device &d, const fsr_params *p, const IO *d_px,
                                call, d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
         if (rc) return rc;
         d.used_tma = ld.used_tma;
+        d.served_fp64 = ld.served_fp64;
     }
     for (int l = 0; l < nl; ++l) {
         Device &ld = *d.lanes[l];
@@ -999,6 +1045,7 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         ld.pend_ob = ob;
         fifo.push_back(&ld);
         d.used_tma = ld.used_tma;
+        d.served_fp64 = ld.served_fp64;
     }
     while (!fifo.empty())
         if ((rc = drain_one())) return rc;
@@ -1070,7 +1117,8 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
         eng->stats.rerun_blocks += hp.reruns;
         eng->stats.kernel_launches += eng->devs[g]->launches;
         if (g == 0) {
-            eng->stats.flags = eng->devs[0]->used_tma ? FSR_STATS_TMA_GATHER : 0;
+            eng->stats.flags = (eng->devs[0]->used_tma ? FSR_STATS_TMA_GATHER : 0) |
+                               (eng->devs[0]->served_fp64 ? FSR_STATS_SERVED_FP64 : 0);
             eng->stats.kernel_ms = hp.ms;
             eng->stats.main_ms = hp.main_ms;
         }
@@ -1119,7 +1167,7 @@ int reconstruct_device(fsr_engine *eng, const fsr_params *p, const IO *d_px, int
     eng->stats = fsr_stats{};
     eng->stats.blocks = (row1 - row0) * ((width + p->block - 1) / p->block);
     eng->stats.kernel_launches = d.launches;
-    eng->stats.flags = d.used_tma ? FSR_STATS_TMA_GATHER : 0;
+    eng->stats.flags = (d.used_tma ? FSR_STATS_TMA_GATHER : 0) | (d.served_fp64 ? FSR_STATS_SERVED_FP64 : 0);
     eng->device_stats_pending = rc == FSR_OK;
     return rc;
 }

@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const IO *spx = reinterpret_cast<const IO *>(sm.region);
             const uint8_t *smk = sm.region + Box::STAGE_MK;
             if (wid == 0)
-                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::STAGE_BYTES);
+                tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::TX_BYTES);
             mbar_wait(bar, phase);
             phase ^= 1u;
             const IO *cpx = spx + 32 * h * Box::PX + (x0 - xp) + v;

@@ -51,6 +51,21 @@ template <typename IO>
 cudaError_t cta64d_grid(int64_t want_blocks, int sms, int *grid);
 template <typename IO>
 cudaError_t cta64d_launch(const Pair64Args<IO> &a, int grid, cudaStream_t st);
+// N in {4, 8, 24} (fsr_warpn.cuh): fp32 loop (reducer in a.tree) and fp64
+template <typename IO, int N>
+cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
+                         int sms, cudaStream_t st);
+template <typename IO>
+cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want_blocks, int sms,
+                          cudaStream_t st);
+template <typename IO>
+inline cudaError_t warpn_any(const Warp32Args &a, const Warp32Maps &m, int N, int am, bool guard,
+                             int opts, int sms, cudaStream_t st) {
+    if (N == 4) return warpn_launch<IO, 4>(a, m, am, guard, opts, sms, st);
+    if (N == 8) return warpn_launch<IO, 8>(a, m, am, guard, opts, sms, st);
+    if (N == 24) return warpn_launch<IO, 24>(a, m, am, guard, opts, sms, st);
+    return kNotBuilt;
+}
 // any support <= 64, strict IEEE (fsr_generic.cuh)
 template <typename Real, typename IO>
 cudaError_t generic_launch(const ImageArgs<Real, IO> &a, int grid, cudaStream_t st);

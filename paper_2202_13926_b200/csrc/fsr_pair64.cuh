@@ -58,6 +58,7 @@ struct Pair64Args {
     unsigned int *empty_count;
     int32_t *empty_list;
     double2 *scratch;               // cta64d: per-CTA 64 KiB staging of W (null elsewhere)
+    int tree;                       // reducer for kernels that take it at run time (warpnd)
 };
 
 struct __align__(16) PairSlot {

@@ -125,7 +125,7 @@ __device__ __forceinline__ double w16_prologue(const Warp32Args &a, const Warp32
         const int xp = x0 & ~(Box::ALIGN - 1), xm = x0 & ~15;
         const IO *spx = reinterpret_cast<const IO *>(ub);
         const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + Box::STAGE_MK;
-        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::STAGE_BYTES);
+        tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0, Box::TX_BYTES);
         mbar_wait(bar, phase);
         phase ^= 1u;
         const IO *cpx = spx + rh * 8 * Box::PX + (x0 - xp) + cl;

@@ -83,6 +83,7 @@ struct Warp32Args {
     int tma_y0;            // image row of the tensor maps' row 0 (maps span only the rows the call reads)
     float omt;             // 1 - tau in fp32 (a parameter operand rather than a live register)
     float kappa;           // guard: scale term, near-tie iff b1 - b2 <= tau b1 + kappa sqrt(b1 B0)
+    int tree;              // reducer (tree 1 / linear 0) for kernels that take it at run time (warpn)
 };
 
 // 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
@@ -99,9 +100,10 @@ template <typename IO, int ROWS, int N>
 struct TmaBox {
     static constexpr int ALIGN = 16 / (int)sizeof(IO);             // pixels per 16 bytes
     static constexpr int PX = N + ALIGN;                           // pixel box columns
-    static constexpr int MK = N + 16;                              // mask box columns
-    static constexpr int STAGE_MK = ROWS * PX * (int)sizeof(IO);   // mask staging offset (bytes)
-    static constexpr int STAGE_BYTES = STAGE_MK + ROWS * MK;
+    static constexpr int MK = (N + 15 + 15) / 16 * 16;             // mask box columns (16 B multiple)
+    static constexpr int STAGE_MK = (ROWS * PX * (int)sizeof(IO) + 127) / 128 * 128;  // mask staging offset
+    static constexpr int STAGE_BYTES = STAGE_MK + ROWS * MK;       // staging footprint
+    static constexpr int TX_BYTES = ROWS * PX * (int)sizeof(IO) + ROWS * MK;  // bytes the two boxes deliver
     static_assert(STAGE_MK % 128 == 0, "TMA destinations must be 128-byte aligned");
 };
 constexpr int W32_BOX_PX = TmaBox<float, 32, 32>::PX, W32_BOX_MK = TmaBox<float, 32, 32>::MK;
@@ -118,8 +120,9 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
+    uint32_t done = 0, spins = 0;
     while (!done) {
+        if (++spins > (1u << 24)) __trap();  // a TMA that never lands: fail loudly, never hang
         asm volatile(
             "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
             " selp.u32 %0, 1, 0, p;\n}"
@@ -393,7 +396,7 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
         const IO *spx = reinterpret_cast<const IO *>(ub);
         const uint8_t *smk = reinterpret_cast<const uint8_t *>(ub) + Box::STAGE_MK;
         tma_window(maps, bar, smem_u32(spx), smem_u32(smk), xp, xm, (int)wr0 - a.tma_y0,
-                   Box::STAGE_BYTES);
+                   Box::TX_BYTES);
         mbar_wait(bar, phase);
         phase ^= 1u;
         const IO *cpx = spx + (x0 - xp) + lane;

@@ -1,0 +1,51 @@
+// k_warpn.cu -- instantiations of the fp32 loop kernel for the paper grid's
+// other supports (fsr_warpn.cuh) for pixel type FSR_IO and support FSR_N (one
+// object per pair): every argmax variant, production (OPTS = 0, + the guard's
+// scale term) and the full build (trace + early stop).
+#include "fsr_launch.cuh"
+#include "fsr_warpn.cuh"
+
+#ifndef FSR_IO
+#define FSR_IO float
+#endif
+#ifndef FSR_N
+#define FSR_N 24
+#endif
+
+namespace fsr {
+
+namespace {
+template <typename IO, int N, int AM, bool GUARD, int OPTS>
+cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_t st) {
+    constexpr int WARPS = 4;
+    auto k = warpn_kernel<IO, N, WARPS, AM, GUARD, OPTS>;
+    const size_t smem = sizeof(WarpNSmem<N, WARPS>);
+    int grid = 1;
+    cudaError_t e = persistent_grid(k, WARPS * 32, smem, (a.nblocks + WARPS - 1) / WARPS, sms, &grid);
+    if (e != cudaSuccess) return e;
+    k<<<grid, WARPS * 32, smem, st>>>(a, maps);
+    return cudaGetLastError();
+}
+
+template <typename IO, int N, int AM>
+cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, bool guard, int opts, int sms,
+                    cudaStream_t st) {
+    if (opts == 0) return guard ? go<IO, N, AM, true, 0>(a, maps, sms, st) : go<IO, N, AM, false, 0>(a, maps, sms, st);
+    if (opts == LOPT_KAPPA && guard) return go<IO, N, AM, true, W32_KAPPA>(a, maps, sms, st);
+    return guard ? go<IO, N, AM, true, W32_ALL>(a, maps, sms, st) : go<IO, N, AM, false, W32_ALL>(a, maps, sms, st);
+}
+}  // namespace
+
+template <typename IO, int N>
+cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
+                         int sms, cudaStream_t st) {
+    if (am == AM_SHFL) return by_opts<IO, N, AM_SHFL>(a, maps, guard, opts, sms, st);
+    if (am == AM_SMEM) return by_opts<IO, N, AM_SMEM>(a, maps, guard, opts, sms, st);
+    if (am == AM_REDUX) return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
+    return kNotBuilt;
+}
+
+template cudaError_t warpn_launch<FSR_IO, FSR_N>(const Warp32Args &, const Warp32Maps &, int, bool,
+                                                 int, int, cudaStream_t);
+
+}  // namespace fsr

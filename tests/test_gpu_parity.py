@@ -448,13 +448,16 @@ def test_support64_fp32_kernel_matches_oracle():
         assert np.array_equal(out[mask], sampled[mask])
 
 
-EDGE_CASES = [(32, 4, "tree"), (32, 2, "linear"), (16, 4, "linear"), (16, 2, "tree"), (64, 4, "linear")]
+EDGE_CASES = [(32, 4, "tree"), (32, 2, "linear"), (16, 4, "linear"), (16, 2, "tree"), (64, 4, "linear"),
+              # the paper grid's other supports, fsr_warpn.cuh
+              (24, 4, "tree"), (24, 2, "linear"), (8, 4, "tree"), (8, 2, "linear"), (4, 4, "tree"),
+              (4, 2, "linear")]
 
 
 @pytest.mark.parametrize("early_stop", [False, True])
 @pytest.mark.parametrize("N,B,reducer", EDGE_CASES)
 def test_register_kernels_edges(N, B, reducer, early_stop):
-    """Every register kernel (warp32, warp16/warp16d, cta64) on a frame whose
+    """Every register kernel (warp32, warp16/warp16d, cta64, warpn/warpnd) on a frame whose
     height is not a multiple of B (truncated bottom target blocks), whose
     width is 16-aligned (TMA gather on) and which has a 26x26 unsampled hole
     (empty-support windows for N=16 -> mean fill, reconstruction.py:272-275),
@@ -700,3 +703,15 @@ def test_guard_beyond_default_iterations(N, I, kind):
     out = fsr.reconstruct(s64, mask, B, N, I, reducer=reducer, precision="fp32", argmax="redux")
     err = float(np.abs(out - ref).max())
     assert err <= FP32_TOL, err
+
+
+@pytest.mark.parametrize("N,B,I,served", [(24, 4, 60, False), (8, 4, 60, False), (16, 4, 60, False),
+                                          (32, 4, 400, True), (4, 4, 60, True), (12, 4, 60, True)])
+def test_guarded_fp32_reports_fp64_service(N, B, I, served):
+    """A guarded fp32 request is served by the fp64 kernels beyond 300 iterations,
+    at N = 4 and for supports without an fp32 register kernel; the call's stats
+    say so (FSR_STATS_SERVED_FP64), so a bench line never labels fp64 work fp32."""
+    img = oracle.synthetic_frame(40, 48, 5)
+    sampled, mask = oracle.quarter_sample(img, 3)
+    _, tr = fsr.reconstruct(sampled, mask, B, N, I, precision="fp32", return_trace=True)
+    assert tr.stats["served_fp64"] is served
