@@ -119,3 +119,28 @@ def test_missing_library_fails_loudly(tmp_path):
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=300)
     assert "raised True" in out.stdout, out.stdout + out.stderr
+
+
+def test_output_pool_never_recycles_live_memory():
+    """Host-buffer calls return new arrays on recycled memory (no first-touch
+    faults per call); memory returns to the pool only after the array AND every
+    view of it are gone."""
+    import gc
+
+    from paper_2202_13926_b200 import _lib
+
+    pool = _lib._OutputPool()
+    a = np.frombuffer(_lib._Lease(pool.take(160), pool), dtype=np.float64).reshape(4, 5)
+    a[:] = 7.0
+    view = a[1:3, 2:]
+    del a
+    gc.collect()
+    assert pool._cached == 0  # the view still holds the lease
+    b = np.frombuffer(_lib._Lease(pool.take(160), pool), dtype=np.float64).reshape(4, 5)
+    b[:] = -1.0
+    assert np.all(view == 7.0)  # b did not get the live view's memory
+    del view, b
+    gc.collect()
+    assert pool._cached == 320
+    c = _lib.new_image((3, 7), np.float32)
+    assert c.flags.c_contiguous and c.flags.writeable and c.dtype == np.float32 and c.shape == (3, 7)
