@@ -196,6 +196,7 @@ struct Device {
     bool chunking = true;        // large calls in row chunks over kLanes streams (FSR_NO_CHUNK=1: off)
     int used_tma = 0;            // last fp32-loop launch gathered by TMA
     int served_fp64 = 0;         // last launch: a guarded fp32 request served by the fp64 kernels
+    bool segmented = true;       // N <= 8: 32/N blocks per warp (FSR_NO_SEG=1: one warp per block)
     // Calls run as K row chunks over kLanes "lanes" (same GPU, own stream, staging
     // buffers and re-run scratch): one chunk's copies, fp64 re-run and launch
     // tail overlap the other chunks' main kernels.
@@ -566,9 +567,6 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     const fsr_params *p_req = p;
     fsr_params pl = *p;
     if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
-    // N = 4 (L = 0 at B = 4: the window is the block) flags ~40 % of the blocks
-    // and its fp64 kernel is faster than fp32 + re-runs (1080p: 378 vs 349 fps)
-    if (pl.precision == FSR_PREC_FP32 && N == 4) pl.precision = FSR_PREC_FP64;
     p = &pl;
     CUDA_TRY(eng, cudaMemsetAsync(cc, 0, sizeof(ChunkCtr), st));
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
@@ -715,6 +713,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, d.sms, st)));
         } else if (fast16) {
             LAUNCH_TRY(eng, d, (warp16_any<IO>(a, maps, tree, p->argmax_impl, guarded, opts, d.sms, st)));
+        } else if (fastn && N <= 8 && p->block <= 4 && d.segmented) {
+            LAUNCH_TRY(eng, d, (warpseg_any<IO>(a, N, guarded, opts, d.sms, st)));
         } else if (fastn) {
             LAUNCH_TRY(eng, d, (warpn_any<IO>(a, maps, N, p->argmax_impl, guarded, opts, d.sms, st)));
         } else {
@@ -842,6 +842,7 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
         ln->id = d.id;
         ln->sms = d.sms;
         ln->tma_enabled = d.tma_enabled;
+        ln->segmented = d.segmented;
         CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
         CUDA_TRY(eng, cudaEventCreateWithFlags(&ln->ev0, cudaEventDisableTiming));
         CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
@@ -1241,6 +1242,8 @@ int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **ou
         d->tma_enabled = !(no_tma && *no_tma && *no_tma != '0');
         const char *no_chunk = std::getenv("FSR_NO_CHUNK");  // one launch per call (kernel timing)
         d->chunking = !(no_chunk && *no_chunk && *no_chunk != '0');
+        const char *no_seg = std::getenv("FSR_NO_SEG");  // A/B switch for the segmented small-N kernel
+        d->segmented = !(no_seg && *no_seg && *no_seg != '0');
         CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));

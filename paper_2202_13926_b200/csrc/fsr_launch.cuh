@@ -58,6 +58,15 @@ cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bo
 template <typename IO>
 cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want_blocks, int sms,
                           cudaStream_t st);
+// N in {4, 8}, B <= 4: 32 / N blocks per warp (fsr_warpseg.cuh; own segmented argmax)
+template <typename IO, int N>
+cudaError_t warpseg_launch(const Warp32Args &a, bool guard, int opts, int sms, cudaStream_t st);
+template <typename IO>
+inline cudaError_t warpseg_any(const Warp32Args &a, int N, bool guard, int opts, int sms, cudaStream_t st) {
+    if (N == 4) return warpseg_launch<IO, 4>(a, guard, opts, sms, st);
+    if (N == 8) return warpseg_launch<IO, 8>(a, guard, opts, sms, st);
+    return kNotBuilt;
+}
 template <typename IO>
 inline cudaError_t warpn_any(const Warp32Args &a, const Warp32Maps &m, int N, int am, bool guard,
                              int opts, int sms, cudaStream_t st) {

@@ -4,6 +4,7 @@
 // scale term) and the full build (trace + early stop).
 #include "fsr_launch.cuh"
 #include "fsr_warpn.cuh"
+#include "fsr_warpseg.cuh"
 
 #ifndef FSR_IO
 #define FSR_IO float
@@ -36,6 +37,29 @@ cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, bool guard, int
 }
 }  // namespace
 
+template <typename IO, int N, bool GUARD, int OPTS>
+cudaError_t seg_go(const Warp32Args &a, int sms, cudaStream_t st) {
+    if constexpr (N == 4 || N == 8) {
+        constexpr int WARPS = 4, BPC = WARPS * SegCfg<N>::BPW;  // blocks per CTA
+        auto k = warpseg_kernel<IO, N, WARPS, GUARD, OPTS>;
+        const size_t smem = sizeof(WarpSegSmem<N, WARPS>);
+        int grid = 1;
+        cudaError_t e = persistent_grid(k, WARPS * 32, smem, (a.nblocks + BPC - 1) / BPC, sms, &grid);
+        if (e != cudaSuccess) return e;
+        k<<<grid, WARPS * 32, smem, st>>>(a);
+        return cudaGetLastError();
+    } else {
+        return kNotBuilt;
+    }
+}
+
+template <typename IO, int N>
+cudaError_t warpseg_launch(const Warp32Args &a, bool guard, int opts, int sms, cudaStream_t st) {
+    if (opts == 0) return guard ? seg_go<IO, N, true, 0>(a, sms, st) : seg_go<IO, N, false, 0>(a, sms, st);
+    if (opts == LOPT_KAPPA && guard) return seg_go<IO, N, true, W32_KAPPA>(a, sms, st);
+    return guard ? seg_go<IO, N, true, W32_ALL>(a, sms, st) : seg_go<IO, N, false, W32_ALL>(a, sms, st);
+}
+
 template <typename IO, int N>
 cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
                          int sms, cudaStream_t st) {
@@ -47,5 +71,6 @@ cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bo
 
 template cudaError_t warpn_launch<FSR_IO, FSR_N>(const Warp32Args &, const Warp32Maps &, int, bool,
                                                  int, int, cudaStream_t);
+template cudaError_t warpseg_launch<FSR_IO, FSR_N>(const Warp32Args &, bool, int, int, cudaStream_t);
 
 }  // namespace fsr
