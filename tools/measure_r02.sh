@@ -5,7 +5,7 @@
 O=gpurun_out/r02
 mkdir -p $O
 timeout 900 python -m pytest tests -m gpu -q --timeout 300 -rA 2>&1 | grep -E "passed|failed|PASSED.*fullframe|^fp" | tail -5 > $O/pytest_gpu.txt
-timeout 900 python -m pytest tests/test_gpu_fullframe.py -m gpu -q -s 2>&1 | grep -E "^fp|passed|failed" > $O/fullframe_1080p.txt
+timeout 900 python -m pytest tests/test_gpu_fullframe.py -m gpu -q -s 2>&1 | grep -oE "fp(32|64) 1080p.*|[0-9]+ passed.*|[0-9]+ failed.*" > $O/fullframe_1080p.txt
 timeout 600 python bench.py > $O/bench_4k_default.json 2> $O/e1.err
 timeout 600 python bench.py --precision fp64 --no-cpu > $O/bench_4k_fp64.json 2> $O/e2.err
 for s in 32 16 24 8 4; do

@@ -80,8 +80,14 @@ def main():
                         "kernel": {(32, False): "warp32 (+pair64 re-runs)", (32, True): "pair64",
                                    (16, False): "warp16 (+warp16d re-runs)", (16, True): "warp16d",
                                    (64, False): "cta64, in-warp redux (+cta64d fp64 re-runs)",
-                                   (64, True): "cta64d"}
+                                   (64, True): "cta64d",
+                                   (24, False): "warpn (+warpnd re-runs)", (24, True): "warpnd",
+                                   (8, False): "warpseg, 4 blocks/warp (+warpnd re-runs)",
+                                   (8, True): "warpnd",
+                                   (4, False): "warpseg, 8 blocks/warp (+warpnd re-runs)",
+                                   (4, True): "warpnd"}
                                   .get((N, args.precision == "fp64" or I > 300), "generic")}
+                line["served_fp64"] = stats.get("served_fp64")
                 print(json.dumps(line), flush=True)
 
 
