@@ -52,8 +52,10 @@ __device__ __forceinline__ void fft_line(cpx<T> (&x)[N]) {
         fft_pow2<2>(x);
     } else if constexpr (N == 8) {
         fft_pow2<3>(x);
+    } else if constexpr (N == 16) {
+        fft_pow2<4>(x);
     } else {
-        static_assert(N == 24, "fft_line: N in {4, 8, 24}");
+        static_assert(N == 24, "fft_line: N in {4, 8, 16, 24}");
         // decimation in time by 3: y_r = FFT8(x[3m + r]); X[k1 + 8 k2] =
         // sum_r W3^{r k2} (W24^{r k1} y_r[k1])
         cpx<T> y[3][8];

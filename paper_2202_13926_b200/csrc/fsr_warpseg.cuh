@@ -1,5 +1,5 @@
-// fsr_warpseg.cuh -- fp32 loop kernel for the small supports N = 4 and 8 with
-// 32 / N target blocks per warp ("segments" of N lanes, one block each).
+// fsr_warpseg.cuh -- fp32 loop kernel for the small supports N = 4, 8 and 16
+// with 32 / N target blocks per warp ("segments" of N lanes, one block each).
 //
 // fsr_warpn.cuh gives a small support one warp per block, so at N = 8 three
 // quarters of the lanes idle and the per-iteration argmax tail is paid per
@@ -10,8 +10,9 @@
 //              half swap of pu >= P (warp-uniform in warp32) differs between
 //              segments, so each segment keeps U and its half-swapped copy U'
 //              and a lane picks the table by pointer (no per-pair selects)
-//   keys       the pair's larger objective with (pair << log2 N | v) in the 5
-//              low bits: unique within a segment, so a log2(N)-step xor
+//   keys       the pair's larger objective with (pair << log2 N | v) in the
+//              low bits (5 for N <= 8; 7 for N = 16, whose 2^-16 truncation the
+//              guard adds to tau): unique within a segment, so a log2(N)-step xor
 //              butterfly (never leaves the segment) yields the winner's pair
 //              and lane; any maximal bin may win (guarded: every near-tie is
 //              re-run in fp64; the Hermitian phase keeps the canonical halves)
@@ -33,14 +34,17 @@ template <int N>
 struct SegCfg {
     static constexpr int P = N / 2;
     static constexpr int BPW = 32 / N;                 // blocks (segments) per warp
-    static constexpr int LV = N == 8 ? 3 : 2;          // log2 N
+    static constexpr int LV = N == 16 ? 4 : N == 8 ? 3 : 2;  // log2 N
+    static constexpr int TAG = LV + (N == 16 ? 3 : N == 8 ? 2 : 1) > 5 ? 7 : 5;  // low key bits
+    static constexpr uint32_t KMASK = ~((1u << TAG) - 1u);
+    static constexpr float TSLACK = TAG > 5 ? 1.0f / 65536.0f : 0.f;  // key truncation (relative)
     static constexpr int TILE = N * (N + 1) * 16;
     static constexpr int UTAB = N * N * 16;
     static constexpr int SEG = TILE > 2 * UTAB ? TILE : 2 * UTAB;  // bytes per segment
     static constexpr int SEG_F4 = SEG / 16;
-    static constexpr int NPIX = 16 / N;                // target pixels per lane (B <= 4)
-    static_assert(N == 4 || N == 8, "segmented kernel: N in {4, 8}");
-    static_assert((P - 1) << LV < 32 && N <= 32, "pair and lane tags fit the 5 key bits");
+    static constexpr int NPIX = (16 + N - 1) / N;      // target pixels per lane (B <= 4)
+    static_assert(N == 4 || N == 8 || N == 16, "segmented kernel: N in {4, 8, 16}");
+    static_assert(((P - 1) << LV) + N - 1 < (1 << TAG), "pair and lane tags fit the key bits");
 };
 
 template <int N, int WARPS>
@@ -57,7 +61,7 @@ __device__ __forceinline__ uint32_t seg_max(uint32_t k) {
     return k;
 }
 
-template <int N, bool GUARD, bool HERM, bool UPDATE>
+template <int N, bool GUARD, bool HERM, bool UPDATE, uint32_t KMASK>
 __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2], const float2 (&wf2)[N / 2],
                                          const float4 *up, float gr, float gi, uint32_t canon,
                                          const uint32_t (&tag)[N / 2], uint32_t &m1, uint32_t &m2) {
@@ -86,7 +90,7 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
             ox = ((canon >> i) & 1u) ? ox : 0.f;
             oy = ((canon >> (i + P)) & 1u) ? oy : 0.f;
         }
-        const uint32_t h = and_or(f2u(fmaxf(ox, oy)), 0xffffffe0u, tag[i]);
+        const uint32_t h = and_or(f2u(fmaxf(ox, oy)), KMASK, tag[i]);
         if (!GUARD || P == 1) {
             m1 = max(m1, h);
         } else if ((i & 1) == 0) {
@@ -100,10 +104,15 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
 }
 
 #ifndef FSR_SEG_WARPS_PER_SM
-#define FSR_SEG_WARPS_PER_SM 32
+#define FSR_SEG_WARPS_PER_SM 32     // N <= 8 (64 registers)
 #endif
+#ifndef FSR_SEG16_WARPS_PER_SM
+#define FSR_SEG16_WARPS_PER_SM 12   // N = 16: 16 KiB of tables per warp
+#endif
+template <int N>
+constexpr int seg_warps_per_sm() { return N == 16 ? FSR_SEG16_WARPS_PER_SM : FSR_SEG_WARPS_PER_SM; }
 template <typename IO, int N, int WARPS, bool GUARD, int OPTS>
-__global__ void __launch_bounds__(WARPS * 32, FSR_SEG_WARPS_PER_SM / WARPS)
+__global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
     warpseg_kernel(Warp32Args a) {
     using C = SegCfg<N>;
     constexpr int P = C::P;
@@ -241,13 +250,13 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_SEG_WARPS_PER_SM / WARPS)
             const uint32_t cn = (H && herm) ? canon : 0xffffffffu;
             uint32_t m1, m2;
             if (H && it == 0)
-                seg_pass<N, GUARD, true, false>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
+                seg_pass<N, GUARD, true, false, C::KMASK>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
             else
-                seg_pass<N, GUARD, H, true>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
+                seg_pass<N, GUARD, H, true, C::KMASK>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
             if (!live) m1 = m2 = 0u;
             const uint32_t kmax = seg_max<N>(m1);
             const int wl = (int)(kmax & (N - 1)), j = (int)((kmax >> C::LV) & (P - 1));
-            const float b1 = __uint_as_float(kmax & ~31u);
+            const float b1 = __uint_as_float(kmax & C::KMASK);
             bool go = live;
             if (EARLY && live && b1 < thr) {
                 if (GUARD && b1 >= thr * a.omt) flagged = true;
@@ -289,16 +298,17 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_SEG_WARPS_PER_SM / WARPS)
                 done = it + 1;
             }
             if (GUARD) {
-                const uint32_t kp = f2u(po) & 0xffffffe0u;
+                const uint32_t kp = f2u(po) & C::KMASK;
                 const uint32_t k2 = seg_max<N>(v == wl ? max(m2, kp) : m1);
-                const float b2 = __uint_as_float(k2 & ~31u);
+                const float b2 = __uint_as_float(k2 & C::KMASK);
+                const float omt = a.omt - C::TSLACK;  // keys truncated to 2^-(23-TAG)
                 float gap;
                 if (KAPPA) {
                     const float sb1 = sqrt_approx(b1);
                     if (H && it == 0) ks = a.kappa * sb1;
-                    gap = b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt));
+                    gap = b2 - fmaf(-ks, sb1, __fmul_rn(b1, omt));
                 } else {
-                    gap = b2 - __fmul_rn(b1, a.omt);
+                    gap = b2 - __fmul_rn(b1, omt);
                 }
                 if (go) fl = fmaxf(fl, gap);
                 if (EARLY && go) flagged |= b1 * a.omt < thr;

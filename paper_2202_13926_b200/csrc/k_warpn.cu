@@ -39,7 +39,7 @@ cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, bool guard, int
 
 template <typename IO, int N, bool GUARD, int OPTS>
 cudaError_t seg_go(const Warp32Args &a, int sms, cudaStream_t st) {
-    if constexpr (N == 4 || N == 8) {
+    if constexpr (N == 4 || N == 8 || N == 16) {
         constexpr int WARPS = 4, BPC = WARPS * SegCfg<N>::BPW;  // blocks per CTA
         auto k = warpseg_kernel<IO, N, WARPS, GUARD, OPTS>;
         const size_t smem = sizeof(WarpSegSmem<N, WARPS>);
@@ -63,10 +63,14 @@ cudaError_t warpseg_launch(const Warp32Args &a, bool guard, int opts, int sms, c
 template <typename IO, int N>
 cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
                          int sms, cudaStream_t st) {
-    if (am == AM_SHFL) return by_opts<IO, N, AM_SHFL>(a, maps, guard, opts, sms, st);
-    if (am == AM_SMEM) return by_opts<IO, N, AM_SMEM>(a, maps, guard, opts, sms, st);
-    if (am == AM_REDUX) return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
-    return kNotBuilt;
+    if constexpr (N == 16) {
+        return kNotBuilt;  // N = 16: warp16 / warpseg
+    } else {
+        if (am == AM_SHFL) return by_opts<IO, N, AM_SHFL>(a, maps, guard, opts, sms, st);
+        if (am == AM_SMEM) return by_opts<IO, N, AM_SMEM>(a, maps, guard, opts, sms, st);
+        if (am == AM_REDUX) return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
+        return kNotBuilt;
+    }
 }
 
 template cudaError_t warpn_launch<FSR_IO, FSR_N>(const Warp32Args &, const Warp32Maps &, int, bool,
