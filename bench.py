@@ -424,7 +424,7 @@ def main():
 
     import paper_2202_13926_b200 as fsr
     from paper_2202_13926_b200 import _lib, shard
-    from paper_2202_13926_b200.engine import effective_guard_tau
+    from paper_2202_13926_b200.engine import effective_guard_kappa, effective_guard_tau
 
     H, W = WORKLOADS[args.workload]
     B, N, I = args.block, args.support, args.iterations
@@ -580,9 +580,9 @@ def main():
     achieved = flop / (mean_main * 1e-3) / 1e12
     clk_hz = pk.get("sm_max_mhz", 1965.0) * 1e6
     # a guarded fp32 request the engine serves in fp64 (fsr_abi.cu enqueue_image:
-    # I > 300 or a support without an fp32 register kernel) is reported as fp64
+    # I > 300, N = 4, or a support without an fp32 register kernel) is reported as fp64
     fp32_kernel = (B * B <= 32 and N in (4, 8, 16, 24, 32)) or (N == 64 and args.reducer == "linear")
-    served64 = args.precision == "fp32" and (I > 300 or not fp32_kernel)
+    served64 = args.precision == "fp32" and (I > 300 or N == 4 or not fp32_kernel)
     fp64 = args.precision == "fp64" or served64
     peak_fl, peak_src = fp_peak(fp64)
     if N == 32 and B * B <= 32:
@@ -623,6 +623,7 @@ def main():
                    "served_precision": "fp64" if fp64 else args.precision,
                    "parallelism": f"strips{world}",
                    "guard_tau": effective_guard_tau(N, I) if args.precision == "fp32" else None,
+                   "guard_kappa": effective_guard_kappa(I, support=N) if args.precision == "fp32" else None,
                    "io": f"{io} pixels + u8 mask in, {io} out",
                    "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": "fp64" if fp64 else "fp32", "achieved": achieved, "peak": peak_fl,

@@ -404,7 +404,10 @@ int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tre
 template <typename IO>
 int launch_warpnd(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int N, int am,
                   int64_t want_blocks, cudaStream_t st) {
-    LAUNCH_TRY(eng, d, (warpnd_launch<IO>(a, N, am, want_blocks, d.sms, st)));
+    if (N <= 8 && a.B <= 4 && d.segmented)  // 32/N blocks per warp (fsr_warpseg.cuh)
+        LAUNCH_TRY(eng, d, (warpsegd_launch<IO>(a, N, want_blocks, d.sms, st)));
+    else
+        LAUNCH_TRY(eng, d, (warpnd_launch<IO>(a, N, am, want_blocks, d.sms, st)));
     return FSR_OK;
 }
 
@@ -530,17 +533,23 @@ bool warp32_eligible(const fsr_params *p) {
 // noise frames with tools/flip_errors.py:
 //     tau   = 5e-5 * k_N,                 k_N = 2 for N = 64, else 1
 //     kappa = 1e-7 * max(0, I / 100 - 1)  (none up to the default 100 iterations)
+// and for the small supports N <= 8 (64 bins or fewer: after a few dozen
+// iterations every objective lies far below B0, so the scale term would flag
+// nearly every block -- 95 % at N = 8, I = 200):
+//     tau   = 2e-4, kappa = 0             (1080p N = 8, I = 100: max 0.09 gray
+//                                          levels at 15 % re-runs; I = 200: 0.17)
 // An explicit guard_tau > 0 / guard_kappa > 0 is used as given; guard_kappa < 0
 // turns the scale term off.
 double guard_tau_for(const fsr_params *p) {
     if (p->guard_tau > 0.0) return p->guard_tau;
     const int N = p->block + 2 * p->border;
-    return N >= 64 ? 1e-4 : 5e-5;
+    return N >= 64 ? 1e-4 : N <= 8 ? 2e-4 : 5e-5;
 }
 
 double guard_kappa_for(const fsr_params *p) {
     if (p->guard_kappa > 0.0) return p->guard_kappa;
     if (p->guard_kappa < 0.0) return 0.0;
+    if (p->block + 2 * p->border <= 8) return 0.0;
     return 1e-7 * std::max(0.0, p->iterations / 100.0 - 1.0);
 }
 
@@ -567,6 +576,10 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     const fsr_params *p_req = p;
     fsr_params pl = *p;
     if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
+    // N = 4 (L = 0 at B = 4: the window is the block) re-runs ~45 % of the blocks,
+    // and its segmented fp64 kernel is faster than fp32 + re-runs (1080p: 2226 vs
+    // 1702 fps) -- and exact
+    if (pl.precision == FSR_PREC_FP32 && N == 4) pl.precision = FSR_PREC_FP64;
     p = &pl;
     CUDA_TRY(eng, cudaMemsetAsync(cc, 0, sizeof(ChunkCtr), st));
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));

@@ -67,6 +67,9 @@ inline cudaError_t warpseg_any(const Warp32Args &a, int N, bool guard, int opts,
     if (N == 8) return warpseg_launch<IO, 8>(a, guard, opts, sms, st);
     return kNotBuilt;
 }
+// N in {4, 8}, B <= 4, fp64: the segmented layout (fsr_warpseg.cuh)
+template <typename IO>
+cudaError_t warpsegd_launch(const Pair64Args<IO> &a, int N, int64_t want_blocks, int sms, cudaStream_t st);
 template <typename IO>
 inline cudaError_t warpn_any(const Warp32Args &a, const Warp32Maps &m, int N, int am, bool guard,
                              int opts, int sms, cudaStream_t st) {

@@ -354,4 +354,211 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
     }
 }
 
+// ---------------------------------------------------------------- fp64 variant
+// warpsegd: the same segmented layout in fp64 (N = 4, 8) for the validation
+// precision and the guarded re-runs (list mode): R[u][v] for the N rows in
+// registers, the segment's row-doubled W table (row u - pu + N, no wrap), 64-bit
+// keys whose low 10 bits hold the reference's tie rank of the flat bin (unique
+// within a block, so the segment butterfly's u64 max is the reference's argmax).
+template <int N>
+struct SegdCfg {
+    static constexpr int BPW = 32 / N;
+    static constexpr int TILE = N * (N + 1);           // double2
+    static constexpr int W2 = 2 * N * N;               // double2
+    static constexpr int SEG = TILE > W2 ? TILE : W2;  // double2 per segment
+    static constexpr int NPIX = 16 / N;
+};
+
+template <int N, int WARPS>
+struct WarpSegdSmem {
+    double2 seg[WARPS][SegdCfg<N>::BPW][SegdCfg<N>::SEG];
+    double2 cs[N];
+};
+
+template <int N>
+__device__ __forceinline__ unsigned long long seg_max64(unsigned long long k) {
+#pragma unroll
+    for (int off = N / 2; off >= 1; off >>= 1) {
+        const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(k >> 32), off);
+        const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)k, off);
+        k = u64max(k, ((unsigned long long)hi << 32) | lo);
+    }
+    return k;
+}
+
+template <int N, int WARPS, typename IO>
+__global__ void __launch_bounds__(WARPS * 32) warpsegd_kernel(Pair64Args<IO> a) {
+    using C = SegdCfg<N>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSegdSmem<N, WARPS> &sm = *reinterpret_cast<WarpSegdSmem<N, WARPS> *>(smem_raw);
+    if (threadIdx.x < N) {
+        double sn, cn;
+        sincospi(2.0 * threadIdx.x / N, &sn, &cn);
+        sm.cs[threadIdx.x] = make_double2(cn, sn);
+    }
+    __syncthreads();
+    const bool TREE = a.tree != 0;
+    const int lane = lane_id(), wid = warp_id();
+    const int sg = lane / N, v = lane % N, sbase = sg * N;
+    double2 *t = sm.seg[wid][sg];
+    uint32_t rk[N];  // 1023 - rank(u N + v)
+    double wfr[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        rk[u] = (uint32_t)(1023 - tie_rank(u * N + v, TREE));
+        wfr[u] = a.wf[u * N + v];
+    }
+    const int64_t nblocks = a.list_count ? (int64_t)*a.list_count : a.nblocks;
+    const int64_t stride = (int64_t)gridDim.x * WARPS * C::BPW;
+    for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * C::BPW; base < nblocks; base += stride) {
+        const int64_t bi = base + sg;
+        const bool real = bi < nblocks;
+        const int64_t bix = real ? bi : nblocks - 1;
+        const int64_t bid = a.list ? (int64_t)a.list[bix] : a.first + bix;
+        const int64_t brow = bid / a.bcols, bcol = bid - brow * a.bcols;
+        const int64_t r0 = brow * a.B, c0 = bcol * a.B;
+        constexpr int TS = N + 1;
+        const int64_t wr0 = r0 - a.L, x = c0 - a.L + v;
+        const bool xin = x >= 0 && x < a.W;
+        double energy = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            const int64_t y = wr0 + k;
+            double f = 0.0, w = 0.0;
+            if (xin && y >= 0 && y < a.H && a.mask[y * a.mask_pitch + x]) {
+                f = load_px(a.px + y * a.px_pitch + x);
+                w = a.decay[k * N + v];
+            }
+            t[k * TS + v] = make_double2(f * w, w);
+            energy = fma(f * f, w, energy);
+        }
+        __syncwarp();
+        cpx<double> R[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) { const double2 z = t[v * TS + j]; R[j] = {z.x, z.y}; }
+        fft_line<N>(R);
+#pragma unroll
+        for (int j = 0; j < N; ++j) t[v * TS + j] = make_double2(R[j].re, R[j].im);
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < N; ++j) { const double2 z = t[j * TS + v]; R[j] = {z.x, z.y}; }
+        fft_line<N>(R);
+#pragma unroll
+        for (int j = 0; j < N; ++j) t[j * TS + v] = make_double2(R[j].re, R[j].im);
+        __syncwarp();
+        double2 Wc[N];
+        {
+            const int mv = (N - v) % N;
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                const int nu = (N - u) % N;
+                const double2 z = t[u * TS + v], zm = t[nu * TS + mv];
+                R[u] = {(z.x + zm.x) * 0.5, (z.y - zm.y) * 0.5};
+                Wc[u] = make_double2((z.y + zm.y) * 0.5, (zm.x - z.x) * 0.5);
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < N; ++u) {
+            t[u * N + v] = Wc[u];
+            t[(u + N) * N + v] = Wc[u];
+        }
+        __syncwarp();
+        const double w00 = t[0].x;
+        const bool empty = !(w00 > 0.0);
+        int32_t *sel_b = (a.sel && real) ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
+        if (empty && real && v == 0) {
+            unsigned slot = atomicAdd(a.empty_count, 1u);
+            if (a.empty_list) a.empty_list[slot] = (int32_t)bid;
+            if (a.done) a.done[bid] = 0;
+        }
+        double thr = 0.0;
+        if (a.early_stop) {
+#pragma unroll
+            for (int off = N / 2; off >= 1; off >>= 1) energy += __shfl_xor_sync(0xffffffffu, energy, off);
+            thr = 1e-12 * energy;
+        }
+        const double ginv = empty ? 0.0 : a.gamma / w00;
+        double acc[C::NPIX];
+        int pmq[C::NPIX], pnq[C::NPIX];
+#pragma unroll
+        for (int q = 0; q < C::NPIX; ++q) {
+            acc[q] = 0.0;
+            const int p = v + q * N;
+            pmq[q] = a.L + p / a.B;
+            pnq[q] = a.L + p % a.B;
+        }
+        bool live = real && !empty;
+        double gr = 0.0, gi = 0.0;
+        int pu = 0, pv = 0, done = 0;
+        for (int it = 0; it < a.iterations; ++it) {
+            if (a.early_stop && !__any_sync(0xffffffffu, live)) break;
+            int col = v - pv;
+            col += col < 0 ? N : 0;
+            const double2 *wp = t + (N - pu) * N + col;  // row u - pu + N of W2
+            unsigned long long best = 0ull;
+#pragma unroll
+            for (int u = 0; u < N; ++u) {
+                double re = R[u].re, im = R[u].im;
+                if (it > 0) {
+                    const double2 w = wp[u * N];
+                    re = fma(-gr, w.x, re);
+                    re = fma(gi, w.y, re);
+                    im = fma(-gr, w.y, im);
+                    im = fma(-gi, w.x, im);
+                    R[u].re = re;
+                    R[u].im = im;
+                }
+                const double o = fma(re, re, im * im) * wfr[u];
+                const uint32_t lo = ((uint32_t)__double2loint(o) & ~1023u) | rk[u];
+                const unsigned long long k =
+                    ((unsigned long long)(uint32_t)__double2hiint(o) << 32) | (unsigned long long)lo;
+                best = u64max(best, k);
+            }
+            if (!live) best = 0ull;
+            const unsigned long long key = seg_max64<N>(best);
+            const int tb = rank_to_bin(1023 - (int)((uint32_t)key & 1023u), TREE);
+            const int bu = tb / N, bv = tb - (tb / N) * N;
+            bool go = live;
+            if (live && thr > 0.0 && __longlong_as_double((long long)key) < thr) live = go = false;
+            if (sel_b && v == 0 && go) sel_b[it] = bu * N + bv;
+            double2 c = make_double2(R[0].re, R[0].im);
+#pragma unroll
+            for (int u = 1; u < N; ++u)
+                if (u == bu) c = make_double2(R[u].re, R[u].im);
+            c.x = __shfl_sync(0xffffffffu, c.x, sbase + bv);
+            c.y = __shfl_sync(0xffffffffu, c.y, sbase + bv);
+            gr = go ? c.x * ginv : 0.0;
+            gi = go ? c.y * ginv : 0.0;
+#pragma unroll
+            for (int q = 0; q < C::NPIX; ++q) {
+                const double2 e = sm.cs[(bu * pmq[q] + bv * pnq[q]) % N];
+                acc[q] = fma(gr, e.x, fma(-gi, e.y, acc[q]));
+            }
+            if (go) {
+                pu = bu;
+                pv = bv;
+                done = it + 1;
+            }
+        }
+        if (sel_b)
+            for (int it = done + v; it < a.iterations; it += N) sel_b[it] = -1;
+        if (real && !empty && v == 0 && a.done) a.done[bid] = done;
+        if (real && !empty) {
+#pragma unroll
+            for (int q = 0; q < C::NPIX; ++q) {
+                const int p = v + q * N;
+                if (p < a.B * a.B) {
+                    const int m = p / a.B, n = p % a.B;
+                    const int64_t y = r0 + m, xx = c0 + n;
+                    if (y < a.H && xx < a.W)
+                        a.out[y * a.out_pitch + xx] =
+                            a.mask[y * a.mask_pitch + xx] ? a.px[y * a.px_pitch + xx] : (IO)acc[q];
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace fsr

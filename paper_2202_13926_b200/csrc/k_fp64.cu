@@ -7,6 +7,7 @@
 #include "fsr_warp16.cuh"
 #include "fsr_warp64.cuh"
 #include "fsr_warpn.cuh"
+#include "fsr_warpseg.cuh"
 
 #ifndef FSR_IO
 #define FSR_IO float
@@ -100,6 +101,25 @@ cudaError_t wnd_am(const Pair64Args<IO> &a, int am, int64_t want, int sms, cudaS
 }
 }  // namespace
 
+template <int N, typename IO>
+cudaError_t wsd_go(const Pair64Args<IO> &a, int64_t want, int sms, cudaStream_t st) {
+    constexpr int WARPS = 4, BPC = WARPS * SegdCfg<N>::BPW;
+    auto k = warpsegd_kernel<N, WARPS, IO>;
+    const size_t smem = sizeof(WarpSegdSmem<N, WARPS>);
+    int grid = 1;
+    cudaError_t e = persistent_grid(k, WARPS * 32, smem, (want + BPC - 1) / BPC, sms, &grid);
+    if (e != cudaSuccess) return e;
+    k<<<grid, WARPS * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename IO>
+cudaError_t warpsegd_launch(const Pair64Args<IO> &a, int N, int64_t want, int sms, cudaStream_t st) {
+    if (N == 4) return wsd_go<4>(a, want, sms, st);
+    if (N == 8) return wsd_go<8>(a, want, sms, st);
+    return kNotBuilt;
+}
+
 template <typename IO>
 cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want, int sms, cudaStream_t st) {
     if (N == 4) return wnd_am<4>(a, am, want, sms, st);
@@ -143,6 +163,7 @@ template cudaError_t warp64_launch<FSR_IO>(const Pair64Args<FSR_IO> &, bool, int
 template cudaError_t warp16d_launch<FSR_IO>(const Pair64Args<FSR_IO> &, bool, int, int64_t, int, cudaStream_t);
 template cudaError_t cta64d_grid<FSR_IO>(int64_t, int, int *);
 template cudaError_t warpnd_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, int, int64_t, int, cudaStream_t);
+template cudaError_t warpsegd_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, int64_t, int, cudaStream_t);
 template cudaError_t cta64d_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, cudaStream_t);
 template cudaError_t generic_launch<double, FSR_IO>(const ImageArgs<double, FSR_IO> &, int, cudaStream_t);
 template cudaError_t generic_launch<float, FSR_IO>(const ImageArgs<float, FSR_IO> &, int, cudaStream_t);

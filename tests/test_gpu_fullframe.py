@@ -68,3 +68,30 @@ def test_fullframe_1080p_fp32_production(frame):
     assert err <= 1e-3 * 255, err
     assert abs(dpsnr) <= 0.01
     assert np.array_equal(out[mask], sampled[mask])
+
+
+@pytest.mark.parametrize("N", [8, 16, 24])
+def test_fullframe_1080p_paper_grid_supports(N):
+    """The paper grid's other supports over the whole 1080p
+    frame: fp64 sequences mirror-equal (or proven co-maximal splits), guarded
+    fp32 within the production tolerance -- the check that exposed the
+    N <= 8 guard defaults."""
+    B = 4
+    Ls = (N - B) // 2
+    img = oracle.synthetic_frame(H, W, 7)
+    sampled, mask = oracle.quarter_sample(img, 42)
+    ref, rtr = oracle.reconstruct_image(sampled, mask, B, Ls, I, 0.7, 0.5, "tree", trace=True)
+    out64, tr = fsr.reconstruct(sampled, mask, B, N, I, precision="fp64", return_trace=True)
+    counts, div = oracle.compare_sequences(tr.selections[:, :I].astype(np.int64),
+                                           rtr["sel"][:, :I].astype(np.int64), N)
+    assert counts["diverged"] <= 129600 // 1000
+    for b in np.nonzero(div)[0]:
+        ok, f, gap = oracle.coemaximal_split(sampled, mask, B, Ls, I, 0.7, 0.5, "tree", int(b),
+                                             tr.selections[b])
+        assert ok, f"block {b}: diverges at iteration {f}, objective gap {gap:.3e}"
+    out32 = fsr.reconstruct(sampled, mask, B, N, I, precision="fp32")
+    err = float(np.abs(out32 - ref).max())
+    print(f"N={N} 1080p: fp64 {counts}, fp32 max|d| {err / 255:.3e}")
+    assert err <= 1e-3 * 255, err
+    assert abs(oracle.psnr(img, out32) - oracle.psnr(img, ref)) <= 0.01
+    assert np.array_equal(out32[mask], sampled[mask])

@@ -706,10 +706,10 @@ def test_guard_beyond_default_iterations(N, I, kind):
 
 
 @pytest.mark.parametrize("N,B,I,served", [(24, 4, 60, False), (8, 4, 60, False), (16, 4, 60, False),
-                                          (32, 4, 400, True), (4, 4, 60, False), (12, 4, 60, True)])
+                                          (32, 4, 400, True), (4, 4, 60, True), (12, 4, 60, True)])
 def test_guarded_fp32_reports_fp64_service(N, B, I, served):
-    """A guarded fp32 request is served by the fp64 kernels beyond 300 iterations
-    and for supports without an fp32 register kernel; the call's stats
+    """A guarded fp32 request is served by the fp64 kernels beyond 300 iterations,
+    at N = 4 and for supports without an fp32 register kernel; the call's stats
     say so (FSR_STATS_SERVED_FP64), so a bench line never labels fp64 work fp32."""
     img = oracle.synthetic_frame(40, 48, 5)
     sampled, mask = oracle.quarter_sample(img, 3)
