@@ -26,8 +26,8 @@ def main():
     fails = 0
     t0 = time.time()
     for c in range(n):
-        N = int(rng.choice([16, 32, 64]))
-        B = int(rng.choice([2, 4, 6] if N < 64 else [4, 6, 8]))
+        N = int(rng.choice([4, 8, 16, 24, 32, 64]))
+        B = int(rng.choice([2, 4] if N == 4 else [2, 4, 6] if N < 64 else [4, 6, 8]))
         if (N - B) % 2:
             B += 1
         reducer = "linear" if N == 64 else str(rng.choice(["tree", "linear"]))
@@ -37,33 +37,52 @@ def main():
         kind = str(rng.choice(["natural", "uniform"]))
         rho = float(rng.choice([0.7, 0.68, 0.82, 0.6, 0.9])) if len(sys.argv) > 3 else 0.7
         gamma = float(rng.choice([0.5, 0.2, 0.6, 0.8])) if len(sys.argv) > 3 else 0.5
-        img = oracle.synthetic_frame(H, W, int(rng.integers(0, 1000)), kind) if H > 1 and W > 1 \
+        iseed = int(rng.integers(0, 1000)) if H > 1 and W > 1 else -1
+        img = oracle.synthetic_frame(H, W, iseed, kind) if H > 1 and W > 1 \
             else rng.uniform(0, 255, (H, W))
-        sampled, mask = oracle.quarter_sample(img, int(rng.integers(0, 2**31)))
+        mseed = int(rng.integers(0, 2**31))
+        sampled, mask = oracle.quarter_sample(img, mseed)
         if not mask.any():
+            continue
+        only = os.environ.get("ONLY")
+        if only and str(c) not in only.split(","):
             continue
         sampled = np.where(mask, sampled, 0.0)
         L = (N - B) // 2
-        s32 = sampled.astype(np.float32)
-        ref32 = oracle.reconstruct_image(s32.astype(np.float64), mask, B, L, I, rho, gamma, reducer, early)
-        out32 = fsr.reconstruct(s32, mask, B, N, I, rho, gamma, reducer=reducer, early_stop=early,
-                                precision="fp32", argmax="redux")
-        e32 = float(np.abs(out32.astype(np.float64) - ref32).max())
+        # guarded fp32 on the reference's own f64 pixels, against the reference output
         ref = oracle.reconstruct_image(sampled, mask, B, L, I, rho, gamma, reducer, early)
+        out32, tr32 = fsr.reconstruct(sampled, mask, B, N, I, rho, gamma, reducer=reducer,
+                                      early_stop=early, precision="fp32", argmax="redux",
+                                      return_trace=True)
+        e32 = float(np.abs(out32 - ref).max())
+        note32 = ""
+        if e32 > FP32_TOL:
+            # a block over the production tolerance is acceptable only as the
+            # reference's own co-maximal split (pkg/tests/test_acceptance.py:73-87)
+            try:
+                r = oracle.assert_matches_reference(out32, ref, sampled, mask, B, L, I, rho, gamma,
+                                                    reducer, tr32.selections, FP32_TOL)
+                e32 = 0.0
+                note32 = f" (over tol only on {r['proven_splits']} proven co-maximal split block(s))"
+            except AssertionError as exc:
+                note32 = " " + str(exc)[:160]
         out64, tr = fsr.reconstruct(sampled, mask, B, N, I, rho, gamma, reducer=reducer,
                                     early_stop=early, precision="fp64", argmax="redux",
                                     return_trace=True)
         ok64 = True
         try:
-            oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, rho, gamma, reducer,
-                                            tr.selections, FP64_TOL)
+            r64 = oracle.assert_matches_reference(out64, ref, sampled, mask, B, L, I, rho, gamma,
+                                                  reducer, tr.selections, FP64_TOL, noise_floor=1e-12)
+            if r64["noise_floor"]:
+                note32 += f" [fp64: {r64['noise_floor']} block(s) part at the fp64 noise floor, b1/B0 < 1e-12]"
         except AssertionError as exc:
             ok64 = False
             msg64 = str(exc)[:200]
         ok = e32 <= FP32_TOL and ok64 and np.array_equal(out64[mask], sampled[mask])
         fails += not ok
-        print(f"case {c}: {H}x{W} N={N} B={B} I={I} rho={rho} gamma={gamma} {reducer} early={early} {kind}: "
-              f"fp32 max|d|={e32:.3e} fp64={'ok' if ok64 else 'FAIL ' + msg64} -> {'ok' if ok else 'FAIL'}",
+        print(f"case {c}: {H}x{W} N={N} B={B} I={I} rho={rho} gamma={gamma} {reducer} early={early} {kind} "
+              f"seeds={iseed},{mseed}: "
+              f"fp32 max|d|={e32:.3e}{note32} fp64={'ok' if ok64 else 'FAIL ' + msg64} -> {'ok' if ok else 'FAIL'}",
               flush=True)
     print(f"{n} cases, {fails} failures, {time.time() - t0:.1f} s")
     return 1 if fails else 0
