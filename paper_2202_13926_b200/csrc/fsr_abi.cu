@@ -877,25 +877,6 @@ inline void chunk_rows(int64_t row0, int64_t row1, int c, int K, int64_t &r0, in
     r1 = row0 + (row1 - row0) * (c + 1) / K;
 }
 
-// Host-buffer calls taper the first and last chunk to half size: the first
-// chunk's staging + H2D and the last chunk's D2H + copy-out are the only copies
-// not hidden under other chunks' kernels (FSR_TAPER=0: uniform chunks).
-inline void host_chunk_rows(int64_t row0, int64_t row1, int c, int K, int64_t &r0, int64_t &r1) {
-    static const bool taper = [] {
-        const char *e = std::getenv("FSR_TAPER");
-        return !(e && *e == '0');
-    }();
-    if (!taper || K < 4) return chunk_rows(row0, row1, c, K, r0, r1);
-    // weights 1/2, 1, ..., 1, 1/2 over K chunks: cumulative position of chunk c
-    const double total = K - 1.0;
-    auto pos = [&](int i) -> int64_t {
-        const double w = i == 0 ? 0.0 : i >= K ? total : 0.5 + (i - 1);
-        return row0 + (int64_t)((row1 - row0) * w / total + 0.5);
-    };
-    r0 = pos(c);
-    r1 = pos(c + 1);
-}
-
 // Per-call scratch of device d: the call counter, K chunk counters and the empty
 // list (capacity nb blocks), zeroed on d.stream after the engine's previous call.
 int begin_call(fsr_engine *eng, Device &d, int K, int64_t nb, cudaStream_t st) {
@@ -1042,7 +1023,7 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         while (ld.pending)
             if ((rc = drain_one())) return rc;
         int64_t r0, r1;
-        host_chunk_rows(hp.row0, hp.row1, c, K, r0, r1);
+        chunk_rows(hp.row0, hp.row1, c, K, r0, r1);  // (half-size first/last chunks: measured no gain)
         const int64_t ya = std::max<int64_t>(0, r0 * B - L), yb = std::min<int64_t>(H, r1 * B + L);
         const int64_t oa = std::min<int64_t>(H, r0 * B), ob = std::min<int64_t>(H, r1 * B);
         const int64_t rows_in = yb - ya, rows_out = ob - oa, nb = (r1 - r0) * bcols;
