@@ -725,8 +725,8 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             a.key_mask = 0xffffffc0u;  // 6 rank bits (row u of 64)
             LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, d.sms, st)));
         } else if (fast16) {
-            // (warpseg with two blocks per warp was measured slower at N = 16:
-            // 2.48 vs 2.21 ms at 1080p -- 16 KiB of tables per warp and 7-bit tags)
+            // (warpseg with two blocks per warp measured 8 % slower at N = 16, 1080p:
+            // 2.39 vs 2.21 ms; warp16's two lanes per column already issue 70 %)
             LAUNCH_TRY(eng, d, (warp16_any<IO>(a, maps, tree, p->argmax_impl, guarded, opts, d.sms, st)));
         } else if (fastn && N <= 8 && p->block <= 4 && d.segmented) {
             LAUNCH_TRY(eng, d, (warpseg_any<IO>(a, N, guarded, opts, d.sms, st)));

@@ -6,16 +6,17 @@
 // block.  Here every lane owns spectral column v = lane % N of block
 // lane / N, so all 32 lanes work and one tail serves 32 / N blocks:
 //   per lane   P = N/2 packed row pairs (i, i + P), FFMA2 update + objective,
-//              one LDS.128 per pair from the segment's row-pair table; the
-//              half swap of pu >= P (warp-uniform in warp32) differs between
-//              segments, so each segment keeps U and its half-swapped copy U'
-//              and a lane picks the table by pointer (no per-pair selects)
-//   keys       the pair's larger objective with (pair << log2 N | v) in the
-//              low bits (5 for N <= 8; 7 for N = 16, whose 2^-16 truncation the
-//              guard adds to tau): unique within a segment, so a log2(N)-step xor
-//              butterfly (never leaves the segment) yields the winner's pair
-//              and lane; any maximal bin may win (guarded: every near-tie is
-//              re-run in fp64; the Hermitian phase keeps the canonical halves)
+//              one LDS.128 per pair from the segment's row-pair table.  warp32
+//              swaps the float4 halves for pu >= P (warp-uniform there); here
+//              pu differs between segments, so the table is extended by P rows
+//              (U[N + k] = U[k]): since U[k + P] is U[k] with its halves
+//              swapped, pair i reads row i + P - pu + (pu >= P ? N : 0), which
+//              never wraps and never needs the swap
+//   keys       the pair's larger objective with the pair index in the 5 low
+//              bits; a log2(N)-step xor butterfly (never leaves the segment)
+//              gives the segment's maximum and a ballot its lane; any maximal
+//              bin may win (guarded: every near-tie is re-run in fp64; the
+//              Hermitian phase keeps the canonical halves)
 //   pick       the winning pair by a select chain (the pair differs between
 //              segments, so no warp-uniform indirect branch)
 //   guard      per-lane top-2 of the pair maxima, the winner's partner
@@ -35,16 +36,16 @@ struct SegCfg {
     static constexpr int P = N / 2;
     static constexpr int BPW = 32 / N;                 // blocks (segments) per warp
     static constexpr int LV = N == 16 ? 4 : N == 8 ? 3 : 2;  // log2 N
-    static constexpr int TAG = LV + (N == 16 ? 3 : N == 8 ? 2 : 1) > 5 ? 7 : 5;  // low key bits
-    static constexpr uint32_t KMASK = ~((1u << TAG) - 1u);
-    static constexpr float TSLACK = TAG > 5 ? 1.0f / 65536.0f : 0.f;  // key truncation (relative)
+    static constexpr uint32_t KMASK = ~31u;            // 5 low key bits: the pair index
+    static constexpr uint32_t SEGMASK = N == 32 ? 0xffffffffu : (1u << N) - 1u;
     static constexpr int TILE = N * (N + 1) * 16;
-    static constexpr int UTAB = N * N * 16;
-    static constexpr int SEG = TILE > 2 * UTAB ? TILE : 2 * UTAB;  // bytes per segment
+    static constexpr int UROWS = 3 * P;                // row-pair table rows, extended (below)
+    static constexpr int UTAB = UROWS * N * 16;
+    static constexpr int SEG = TILE > UTAB ? TILE : UTAB;  // bytes per segment
     static constexpr int SEG_F4 = SEG / 16;
     static constexpr int NPIX = (16 + N - 1) / N;      // target pixels per lane (B <= 4)
     static_assert(N == 4 || N == 8 || N == 16, "segmented kernel: N in {4, 8, 16}");
-    static_assert(((P - 1) << LV) + N - 1 < (1 << TAG), "pair and lane tags fit the key bits");
+    static_assert(P <= 32, "the pair index fits the 5 key bits");
 };
 
 template <int N, int WARPS>
@@ -107,7 +108,7 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
 #define FSR_SEG_WARPS_PER_SM 32     // N <= 8 (64 registers)
 #endif
 #ifndef FSR_SEG16_WARPS_PER_SM
-#define FSR_SEG16_WARPS_PER_SM 12   // N = 16: 16 KiB of tables per warp
+#define FSR_SEG16_WARPS_PER_SM 16   // N = 16: 12 KiB of tables per warp
 #endif
 template <int N>
 constexpr int seg_warps_per_sm() { return N == 16 ? FSR_SEG16_WARPS_PER_SM : FSR_SEG_WARPS_PER_SM; }
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
     const int sg = lane / N, v = lane % N, sbase = sg * N;
     float4 *segbuf = sm.seg[wid][sg];
     double2 *t = reinterpret_cast<double2 *>(segbuf);
-    float4 *U = segbuf, *Us = segbuf + N * N;  // row-pair table and its half-swapped copy
+    float4 *U = segbuf;  // row-pair table, 3P rows (rows N.. repeat rows 0..P-1)
     uint32_t canon = 0;
 #pragma unroll
     for (int u = 0; u < N; ++u) {
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
 #pragma unroll
     for (int i = 0; i < P; ++i) {
         wf2[i] = make_float2(__ldg(a.wf + i * N + v), __ldg(a.wf + (i + P) * N + v));
-        tag[i] = ((uint32_t)i << C::LV) | (uint32_t)v;
+        tag[i] = (uint32_t)i;
     }
     const int64_t stride = (int64_t)gridDim.x * WARPS * C::BPW;
     for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * C::BPW; base < a.nblocks; base += stride) {
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
         for (int k = 0; k < N; ++k) {
             const int k2 = (k + P) % N;
             U[k * N + v] = make_float4(Wf[k2].x, Wf[k].x, Wf[k2].y, Wf[k].y);
-            Us[k * N + v] = make_float4(Wf[k].x, Wf[k2].x, Wf[k].y, Wf[k2].y);
+            if (k < P) U[(k + N) * N + v] = make_float4(Wf[k2].x, Wf[k].x, Wf[k2].y, Wf[k].y);
         }
         __syncwarp();
         const float w00 = U[P * N].x;  // Wx[0][0] = sum of the weights
@@ -245,8 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
             constexpr bool H = decltype(hconst)::value;
             int col = v - pv;
             col += col < 0 ? N : 0;
-            const int pr = pu >= P ? pu - P : pu;
-            const float4 *up = (pu >= P ? Us : U) + (P - pr) * N + col;
+            const float4 *up = U + (P - pu + (pu >= P ? N : 0)) * N + col;
             const uint32_t cn = (H && herm) ? canon : 0xffffffffu;
             uint32_t m1, m2;
             if (H && it == 0)
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
                 seg_pass<N, GUARD, H, true, C::KMASK>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
             if (!live) m1 = m2 = 0u;
             const uint32_t kmax = seg_max<N>(m1);
-            const int wl = (int)(kmax & (N - 1)), j = (int)((kmax >> C::LV) & (P - 1));
+            const uint32_t bal = (__ballot_sync(0xffffffffu, m1 == kmax) >> sbase) & C::SEGMASK;
+            const int wl = __ffs(bal) - 1, j = (int)(kmax & 31u);
             const float b1 = __uint_as_float(kmax & C::KMASK);
             bool go = live;
             if (EARLY && live && b1 < thr) {
@@ -301,7 +302,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
                 const uint32_t kp = f2u(po) & C::KMASK;
                 const uint32_t k2 = seg_max<N>(v == wl ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & C::KMASK);
-                const float omt = a.omt - C::TSLACK;  // keys truncated to 2^-(23-TAG)
+                const float omt = a.omt;
                 float gap;
                 if (KAPPA) {
                     const float sb1 = sqrt_approx(b1);
