@@ -187,6 +187,9 @@ struct Device {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_done = nullptr;  // end of the engine's last call on this device (calls are serialised)
     DevBuf px, mask, out, sel, done, empty_list, rerun_list, call_ctr, chunk_ctrs, fill_partials;
+    DevBuf rerun_kf, rerun_seq;  // replay records of the guarded N = 32 kernel (per re-run slot)
+    int replay_min_iters = 101;  // replay the fp64 re-runs' unambiguous prefix from this I on
+                                 // (FSR_REPLAY_MIN; 0 = never)
     DevBuf R, G, W, wf, thr, obj, ties, partials, c64scratch;
     HostBuf hin, hout;  // pinned staging of a lane's chunk (host-buffer calls)
     std::map<std::pair<int, double>, std::unique_ptr<TableSet>> tables;
@@ -585,6 +588,15 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
+    // replay (N = 32, redux argmax): the fp32 kernel records each flagged block's
+    // selections up to its first ambiguous iteration; pair64 replays them without
+    // the objective / argmax, then searches in fp64 from there
+    const bool replay = guarded && warp32_eligible(p) && p->argmax_impl == FSR_ARGMAX_REDUX &&
+                        d.replay_min_iters > 0 && p->iterations >= d.replay_min_iters;
+    if (replay) {
+        CUDA_TRY(eng, d.rerun_kf.ensure((size_t)nblocks * sizeof(int32_t)));
+        CUDA_TRY(eng, d.rerun_seq.ensure((size_t)nblocks * p->iterations * sizeof(uint16_t)));
+    }
     const int gen_grid = d.sms * 8;
     int rc = FSR_OK;
     // the fp32-loop kernels take f32 or f64 pixels (the reference's own input
@@ -692,6 +704,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         a.omt = 1.f - a.tau;
         a.kappa = (float)guard_kappa_for(p);
         a.tree = p->reducer == FSR_REDUCER_TREE;
+        if (replay) {
+            a.rerun_kf = d.rerun_kf.as<int32_t>();
+            a.rerun_seq = d.rerun_seq.as<uint16_t>();
+            a.seq_stride = p->iterations;
+        }
         a.wf = tf.wf;
         a.sel = sel;
         a.done = done;
@@ -716,7 +733,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         const bool tree = p->reducer == FSR_REDUCER_TREE;
         // trace / early-stop code only in the launches that need it
         const int opts = (sel ? LOPT_TRACE : 0) | (p->early_stop ? LOPT_EARLY : 0) |
-                         (guarded && a.kappa > 0.f ? LOPT_KAPPA : 0);
+                         (guarded && a.kappa > 0.f ? LOPT_KAPPA : 0) | (replay ? LOPT_REPLAY : 0);
         const int nsup = fast64 ? 64 : fast16 ? 16 : fastn ? N : 32;
         a.use_tma = (d.tma_enabled &&
                      window_maps<IO>(tpx, px_pitch, tmk, mask_pitch, ty1 - ty0, W, &maps, nsup)) ? 1 : 0;
@@ -781,6 +798,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &cc->rerun_count;
+            if (replay) {
+                r.list_kf = d.rerun_kf.as<int32_t>();
+                r.list_seq = d.rerun_seq.as<uint16_t>();
+                r.seq_stride = p->iterations;
+            }
             if ((rc = launch_fp64_n32<IO>(eng, d, r, p, (int64_t)d.sms * 16, st))) return rc;
         }
     }
@@ -858,6 +880,7 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
         ln->sms = d.sms;
         ln->tma_enabled = d.tma_enabled;
         ln->segmented = d.segmented;
+        ln->replay_min_iters = d.replay_min_iters;
         CUDA_TRY(eng, cudaStreamCreateWithFlags(&ln->stream, cudaStreamNonBlocking));
         CUDA_TRY(eng, cudaEventCreateWithFlags(&ln->ev0, cudaEventDisableTiming));
         CUDA_TRY(eng, cudaEventCreate(&ln->ev1));
@@ -1263,6 +1286,8 @@ int fsr_engine_create(const int32_t *devices, int32_t n_devices, fsr_engine **ou
         d->chunking = !(no_chunk && *no_chunk && *no_chunk != '0');
         const char *no_seg = std::getenv("FSR_NO_SEG");  // A/B switch for the segmented small-N kernel
         d->segmented = !(no_seg && *no_seg && *no_seg != '0');
+        const char *rmin = std::getenv("FSR_REPLAY_MIN");  // A/B: smallest I that replays (0 = never)
+        if (rmin && *rmin) d->replay_min_iters = atoi(rmin);
         CUDA_TRY(nullptr, cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev0));
         CUDA_TRY(nullptr, cudaEventCreate(&d->ev1));
@@ -1283,7 +1308,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
         d.pool.reset();
         for (auto &ln : d.lanes) {
             cudaStreamSynchronize(ln->stream);
-            for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->rerun_list,
+            for (DevBuf *b : {&ln->px, &ln->mask, &ln->out, &ln->sel, &ln->done, &ln->rerun_list, &ln->rerun_kf, &ln->rerun_seq,
                               &ln->c64scratch})
                 b->release();
             ln->hin.release();
@@ -1296,7 +1321,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
             cudaEventDestroy(ln->ev1);
             cudaStreamDestroy(ln->stream);
         }
-        for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list,
+        for (DevBuf *b : {&d.px, &d.mask, &d.out, &d.sel, &d.done, &d.empty_list, &d.rerun_list, &d.rerun_kf, &d.rerun_seq,
                           &d.call_ctr, &d.chunk_ctrs, &d.fill_partials, &d.R, &d.G, &d.W, &d.wf,
                           &d.thr, &d.obj, &d.ties, &d.partials, &d.c64scratch})
             b->release();

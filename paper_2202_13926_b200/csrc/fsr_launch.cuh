@@ -19,7 +19,7 @@ namespace fsr {
 constexpr cudaError_t kNotBuilt = cudaErrorNotYetImplemented;
 
 // OPTS bits for the fp32 kernels (trace / early-stop code compiled in)
-constexpr int LOPT_TRACE = 1, LOPT_EARLY = 2, LOPT_KAPPA = 4;  // = W32_TRACE/EARLY/KAPPA
+constexpr int LOPT_TRACE = 1, LOPT_EARLY = 2, LOPT_KAPPA = 4, LOPT_REPLAY = 8;  // = W32_*
 
 // N = 32 fp32 loop (fsr_warp32.cuh).  study: guard-study instrumentation
 // (tools/guard_study.py; redux, f32 pixels only).

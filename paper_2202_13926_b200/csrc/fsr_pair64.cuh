@@ -59,6 +59,12 @@ struct Pair64Args {
     int32_t *empty_list;
     double2 *scratch;               // cta64d: per-CTA 64 KiB staging of W (null elsewhere)
     int tree;                       // reducer for kernels that take it at run time (warpnd)
+    // replay (pair64 list mode): list entry b re-runs iterations [0, list_kf[b]) as
+    // argmax-free updates along the fp32 kernel's selections list_seq[b * seq_stride + j]
+    // (u * 32 + v), whose decisions the guard found unambiguous, then searches in fp64
+    const int32_t *list_kf;
+    const uint16_t *list_seq;
+    int seq_stride;
 };
 
 struct __align__(16) PairSlot {
@@ -193,6 +199,26 @@ __device__ __forceinline__ double2 pick16_brx(const cpx<double> (&R)[16], int i)
 // flat index); every bin's key is unique, so a plain u64 max is the argmax.
 __device__ __forceinline__ unsigned long long u64max(unsigned long long a, unsigned long long b) {
     return a > b ? a : b;
+}
+
+// The residual update alone (replayed iterations): R -= gp W(. - pu, . - pv).
+template <int H>
+__device__ __forceinline__ void p64_update(cpx<double> (&R)[16], uint32_t P, uint32_t ycv, double gr,
+                                           double gi) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int u = p64_row(H, i);
+        const uint32_t addr = ((P + ((uint32_t)u << 9)) & 0x3E00u) | ycv;
+        double2 w;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "r"(addr));
+        double re = R[i].re, im = R[i].im;
+        re = fma(-gr, w.x, re);
+        re = fma(gi, w.y, re);
+        im = fma(-gr, w.y, im);
+        im = fma(-gi, w.x, im);
+        R[i].re = re;
+        R[i].im = im;
+    }
 }
 
 // One residual-update + objective pass over the 16 rows of half H.
@@ -423,7 +449,41 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
         const uint32_t cmask = 0x3FFu;
         SelEntry *hist = sm.hist[pair][H];
         int done = 0;
+        const int kf = a.list_kf ? a.list_kf[bi] : 0;
+        const uint16_t *seq = a.list_kf ? a.list_seq + bi * (int64_t)a.seq_stride : nullptr;
         for (int it = 0; it < a.iterations; ++it) {
+            if (it < kf) {
+                // replayed iteration: the selection is known, only the update runs;
+                // the half holding row wu publishes R[wu][wv] (one pair barrier)
+                const uint32_t s = seq[it];
+                const int wu = (int)(s >> 5), wv = (int)(s & 31u);
+                if (it > 0) p64_update<H>(R, P, ycv, gr, gi);
+                const int hold = p64_slot(0, wu) >= 0 ? 0 : 1;
+                PairSlot *ps = &sm.slot[pair][parity][0];
+                if (H == hold) {
+                    const double2 cw = pick16_brx(R, p64_slot(H, wu) & 15);
+                    if (lane == wv) {
+                        ps[H].cre = cw.x;
+                        ps[H].cim = cw.y;
+                    }
+                }
+                bar_pair(bar_id);
+                const double2 c = make_double2(ps[hold].cre, ps[hold].cim);
+                parity ^= 1;
+                if (H == 0 && sel_b && lane == 0) sel_b[it] = wu * 32 + wv;
+                gr = c.x * ginv;
+                gi = c.y * ginv;
+                P = (uint32_t)((32 - wu) & 31) << 9;
+                ycv = wb | ((uint32_t)((lane - wv) & 31) << 4);
+                if ((it & 1) == H && lane == 0) hist[(it >> 1) & 15] = SelEntry{gr, gi, wu, wv, {0, 0}};
+                if ((it & 31) == 31) {
+                    __syncwarp();
+                    acc = p64_flush(sm, hist, 16, pm, pn, acc);
+                    __syncwarp();
+                }
+                done = it + 1;
+                continue;
+            }
             unsigned long long kb = it == 0
                 ? p64_pass<H, TREE, false>(R, wfr, P, ycv, gr, gi, cmask)
                 : p64_pass<H, TREE, true>(R, wfr, P, ycv, gr, gi, cmask);

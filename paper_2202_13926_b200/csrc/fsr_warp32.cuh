@@ -84,6 +84,11 @@ struct Warp32Args {
     float omt;             // 1 - tau in fp32 (a parameter operand rather than a live register)
     float kappa;           // guard: scale term, near-tie iff b1 - b2 <= tau b1 + kappa sqrt(b1 B0)
     int tree;              // reducer (tree 1 / linear 0) for kernels that take it at run time (warpn)
+    // replay recording (W32_REPLAY): per re-run slot the first flagged iteration and the
+    // selections before it (u * 32 + v), for the fp64 re-run's argmax-free prefix
+    int32_t *rerun_kf;
+    uint16_t *rerun_seq;
+    int seq_stride;
 };
 
 // 2-D tensor maps of the pixel (f32) and mask (u8) images, zero fill outside
@@ -521,6 +526,9 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
 // W32_KAPPA the guard's scale term; production launches without them carry no
 // per-iteration work for either (the scale term's sqrt costs ~1 % of the loop).
 constexpr int W32_TRACE = 1, W32_EARLY = 2, W32_KAPPA = 4, W32_ALL = 7;
+// W32_REPLAY: record the selections and the first flagged iteration (dynamic shared
+// memory: WARPS * seq_stride u16 after Warp32Smem) for the fp64 re-run's replay
+constexpr int W32_REPLAY = 8;
 
 #ifndef FSR_W32_WARPS_PER_SM
 #define FSR_W32_WARPS_PER_SM 12  // resident warps (blocks) per SM the register budget targets
@@ -530,6 +538,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     warp32_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     constexpr bool TRACE = (OPTS & W32_TRACE) != 0, EARLY = (OPTS & W32_EARLY) != 0;
     constexpr bool KAPPA = (OPTS & W32_KAPPA) != 0;
+    constexpr bool REC = GUARD && (OPTS & W32_REPLAY) != 0;
     // pair keys (one key per row pair, half resolved after the argmax): exact ties
     // between bins are ordered differently than the reference, so only where the
     // guard re-runs every near-tie in fp64 anyway
@@ -543,6 +552,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
     __shared__ float2 w32_cs[32];  // cos/sin(2 pi j / 32), static: a constant shared address
     Warp32Smem<WARPS> &sm = *reinterpret_cast<Warp32Smem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
+    uint16_t *seqw = REC ? reinterpret_cast<uint16_t *>(smem_raw + sizeof(Warp32Smem<WARPS>)) +
+                               wid * a.seq_stride
+                         : nullptr;
     if (threadIdx.x < 32) {
         const double th = 6.283185307179586476925286766559 * threadIdx.x / 32.0;
         w32_cs[threadIdx.x] = make_float2((float)cos(th), (float)sin(th));
@@ -616,6 +628,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         // the guard's main test accumulated as a float: flagged iff fl >= 0
         // (b2 >= b1 (1 - tau) <=> b2 - b1 (1 - tau) >= 0, exact in float)
         float fl = -1.f;
+        int kf = -1;  // REC: the first flagged iteration
         float ks = 0.f;  // kappa sqrt(B0), B0 = the block's first maximum (set at it = 0)
         // One greedy iteration; H: the state is still exactly Hermitian.  The
         // Hermitian phase (a few iterations at most) and the rest run as two
@@ -652,7 +665,10 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             int bu = PK ? (int)(kmax & 15u) : LT ? (int)bitrev5(urank) : (int)urank;  // PK: the pair
             const float b1 = __uint_as_float(kmax & ~31u);
             if (EARLY && b1 < thr) {  // thr == 0 unless early stop is on
-                if (GUARD && b1 >= thr * a.omt) flagged = true;  // a stop decision within tau
+                if (GUARD && b1 >= thr * a.omt) {  // a stop decision within tau
+                    flagged = true;
+                    if (REC && kf < 0) kf = it;
+                }
                 return false;
             }
             float2 wfp;
@@ -680,6 +696,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             }
             const bool lo = bu < 16;
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
+            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 32 + bv);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             gr = c.x * ginv;
@@ -708,15 +725,22 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                                                       ((int)(tid & 31u) == wl) ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
                 // near-tie iff b2 >= b1 (1 - tau) - ks sqrt(b1), ks = kappa sqrt(B0)
+                float gtest;
                 if (KAPPA) {
                     const float sb1 = sqrt_approx(b1);
                     if (H && it == 0) ks = a.kappa * sb1;
-                    fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                    gtest = b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt));
                 } else {
-                    fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));  // no FMA contraction: same test
+                    gtest = b2 - __fmul_rn(b1, a.omt);  // no FMA contraction: same test
                 }
+                fl = fmaxf(fl, gtest);
+                if (REC && kf < 0 && gtest >= 0.f) kf = it;
                 // a continue decision within tau of the stop threshold is ambiguous too
-                if (EARLY) flagged |= b1 * a.omt < thr;
+                if (EARLY) {
+                    const bool near_stop = b1 * a.omt < thr;
+                    flagged |= near_stop;
+                    if (REC && near_stop && kf < 0) kf = it;
+                }
                 if (STUDY) {  // guard-study instrumentation (tools/guard_study.py)
                     const float g = b1 > 0.f ? (b1 - b2) / b1 : 1.f;
                     min_gap = fminf(min_gap, g);
@@ -761,9 +785,21 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                 a.gap_out[2 * bid] = min_gap;
                 a.gap_out[2 * bid + 1] = min_gap2;
             }
-            if (GUARD && flagged && a.rerun_list) {
-                unsigned slot = atomicAdd(a.rerun_count, 1u);
+        }
+        if (GUARD && flagged && a.rerun_list) {
+            unsigned slot = 0;
+            if (lane == 0) {
+                slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;
+            }
+            if (REC) {
+                // the unambiguous prefix: selections 0 .. kf-1 for the replay
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                const int n = kf < 0 ? 0 : min(kf, a.seq_stride);
+                if (lane == 0) a.rerun_kf[slot] = n;
+                __syncwarp();
+                uint16_t *dst = a.rerun_seq + (int64_t)slot * a.seq_stride;
+                for (int j = lane; j < n; j += 32) dst[j] = seqw[j];
             }
         }
         // merge + stitch

@@ -25,7 +25,9 @@ template <typename IO, int AM, bool TREE, bool GUARD, bool STUDY, int OPTS>
 cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_t st) {
     constexpr int WARPS = FSR_W32_CTA_WARPS;
     auto k = warp32_kernel<IO, WARPS, TREE, AM, GUARD, STUDY, OPTS>;
-    const size_t smem = sizeof(Warp32Smem<WARPS>);
+    // W32_REPLAY: the warps' selection records after the struct
+    const size_t smem = sizeof(Warp32Smem<WARPS>) +
+                        ((OPTS & W32_REPLAY) ? ((size_t)WARPS * a.seq_stride * 2 + 15) / 16 * 16 : 0);
     int grid = 1;
     cudaError_t e = persistent_grid(k, WARPS * 32, smem, (a.nblocks + WARPS - 1) / WARPS, sms, &grid);
     if (e != cudaSuccess) return e;
@@ -36,12 +38,20 @@ cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_
 template <typename IO, int AM, bool TREE, bool GUARD>
 cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, int opts, int sms, cudaStream_t st) {
     if (opts == 0) return go<IO, AM, TREE, GUARD, false, 0>(a, maps, sms, st);
-    if constexpr (GUARD)
+    if constexpr (GUARD) {
         if (opts == LOPT_KAPPA) return go<IO, AM, TREE, GUARD, false, LOPT_KAPPA>(a, maps, sms, st);
+        if constexpr (AM == AM_REDUX) {
+            if (opts == LOPT_REPLAY) return go<IO, AM, TREE, GUARD, false, LOPT_REPLAY>(a, maps, sms, st);
+            if (opts == (LOPT_KAPPA | LOPT_REPLAY))
+                return go<IO, AM, TREE, GUARD, false, LOPT_KAPPA | LOPT_REPLAY>(a, maps, sms, st);
+        }
+    }
     if constexpr (AM == AM_REDUX) {
         if (opts == LOPT_TRACE) return go<IO, AM, TREE, GUARD, false, LOPT_TRACE>(a, maps, sms, st);
         if (opts == LOPT_EARLY) return go<IO, AM, TREE, GUARD, false, LOPT_EARLY>(a, maps, sms, st);
     }
+    if constexpr (GUARD && AM == AM_REDUX)
+        if (opts & LOPT_REPLAY) return go<IO, AM, TREE, GUARD, false, W32_ALL | W32_REPLAY>(a, maps, sms, st);
     return go<IO, AM, TREE, GUARD, false, W32_ALL>(a, maps, sms, st);
 }
 }  // namespace
