@@ -715,3 +715,29 @@ def test_guarded_fp32_reports_fp64_service(N, B, I, served):
     sampled, mask = oracle.quarter_sample(img, 3)
     _, tr = fsr.reconstruct(sampled, mask, B, N, I, precision="fp32", return_trace=True)
     assert tr.stats["served_fp64"] is served
+
+
+def test_replay_matches_full_reruns(monkeypatch):
+    """Beyond 100 iterations the N=32 fp64 re-runs replay the fp32 kernel's
+    unambiguous prefix: on this frame the output is bitwise the
+    output of full fp64 re-runs (FSR_REPLAY_MIN=0), and the replayed path stays
+    within the production tolerance of the reference."""
+    from paper_2202_13926_b200 import _lib, frames, synth
+
+    H, W, I = 540, 960, 200
+    img = synth.frame(H, W, 7, "natural")
+    mask = frames.quarter_sample_mask(H, W, 42)
+    px = np.where(mask, img, 0.0)
+    p = _lib.make_params(4, 14, I, precision="fp32")
+    monkeypatch.setenv("FSR_REPLAY_MIN", "1")
+    on = _lib.Engine([0])
+    monkeypatch.setenv("FSR_REPLAY_MIN", "0")
+    off = _lib.Engine([0])
+    o_on = on.reconstruct(px, mask, p)
+    o_off = off.reconstruct(px, mask, p)
+    assert on.last_stats()["rerun_blocks"] == off.last_stats()["rerun_blocks"] > 0
+    assert np.array_equal(o_on, o_off)
+    rows = (60, 72)  # a band of block rows against the reference restatement
+    ref = oracle.reconstruct_image(px, mask, 4, 14, I, 0.7, 0.5, "tree", block_rows=rows)
+    y0, y1 = rows[0] * 4, rows[1] * 4
+    assert float(np.abs(o_on[y0:y1] - ref[y0:y1]).max()) <= FP32_TOL
