@@ -187,7 +187,7 @@ struct Device {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_done = nullptr;  // end of the engine's last call on this device (calls are serialised)
     DevBuf px, mask, out, sel, done, empty_list, rerun_list, call_ctr, chunk_ctrs, fill_partials;
-    DevBuf rerun_kf, rerun_seq;  // replay records of the guarded N = 32 kernel (per re-run slot)
+    DevBuf rerun_kf, rerun_seq;  // replay records of the guarded N = 32 / 16 kernels (per re-run slot)
     int replay_min_iters = 101;  // replay the fp64 re-runs' unambiguous prefix from this I on
                                  // (FSR_REPLAY_MIN; 0 = never)
     DevBuf R, G, W, wf, thr, obj, ties, partials, c64scratch;
@@ -588,11 +588,12 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
-    // replay (N = 32, redux argmax): the fp32 kernel records each flagged block's
-    // selections up to its first ambiguous iteration; pair64 replays them without
+    // replay (N = 32 and 16, redux argmax): the fp32 kernel records each flagged block's
+    // selections up to its first ambiguous iteration; pair64 / warp16d replay them without
     // the objective / argmax, then searches in fp64 from there
-    const bool replay = guarded && warp32_eligible(p) && p->argmax_impl == FSR_ARGMAX_REDUX &&
-                        d.replay_min_iters > 0 && p->iterations >= d.replay_min_iters;
+    const bool replay = guarded && (warp32_eligible(p) || warp16_eligible(p)) &&
+                        p->argmax_impl == FSR_ARGMAX_REDUX && d.replay_min_iters > 0 &&
+                        p->iterations >= d.replay_min_iters;
     if (replay) {
         CUDA_TRY(eng, d.rerun_kf.ensure((size_t)nblocks * sizeof(int32_t)));
         CUDA_TRY(eng, d.rerun_seq.ensure((size_t)nblocks * p->iterations * sizeof(uint16_t)));
@@ -786,6 +787,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &cc->rerun_count;
+            if (replay) {
+                r.list_kf = d.rerun_kf.as<int32_t>();
+                r.list_seq = d.rerun_seq.as<uint16_t>();
+                r.seq_stride = p->iterations;
+            }
             if ((rc = launch_warp16d<IO>(eng, d, r, p->reducer == FSR_REDUCER_TREE, p->argmax_impl,
                                          (int64_t)d.sms * 16, st)))
                 return rc;

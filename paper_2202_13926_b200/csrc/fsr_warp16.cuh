@@ -230,6 +230,10 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
     constexpr bool LT = TREE && !GUARD;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp16Smem<WARPS> &sm = *reinterpret_cast<Warp16Smem<WARPS> *>(smem_raw);
+    constexpr bool REC = GUARD && (OPTS & W32_REPLAY) != 0;  // replay records (see warp32)
+    uint16_t *seqw = REC ? reinterpret_cast<uint16_t *>(smem_raw + sizeof(Warp16Smem<WARPS>)) +
+                               warp_id() * a.seq_stride
+                         : nullptr;
     const int lane = lane_id(), wid = warp_id();
     if (threadIdx.x < 16) {
         const double th = 6.283185307179586476925286766559 * threadIdx.x / 16.0;
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
         int it = 0;
         float fl = -1.f;  // guard test as a float max (see warp32): flagged iff fl >= 0
         float ks = 0.f;   // kappa sqrt(B0) (see warp32)
+        int kf = -1;      // REC: the first flagged iteration
         // one iteration; H: Hermitian phase (run as its own loop, see warp32)
         // synthesis deferred by one iteration (see warp32)
         int sidx = 0;
@@ -324,8 +329,12 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             const int bv = LT ? (int)bitrev4((uint32_t)(wl >> 1)) : (wl >> 1);
             const float b1 = __uint_as_float(kmax & ~31u);
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
+            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 16 + bv);
             if (EARLY && b1 < thr) {
-                if (GUARD && b1 >= thr * a.omt) flagged = true;
+                if (GUARD && b1 >= thr * a.omt) {
+                    flagged = true;
+                    if (REC && kf < 0) kf = it;
+                }
                 return false;
             }
             float4 q;
@@ -345,14 +354,21 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             if (GUARD) {
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
+                float gtest;
                 if (KAPPA) {  // scale term (see warp32)
                     const float sb1 = sqrt_approx(b1);
                     if (H && it == 0) ks = a.kappa * sb1;
-                    fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                    gtest = b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt));
                 } else {
-                    fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));
+                    gtest = b2 - __fmul_rn(b1, a.omt);
                 }
-                if (EARLY) flagged |= b1 * a.omt < thr;
+                fl = fmaxf(fl, gtest);
+                if (REC && kf < 0 && gtest >= 0.f) kf = it;
+                if (EARLY) {
+                    const bool near_stop = b1 * a.omt < thr;
+                    flagged |= near_stop;
+                    if (REC && near_stop && kf < 0) kf = it;
+                }
             }
             if (H) herm = ((bu & 7) == 0) && ((bv & 7) == 0);
             sidx = (bu * pm + bv * pn) & 15;
@@ -374,11 +390,20 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
         const int done = it;
         if (sel_b)
             for (int jj = done + lane; jj < a.iterations; jj += 32) sel_b[jj] = -1;
-        if (lane == 0) {
-            if (a.done) a.done[bid] = done;
-            if (GUARD && flagged && a.rerun_list) {
-                unsigned slot = atomicAdd(a.rerun_count, 1u);
+        if (lane == 0 && a.done) a.done[bid] = done;
+        if (GUARD && flagged && a.rerun_list) {
+            unsigned slot = 0;
+            if (lane == 0) {
+                slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;
+            }
+            if (REC) {
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                const int n = kf < 0 ? 0 : min(kf, a.seq_stride);
+                if (lane == 0) a.rerun_kf[slot] = n;
+                __syncwarp();
+                uint16_t *dst = a.rerun_seq + (int64_t)slot * a.seq_stride;
+                for (int jj = lane; jj < n; jj += 32) dst[jj] = seqw[jj];
             }
         }
         if (lane < a.B * a.B) {
@@ -490,7 +515,7 @@ __device__ __forceinline__ double w16d_prologue(const Pair64Args<IO> &a, double2
     return energy;
 }
 
-template <bool TREE, bool UPDATE, bool SWAP>
+template <bool TREE, bool UPDATE, bool SWAP, bool OBJ = true>
 __device__ __forceinline__ unsigned long long pass16d(double (&rre)[8], double (&rim)[8],
                                                       const double (&wf)[8], const double2 *pux,
                                                       const double2 *puy, double gr, double gi) {
@@ -516,12 +541,14 @@ __device__ __forceinline__ unsigned long long pass16d(double (&rre)[8], double (
                 rre[j] = re;
                 rim[j] = im;
             }
-            const double o = fma(re, re, im * im) * wf[j];
-            const uint32_t rk = TREE ? bitrev3((uint32_t)j) : (uint32_t)j;
-            const uint32_t lo = ((uint32_t)__double2loint(o) & ~7u) | (7u - rk);
-            const unsigned long long k =
-                ((unsigned long long)(uint32_t)__double2hiint(o) << 32) | (unsigned long long)lo;
-            best[hh] = u64max(best[hh], k);
+            if (OBJ) {
+                const double o = fma(re, re, im * im) * wf[j];
+                const uint32_t rk = TREE ? bitrev3((uint32_t)j) : (uint32_t)j;
+                const uint32_t lo = ((uint32_t)__double2loint(o) & ~7u) | (7u - rk);
+                const unsigned long long k =
+                    ((unsigned long long)(uint32_t)__double2hiint(o) << 32) | (unsigned long long)lo;
+                best[hh] = u64max(best[hh], k);
+            }
         }
     }
     return u64max(best[0], best[1]);
@@ -581,6 +608,40 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16D_WARPS_PER_SM / WARPS) war
         const int pm = a.L + lane / a.B, pn = a.L + lane % a.B;
         double acc = 0.0, gr = 0.0, gi = 0.0;
         int pu = 0, pv = 0, it = 0;
+        // replay (list mode): iterations < kf follow the fp32 kernel's recorded
+        // selections with the update alone (see fsr_pair64.cuh)
+        const int kf = a.list_kf ? a.list_kf[bi] : 0;
+        const uint16_t *seq = a.list_kf ? a.list_seq + bi * (int64_t)a.seq_stride : nullptr;
+        for (; it < kf; ++it) {
+            const int roff = (8 + p - (pu & 7)) * W16_US + ucol16<TREE>((v - pv) & 15);
+            if (it > 0) {
+                if (pu >= 8)
+                    pass16d<TREE, true, true, false>(rre, rim, wf, ux + roff, uy + roff, gr, gi);
+                else
+                    pass16d<TREE, true, false, false>(rre, rim, wf, ux + roff, uy + roff, gr, gi);
+            }
+            const uint32_t s = seq[it];
+            const int bu = (int)(s >> 4), bv = (int)(s & 15u);
+            const int j = bu >> 1;
+            const int wl = ((TREE ? (int)bitrev4((uint32_t)bv) : bv) << 1) | (bu & 1);
+            if (sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
+            double cre, cim;
+            switch (j) {
+#define FSR_P16R(q) \
+    case q: cre = rre[q]; cim = rim[q]; break;
+                FSR_P16R(0) FSR_P16R(1) FSR_P16R(2) FSR_P16R(3) FSR_P16R(4) FSR_P16R(5) FSR_P16R(6)
+                default: cre = rre[7]; cim = rim[7]; break;
+#undef FSR_P16R
+            }
+            cre = __shfl_sync(0xffffffffu, cre, wl);
+            cim = __shfl_sync(0xffffffffu, cim, wl);
+            gr = cre * ginv;
+            gi = cim * ginv;
+            pu = bu;
+            pv = bv;
+            const double2 e = sm.cs[(bu * pm + bv * pn) & 15];
+            acc = fma(gr, e.x, fma(-gi, e.y, acc));
+        }
         for (; it < a.iterations; ++it) {
             const int roff = (8 + p - (pu & 7)) * W16_US + ucol16<TREE>((v - pv) & 15);
             unsigned long long kb;

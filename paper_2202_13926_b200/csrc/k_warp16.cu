@@ -19,7 +19,8 @@ template <typename IO, int AM, bool TREE, bool GUARD, int OPTS>
 cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_t st) {
     constexpr int WARPS = 4;
     auto k = warp16_kernel<IO, WARPS, TREE, AM, GUARD, OPTS>;
-    const size_t smem = sizeof(Warp16Smem<WARPS>);
+    const size_t smem = sizeof(Warp16Smem<WARPS>) +
+                        ((OPTS & W32_REPLAY) ? ((size_t)WARPS * a.seq_stride * 2 + 15) / 16 * 16 : 0);
     int grid = 1;
     cudaError_t e = persistent_grid(k, WARPS * 32, smem, (a.nblocks + WARPS - 1) / WARPS, sms, &grid);
     if (e != cudaSuccess) return e;
@@ -37,6 +38,17 @@ cudaError_t warp16_launch(const Warp32Args &a, const Warp32Maps &maps, bool tree
     }
     if (opts == LOPT_KAPPA && guard)
         return tree ? go<IO, AM, true, true, W32_KAPPA>(a, maps, sms, st) : go<IO, AM, false, true, W32_KAPPA>(a, maps, sms, st);
+    if constexpr (AM == AM_REDUX) {
+        if (guard && opts == LOPT_REPLAY)
+            return tree ? go<IO, AM, true, true, W32_REPLAY>(a, maps, sms, st)
+                        : go<IO, AM, false, true, W32_REPLAY>(a, maps, sms, st);
+        if (guard && opts == (LOPT_KAPPA | LOPT_REPLAY))
+            return tree ? go<IO, AM, true, true, W32_KAPPA | W32_REPLAY>(a, maps, sms, st)
+                        : go<IO, AM, false, true, W32_KAPPA | W32_REPLAY>(a, maps, sms, st);
+        if (guard && (opts & LOPT_REPLAY))
+            return tree ? go<IO, AM, true, true, W32_ALL | W32_REPLAY>(a, maps, sms, st)
+                        : go<IO, AM, false, true, W32_ALL | W32_REPLAY>(a, maps, sms, st);
+    }
     if (tree) return guard ? go<IO, AM, true, true, W32_ALL>(a, maps, sms, st) : go<IO, AM, true, false, W32_ALL>(a, maps, sms, st);
     return guard ? go<IO, AM, false, true, W32_ALL>(a, maps, sms, st) : go<IO, AM, false, false, W32_ALL>(a, maps, sms, st);
 }

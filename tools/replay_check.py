@@ -22,21 +22,22 @@ def engine(replay_min):
 
 def main():
     H, W, I = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (540, 960, 200)
+    N = int(sys.argv[4]) if len(sys.argv) > 4 else 32
     img = synth.frame(H, W, 7, "natural")
     mask = frames.quarter_sample_mask(H, W, 42)
     px = np.where(mask, img, 0.0)
-    p = _lib.make_params(4, 14, I, precision="fp32")
+    p = _lib.make_params(4, (N - 4) // 2, I, precision="fp32")
     on, off = engine(1), engine(0)
     o_on = on.reconstruct(px, mask, p)
     st_on = on.last_stats()
     o_off = off.reconstruct(px, mask, p)
     st_off = off.last_stats()
     diff = np.abs(o_on - o_off)
-    print(f"{H}x{W} I={I}: re-runs {st_on['rerun_blocks']} / {st_off['rerun_blocks']}, "
+    print(f"{H}x{W} N={N} I={I}: re-runs {st_on['rerun_blocks']} / {st_off['rerun_blocks']}, "
           f"pixels differing {int((diff > 0).sum())}, max |d| {diff.max():.3e}, "
           f"kernel ms {st_on['kernel_ms']:.2f} (replay) vs {st_off['kernel_ms']:.2f}")
     if H * W <= 600 * 1000:
-        ref = oracle.reconstruct_image(px, mask, 4, 14, I, 0.7, 0.5, "tree")
+        ref = oracle.reconstruct_image(px, mask, 4, (N - 4) // 2, I, 0.7, 0.5, "tree")
         print(f"  vs reference: replay max |d| {np.abs(o_on - ref).max() / 255:.3e}, "
               f"full re-run {np.abs(o_off - ref).max() / 255:.3e} (0..1)")
 
