@@ -588,10 +588,12 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     CUDA_TRY(eng, cudaEventRecord(ev_main0, st));
     const bool guarded = p->precision == FSR_PREC_FP32;
     if (guarded) CUDA_TRY(eng, d.rerun_list.ensure((size_t)nblocks * sizeof(int32_t)));
-    // replay (N = 32 and 16, redux argmax): the fp32 kernel records each flagged block's
-    // selections up to its first ambiguous iteration; pair64 / warp16d replay them without
+    // replay (N = 16, 32, 64; redux argmax): the fp32 kernel records each flagged block's
+    // selections up to its first ambiguous iteration; warp16d / pair64 / cta64d replay them without
     // the objective / argmax, then searches in fp64 from there
-    const bool replay = guarded && (warp32_eligible(p) || warp16_eligible(p)) &&
+    // (the segmented N <= 8 kernel does not record: its re-runs are cheap)
+    const bool replay = guarded && (warp32_eligible(p) || warp16_eligible(p) || cta64_eligible(p) ||
+                                    (warpn_eligible(p) && N == 24)) &&
                         p->argmax_impl == FSR_ARGMAX_REDUX && d.replay_min_iters > 0 &&
                         p->iterations >= d.replay_min_iters;
     if (replay) {
@@ -741,7 +743,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
         d.used_tma = a.use_tma;
         if (fast64) {
             a.key_mask = 0xffffffc0u;  // 6 rank bits (row u of 64)
-            LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, d.sms, st)));
+            LAUNCH_TRY(eng, d, (cta64_any<IO>(a, maps, p->argmax_impl, guarded, opts, d.sms, st)));
         } else if (fast16) {
             // (warpseg with two blocks per warp measured 8 % slower at N = 16, 1080p:
             // 2.39 vs 2.21 ms; warp16's two lanes per column already issue 70 %)
@@ -767,6 +769,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &cc->rerun_count;
+            if (replay) {
+                r.list_kf = d.rerun_kf.as<int32_t>();
+                r.list_seq = d.rerun_seq.as<uint16_t>();
+                r.seq_stride = p->iterations;
+            }
             if ((rc = launch_cta64d<IO>(eng, d, r, (int64_t)d.sms, st))) return rc;
         } else if (guarded && fastn) {
             // fp64 re-run of ambiguous blocks on the fp64 one-warp kernel (list mode)
@@ -777,6 +784,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
                                                &cc->skip_empty /* empties already counted */, nullptr);
             r.list = d.rerun_list.as<int32_t>();
             r.list_count = &cc->rerun_count;
+            if (replay) {
+                r.list_kf = d.rerun_kf.as<int32_t>();
+                r.list_seq = d.rerun_seq.as<uint16_t>();
+                r.seq_stride = p->iterations;
+            }
             if ((rc = launch_warpnd<IO>(eng, d, r, N, p->argmax_impl, (int64_t)d.sms * 16, st))) return rc;
         } else if (guarded && fast16) {
             // fp64 re-run of ambiguous blocks on the N=16 fp64 register kernel (list mode)

@@ -54,6 +54,7 @@ struct C64Smem {
     unsigned int red_key[4][32], red_rank[4][32];
     double esum[4];
     unsigned long long bar;
+    unsigned int rec_slot;  // replay records: the block's re-run slot
 };
 
 __device__ __forceinline__ int c64_pos(int f) { return ((f & 15) << 2) | (f >> 4); }
@@ -164,13 +165,16 @@ __device__ __forceinline__ void pass64(float2 (&re)[16], float2 (&im)[16], const
 #ifndef FSR_C64_PAIRKEY
 #define FSR_C64_PAIRKEY 1
 #endif
-template <typename IO, int ARGMAX, bool GUARD>
+template <typename IO, int ARGMAX, bool GUARD, int OPTS = 0>
 __global__ void __launch_bounds__(C64_THREADS, 3)
     cta64_kernel(Warp32Args a, const __grid_constant__ Warp32Maps maps) {
     // pair keys in guarded mode (every near-tie is re-run in fp64, see warp32)
     constexpr bool PK = GUARD && FSR_C64_PAIRKEY;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     C64Smem &sm = *reinterpret_cast<C64Smem *>(smem_raw);
+    // replay records (see warp32): the block's selections after the struct
+    constexpr bool REC = GUARD && (OPTS & W32_REPLAY) != 0;
+    uint16_t *seqw = REC ? reinterpret_cast<uint16_t *>(smem_raw + sizeof(C64Smem)) : nullptr;
     const int tid = threadIdx.x, lane = lane_id(), wid = warp_id();
     const int h = tid >> 6, v = tid & 63;
     if (tid < 64) {
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         float acc = 0.f, gr = 0.f, gi = 0.f;
         bool herm = true, flagged = false;
         float ks = 0.f;  // kappa sqrt(B0) (see warp32)
+        int kf = -1;     // REC: the first flagged iteration
         int pu = 0, pv = 0, it = 0;
         // one iteration; H: Hermitian phase, run as its own loop (see warp32)
         auto step = [&](auto hconst) -> bool {
@@ -397,8 +402,12 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const int bv = (bw * 32 + sl[bw].lane) & 63;
             const float b1 = __uint_as_float(best & ~63u);
             if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
+            if (REC && tid == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 64 + bv);
             if (b1 < thr) {
-                if (GUARD && b1 >= thr * one_minus_tau) flagged = true;
+                if (GUARD && b1 >= thr * one_minus_tau) {
+                    flagged = true;
+                    if (REC && kf < 0) kf = it;
+                }
                 return false;
             }
             gr = sl[bw].cre * ginv;
@@ -409,8 +418,9 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 const float b2 = __uint_as_float(second & ~63u);
                 const float sb1 = sqrt_approx(b1);  // scale term (see warp32)
                 if (H && it == 0) ks = a.kappa * sb1;
-                flagged |= b2 >= fmaf(-ks, sb1, b1 * one_minus_tau);
-                flagged |= b1 * one_minus_tau < thr;
+                const bool g = b2 >= fmaf(-ks, sb1, b1 * one_minus_tau) || b1 * one_minus_tau < thr;
+                flagged |= g;
+                if (REC && g && kf < 0) kf = it;
             }
             if (H) herm = ((bu & 31) == 0) && ((bv & 31) == 0);
             const float2 e = sm.cs[(bu * pm_ + bv * pn_) & 63];
@@ -427,11 +437,20 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         const int done = it;
         if (sel_b)
             for (int jj = done + tid; jj < a.iterations; jj += C64_THREADS) sel_b[jj] = -1;
-        if (tid == 0) {
-            if (a.done) a.done[bid] = done;
-            if (GUARD && flagged && a.rerun_list) {
-                unsigned slot = atomicAdd(a.rerun_count, 1u);
+        if (tid == 0 && a.done) a.done[bid] = done;
+        if (GUARD && flagged && a.rerun_list) {
+            if (tid == 0) {
+                const unsigned slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;
+                if (REC) sm.rec_slot = slot;
+            }
+            if (REC) {
+                __syncthreads();  // the slot and the records
+                const unsigned slot = sm.rec_slot;
+                const int n = kf < 0 ? 0 : min(kf, a.seq_stride);
+                if (tid == 0) a.rerun_kf[slot] = n;
+                uint16_t *dst = a.rerun_seq + (int64_t)slot * a.seq_stride;
+                for (int jj = tid; jj < n; jj += C64_THREADS) dst[jj] = seqw[jj];
             }
         }
         if (tid < a.B * a.B) {
@@ -480,7 +499,7 @@ __device__ __forceinline__ unsigned long long c64d_key(double o, int u) {
     return ((unsigned long long)__double_as_longlong(o) & ~63ull) | (unsigned long long)(63 - u);
 }
 
-template <bool UPDATE>
+template <bool UPDATE, bool OBJ = true>
 __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], double2 (&rh)[16],
                                                         const double (&wl)[16], const double (&wh)[16],
                                                         const double2 *Wt, int h, int v, int pu, int pv,
@@ -505,9 +524,11 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
             rl[i] = a;
             rh[i] = b;
         }
-        const unsigned long long ka = c64d_key(fma(a.x, a.x, a.y * a.y) * wl[i], u);
-        const unsigned long long kb = c64d_key(fma(b.x, b.x, b.y * b.y) * wh[i], u + 32);
-        m = max(m, max(ka, kb));
+        if (OBJ) {
+            const unsigned long long ka = c64d_key(fma(a.x, a.x, a.y * a.y) * wl[i], u);
+            const unsigned long long kb = c64d_key(fma(b.x, b.x, b.y * b.y) * wh[i], u + 32);
+            m = max(m, max(ka, kb));
+        }
     }
     return m;
 }
@@ -648,6 +669,31 @@ __global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a
         const int pm_ = a.L + tid / a.B, pn_ = a.L + tid % a.B;
         double acc = 0.0, gr = 0.0, gi = 0.0;
         int pu = 0, pv = 0, it = 0;
+        // replay (list mode): iterations < kf follow the fp32 kernel's recorded
+        // selections with the update alone (see fsr_pair64.cuh)
+        const int kf = a.list_kf ? a.list_kf[bi] : 0;
+        const uint16_t *seq = a.list_kf ? a.list_seq + bi * (int64_t)a.seq_stride : nullptr;
+        for (; it < kf; ++it) {
+            if (it > 0) c64d_pass<true, false>(rl, rh, wl, wh, Wt, h, v, pu, pv, gr, gi);
+            const uint32_t s = seq[it];
+            const int bu = (int)(s >> 6), bv = (int)(s & 63u);
+            C64dSlot *sl = sm.slot[it & 1];
+            double2 plo, phi;
+            c64d_pick(rl, rh, bu & 15, plo, phi);  // bu uniform
+            if (h == ((bu & 31) >> 4) && v == bv) {
+                const double2 c = bu >= 32 ? phi : plo;
+                sl[0].cre = c.x;
+                sl[0].cim = c.y;
+            }
+            __syncthreads();
+            if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
+            gr = sl[0].cre * ginv;
+            gi = sl[0].cim * ginv;
+            pu = bu;
+            pv = bv;
+            const double2 e = sm.cs[(bu * pm_ + bv * pn_) & 63];
+            acc = fma(gr, e.x, fma(-gi, e.y, acc));
+        }
         for (; it < a.iterations; ++it) {
             const unsigned long long kb =
                 it == 0 ? c64d_pass<false>(rl, rh, wl, wh, Wt, h, v, pu, pv, gr, gi)

@@ -32,7 +32,7 @@ cudaError_t warp16_launch(const Warp32Args &a, const Warp32Maps &maps, bool tree
                           int opts, int sms, cudaStream_t st);
 // N = 64 fp32 loop (fsr_cta64.cuh), linear reducer
 template <typename IO, int AM>
-cudaError_t cta64_launch(const Warp32Args &a, const Warp32Maps &maps, bool guard, int sms,
+cudaError_t cta64_launch(const Warp32Args &a, const Warp32Maps &maps, bool guard, int opts, int sms,
                          cudaStream_t st);
 
 // fp64 kernels: validation precision and the guarded re-runs (list mode)
@@ -100,11 +100,11 @@ inline cudaError_t warp16_any(const Warp32Args &a, const Warp32Maps &m, bool tre
     return kNotBuilt;
 }
 template <typename IO>
-inline cudaError_t cta64_any(const Warp32Args &a, const Warp32Maps &m, int am, bool guard, int sms,
-                             cudaStream_t st) {
-    if (am == AM_SHFL) return cta64_launch<IO, AM_SHFL>(a, m, guard, sms, st);
-    if (am == AM_SMEM) return cta64_launch<IO, AM_SMEM>(a, m, guard, sms, st);
-    if (am == AM_REDUX) return cta64_launch<IO, AM_REDUX>(a, m, guard, sms, st);
+inline cudaError_t cta64_any(const Warp32Args &a, const Warp32Maps &m, int am, bool guard, int opts,
+                             int sms, cudaStream_t st) {
+    if (am == AM_SHFL) return cta64_launch<IO, AM_SHFL>(a, m, guard, opts, sms, st);
+    if (am == AM_SMEM) return cta64_launch<IO, AM_SMEM>(a, m, guard, opts, sms, st);
+    if (am == AM_REDUX) return cta64_launch<IO, AM_REDUX>(a, m, guard, opts, sms, st);
     return kNotBuilt;
 }
 

@@ -269,6 +269,10 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
     constexpr bool KAPPA = (OPTS & W32_KAPPA) != 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpNSmem<N, WARPS> &sm = *reinterpret_cast<WarpNSmem<N, WARPS> *>(smem_raw);
+    constexpr bool REC = GUARD && (OPTS & W32_REPLAY) != 0;  // replay records (see warp32)
+    uint16_t *seqw = REC ? reinterpret_cast<uint16_t *>(smem_raw + sizeof(WarpNSmem<N, WARPS>)) +
+                               warp_id() * a.seq_stride
+                         : nullptr;
     const int lane = lane_id(), wid = warp_id();
     if (threadIdx.x < N) {
         const double th = 6.283185307179586476925286766559 * threadIdx.x / N;
@@ -360,6 +364,7 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
         int pu = 0, pv = 0;
         int it = 0;
         float fl = -1.f, ks = 0.f;
+        int kf = -1;  // REC: the first flagged iteration
         auto step = [&](auto hconst) -> bool {
             constexpr bool H = decltype(hconst)::value;
             uint32_t m1, m2;
@@ -381,7 +386,10 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
             const int j = (int)(kmax & 31u);  // the winning pair
             const float b1 = __uint_as_float(kmax & ~31u);
             if (EARLY && b1 < thr) {
-                if (GUARD && b1 >= thr * a.omt) flagged = true;
+                if (GUARD && b1 >= thr * a.omt) {
+                    flagged = true;
+                    if (REC && kf < 0) kf = it;
+                }
                 return false;
             }
             float2 wfp;
@@ -398,6 +406,7 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
             const bool hi = __shfl_sync(0xffffffffu, (int)hl, wl) != 0;
             const int bu = j + (hi ? P : 0), bv = wl % N;
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * N + bv;
+            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * N + bv);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             const float2 cs = sm.cs[(bu * pm + bv * pn) % N];
@@ -410,14 +419,21 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
                 const uint32_t kp = f2u(po) & a.key_mask;
                 const uint32_t k2 = __reduce_max_sync(0xffffffffu, lane == wl ? max(m2, kp) : m1);
                 const float b2 = __uint_as_float(k2 & ~31u);
+                float gtest;
                 if (KAPPA) {
                     const float sb1 = sqrt_approx(b1);
                     if (H && it == 0) ks = a.kappa * sb1;
-                    fl = fmaxf(fl, b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt)));
+                    gtest = b2 - fmaf(-ks, sb1, __fmul_rn(b1, a.omt));
                 } else {
-                    fl = fmaxf(fl, b2 - __fmul_rn(b1, a.omt));
+                    gtest = b2 - __fmul_rn(b1, a.omt);
                 }
-                if (EARLY) flagged |= b1 * a.omt < thr;
+                fl = fmaxf(fl, gtest);
+                if (REC && kf < 0 && gtest >= 0.f) kf = it;
+                if (EARLY) {
+                    const bool near_stop = b1 * a.omt < thr;
+                    flagged |= near_stop;
+                    if (REC && near_stop && kf < 0) kf = it;
+                }
             }
             if (H) herm = (bu % (N / 2) == 0) && (bv % (N / 2) == 0);
             return true;
@@ -433,11 +449,20 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
         const int done = it;
         if (sel_b)
             for (int jj = done + lane; jj < a.iterations; jj += 32) sel_b[jj] = -1;
-        if (lane == 0) {
-            if (a.done) a.done[bid] = done;
-            if (GUARD && flagged && a.rerun_list) {
-                unsigned slot = atomicAdd(a.rerun_count, 1u);
+        if (lane == 0 && a.done) a.done[bid] = done;
+        if (GUARD && flagged && a.rerun_list) {
+            unsigned slot = 0;
+            if (lane == 0) {
+                slot = atomicAdd(a.rerun_count, 1u);
                 a.rerun_list[slot] = (int32_t)bid;
+            }
+            if (REC) {
+                slot = __shfl_sync(0xffffffffu, slot, 0);
+                const int n = kf < 0 ? 0 : min(kf, a.seq_stride);
+                if (lane == 0) a.rerun_kf[slot] = n;
+                __syncwarp();
+                uint16_t *dst = a.rerun_seq + (int64_t)slot * a.seq_stride;
+                for (int jj = lane; jj < n; jj += 32) dst[jj] = seqw[jj];
             }
         }
         if (lane < a.B * a.B) {
@@ -577,7 +602,47 @@ __global__ void __launch_bounds__(WARPS * 32) warpnd_kernel(Pair64Args<IO> a) {
         double acc = 0.0, gr = 0.0, gi = 0.0;
         int pu = 0, pv = 0;
         int done = 0;
-        for (int it = 0; it < a.iterations; ++it) {
+        // replay (list mode): iterations < kf follow the fp32 kernel's recorded
+        // selections with the update alone (see fsr_pair64.cuh)
+        const int kf = a.list_kf ? a.list_kf[bi] : 0;
+        const uint16_t *seq = a.list_kf ? a.list_seq + bi * (int64_t)a.seq_stride : nullptr;
+        for (int it = 0; it < kf; ++it) {
+            if (it > 0) {
+                int col = v - pv;
+                col += col < 0 ? N : 0;
+                const double2 *wp = t + (N - pu) * N + col;
+#pragma unroll
+                for (int u = 0; u < N; ++u) {
+                    const double2 w = wp[u * N];
+                    double re = R[u].re, im = R[u].im;
+                    re = fma(-gr, w.x, re);
+                    re = fma(gi, w.y, re);
+                    im = fma(-gr, w.y, im);
+                    im = fma(-gi, w.x, im);
+                    R[u].re = re;
+                    R[u].im = im;
+                }
+            }
+            const uint32_t s = seq[it];
+            const int bu = (int)(s / N), bv = (int)(s - (s / N) * N);
+            if (sel_b && lane == 0) sel_b[it] = bu * N + bv;
+            double2 c = make_double2(R[0].re, R[0].im);
+#pragma unroll
+            for (int u = 1; u < N; ++u)
+                if (u == bu) c = make_double2(R[u].re, R[u].im);
+            c.x = __shfl_sync(0xffffffffu, c.x, bv);
+            c.y = __shfl_sync(0xffffffffu, c.y, bv);
+            gr = c.x * ginv;
+            gi = c.y * ginv;
+            pu = bu;
+            pv = bv;
+            if (has_pix) {
+                const double2 e = sm.cs[(bu * pm + bv * pn) % N];
+                acc = fma(gr, e.x, fma(-gi, e.y, acc));
+            }
+            done = it + 1;
+        }
+        for (int it = kf; it < a.iterations; ++it) {
             int col = v - pv;
             col += col < 0 ? N : 0;
             const double2 *wp = t + (N - pu) * N + col;  // row u - pu + N of W2

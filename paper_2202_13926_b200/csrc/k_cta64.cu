@@ -14,10 +14,10 @@
 namespace fsr {
 
 namespace {
-template <typename IO, int AM, bool GUARD>
+template <typename IO, int AM, bool GUARD, int OPTS = 0>
 cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_t st) {
-    auto k = cta64_kernel<IO, AM, GUARD>;
-    const size_t smem = sizeof(C64Smem);
+    auto k = cta64_kernel<IO, AM, GUARD, OPTS>;
+    const size_t smem = sizeof(C64Smem) + ((OPTS & W32_REPLAY) ? ((size_t)a.seq_stride * 2 + 15) / 16 * 16 : 0);
     int grid = 1;
     cudaError_t e = persistent_grid(k, C64_THREADS, smem, a.nblocks, sms, &grid);
     if (e != cudaSuccess) return e;
@@ -27,12 +27,14 @@ cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_
 }  // namespace
 
 template <typename IO, int AM>
-cudaError_t cta64_launch(const Warp32Args &a, const Warp32Maps &maps, bool guard, int sms,
+cudaError_t cta64_launch(const Warp32Args &a, const Warp32Maps &maps, bool guard, int opts, int sms,
                          cudaStream_t st) {
+    if constexpr (AM == AM_REDUX)
+        if (guard && (opts & LOPT_REPLAY)) return go<IO, AM, true, W32_REPLAY>(a, maps, sms, st);
     return guard ? go<IO, AM, true>(a, maps, sms, st) : go<IO, AM, false>(a, maps, sms, st);
 }
 
 template cudaError_t cta64_launch<FSR_IO, FSR_AM>(const Warp32Args &, const Warp32Maps &, bool, int,
-                                                  cudaStream_t);
+                                                  int, cudaStream_t);
 
 }  // namespace fsr

@@ -20,7 +20,8 @@ template <typename IO, int N, int AM, bool GUARD, int OPTS>
 cudaError_t go(const Warp32Args &a, const Warp32Maps &maps, int sms, cudaStream_t st) {
     constexpr int WARPS = 4;
     auto k = warpn_kernel<IO, N, WARPS, AM, GUARD, OPTS>;
-    const size_t smem = sizeof(WarpNSmem<N, WARPS>);
+    const size_t smem = sizeof(WarpNSmem<N, WARPS>) +
+                        ((OPTS & W32_REPLAY) ? ((size_t)WARPS * a.seq_stride * 2 + 15) / 16 * 16 : 0);
     int grid = 1;
     cudaError_t e = persistent_grid(k, WARPS * 32, smem, (a.nblocks + WARPS - 1) / WARPS, sms, &grid);
     if (e != cudaSuccess) return e;
@@ -33,6 +34,12 @@ cudaError_t by_opts(const Warp32Args &a, const Warp32Maps &maps, bool guard, int
                     cudaStream_t st) {
     if (opts == 0) return guard ? go<IO, N, AM, true, 0>(a, maps, sms, st) : go<IO, N, AM, false, 0>(a, maps, sms, st);
     if (opts == LOPT_KAPPA && guard) return go<IO, N, AM, true, W32_KAPPA>(a, maps, sms, st);
+    if constexpr (AM == AM_REDUX) {
+        if (guard && opts == LOPT_REPLAY) return go<IO, N, AM, true, W32_REPLAY>(a, maps, sms, st);
+        if (guard && opts == (LOPT_KAPPA | LOPT_REPLAY))
+            return go<IO, N, AM, true, W32_KAPPA | W32_REPLAY>(a, maps, sms, st);
+        if (guard && (opts & LOPT_REPLAY)) return go<IO, N, AM, true, W32_ALL | W32_REPLAY>(a, maps, sms, st);
+    }
     return guard ? go<IO, N, AM, true, W32_ALL>(a, maps, sms, st) : go<IO, N, AM, false, W32_ALL>(a, maps, sms, st);
 }
 }  // namespace

@@ -26,7 +26,8 @@ def main():
     img = synth.frame(H, W, 7, "natural")
     mask = frames.quarter_sample_mask(H, W, 42)
     px = np.where(mask, img, 0.0)
-    p = _lib.make_params(4, (N - 4) // 2, I, precision="fp32")
+    red = "linear" if N == 64 else "tree"
+    p = _lib.make_params(4, (N - 4) // 2, I, precision="fp32", reducer=red)
     on, off = engine(1), engine(0)
     o_on = on.reconstruct(px, mask, p)
     st_on = on.last_stats()
@@ -37,7 +38,7 @@ def main():
           f"pixels differing {int((diff > 0).sum())}, max |d| {diff.max():.3e}, "
           f"kernel ms {st_on['kernel_ms']:.2f} (replay) vs {st_off['kernel_ms']:.2f}")
     if H * W <= 600 * 1000:
-        ref = oracle.reconstruct_image(px, mask, 4, (N - 4) // 2, I, 0.7, 0.5, "tree")
+        ref = oracle.reconstruct_image(px, mask, 4, (N - 4) // 2, I, 0.7, 0.5, red)
         print(f"  vs reference: replay max |d| {np.abs(o_on - ref).max() / 255:.3e}, "
               f"full re-run {np.abs(o_off - ref).max() / 255:.3e} (0..1)")
 
