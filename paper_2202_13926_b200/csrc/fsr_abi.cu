@@ -592,10 +592,13 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     // selections up to its first ambiguous iteration; warp16d / pair64 / cta64d replay them without
     // the objective / argmax, then searches in fp64 from there
     // (the segmented N <= 8 kernel does not record: its re-runs are cheap)
+    // From I = 101 on (recording costs the N <= 32 main kernels ~3.6 %, more
+    // than the replay saves at I = 100), at any I for N = 64 (recording is free
+    // next to its 4096-bin pass; 1080p I=100: 24.4 -> 25.5 fps).
     const bool replay = guarded && (warp32_eligible(p) || warp16_eligible(p) || cta64_eligible(p) ||
                                     (warpn_eligible(p) && N == 24)) &&
                         p->argmax_impl == FSR_ARGMAX_REDUX && d.replay_min_iters > 0 &&
-                        p->iterations >= d.replay_min_iters;
+                        (p->iterations >= d.replay_min_iters || (cta64_eligible(p) && d.replay_min_iters <= 101));
     if (replay) {
         CUDA_TRY(eng, d.rerun_kf.ensure((size_t)nblocks * sizeof(int32_t)));
         CUDA_TRY(eng, d.rerun_seq.ensure((size_t)nblocks * p->iterations * sizeof(uint16_t)));
