@@ -591,6 +591,8 @@ def main():
         kernel = "warp16d_kernel" if fp64 else "warp16_kernel"
     elif N == 64 and B * B <= 128 and args.reducer == "linear":
         kernel = "cta64d_kernel" if fp64 else "cta64_kernel"
+    elif N in (4, 8) and B <= 4:
+        kernel = "warpsegd_kernel" if fp64 else "warpseg_kernel"
     elif N in (4, 8, 24) and B * B <= 32:
         kernel = "warpnd_kernel" if fp64 else "warpn_kernel"
     else:

@@ -18,7 +18,10 @@ def row(cfg, d, cpu, parity):
     iss = (r.get("issue") or {}).get("issue_active_pct")
     sm = (r.get("smem") or {}).get("frac")
     e2e = (d.get("e2e") or {}).get("value")
-    loop = f"{r['bound'].upper()} {r['frac']:.2f} of measured {r['peak']} TF/s ({r['kernel']})"
+    kern = r["kernel"]
+    if d["config"].get("N") in (4, 8) and d["config"].get("B", 4) <= 4:  # lines from before the label fix
+        kern = kern.replace("warpnd", "warpsegd").replace("warpn_", "warpseg_")
+    loop = f"{r['bound'].upper()} {r['frac']:.2f} of measured {r['peak']} TF/s ({kern})"
     if iss:
         loop += f", issue {iss:.0f} %"
     if sm:
