@@ -603,8 +603,12 @@ def main():
     traffic, traffic_src, issue = None, None, None
     # committed ncu captures (tools/profile_round.sh) for the default line of each kernel
     captured = {("warp32_kernel", "4k"): ("warp32_ncu.json", "void warp32_kernel<"),
-                ("warp16_kernel", "1080p"): ("warp16_ncu.json", "void warp16_kernel<"),
-                ("cta64_kernel", "1080p"): ("cta64_ncu.json", "void cta64_kernel<")}
+                ("warp32_kernel", "1080p"): ("warp32_1080p_redux_ncu.json", "void warp32_kernel<"),
+                ("warp16_kernel", "1080p"): ("warp16_1080p_ncu.json", "void warp16_kernel<"),
+                ("cta64_kernel", "1080p"): ("cta64_1080p_ncu.json", "void cta64_kernel<"),
+                ("warpn_kernel", "1080p"): ("warpn24_1080p_ncu.json", "void warpn_kernel<"),
+                ("warpseg_kernel", "1080p"): ("warpseg8_1080p_ncu.json", "void warpseg_kernel<"),
+                ("warpsegd_kernel", "1080p"): ("warpsegd4_1080p_ncu.json", "void warpsegd_kernel<")}
     cap = captured.get((kernel, args.workload))
     if (cap is not None and world == 1 and args.precision == "fp32" and args.argmax == "redux"
             and I == 100 and B == 4):
