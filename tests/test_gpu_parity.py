@@ -717,18 +717,21 @@ def test_guarded_fp32_reports_fp64_service(N, B, I, served):
     assert tr.stats["served_fp64"] is served
 
 
-def test_replay_matches_full_reruns(monkeypatch):
-    """Beyond 100 iterations the N=32 fp64 re-runs replay the fp32 kernel's
-    unambiguous prefix: on this frame the output is bitwise the
-    output of full fp64 re-runs (FSR_REPLAY_MIN=0), and the replayed path stays
-    within the production tolerance of the reference."""
+@pytest.mark.parametrize("N,H,W", [(32, 540, 960), (16, 540, 960), (24, 540, 960), (64, 270, 480)])
+def test_replay_matches_full_reruns(monkeypatch, N, H, W):
+    """Beyond 100 iterations (N = 64: always) the fp64 re-runs replay the fp32
+    kernel's unambiguous prefix: on these frames the output is
+    bitwise the output of full fp64 re-runs (FSR_REPLAY_MIN=0), and the replayed
+    path stays within the production tolerance of the reference."""
     from paper_2202_13926_b200 import _lib, frames, synth
 
-    H, W, I = 540, 960, 200
+    I = 200
+    red = "linear" if N == 64 else "tree"
+    L = (N - 4) // 2
     img = synth.frame(H, W, 7, "natural")
     mask = frames.quarter_sample_mask(H, W, 42)
     px = np.where(mask, img, 0.0)
-    p = _lib.make_params(4, 14, I, precision="fp32")
+    p = _lib.make_params(4, L, I, precision="fp32", reducer=red)
     monkeypatch.setenv("FSR_REPLAY_MIN", "1")
     on = _lib.Engine([0])
     monkeypatch.setenv("FSR_REPLAY_MIN", "0")
@@ -737,7 +740,7 @@ def test_replay_matches_full_reruns(monkeypatch):
     o_off = off.reconstruct(px, mask, p)
     assert on.last_stats()["rerun_blocks"] == off.last_stats()["rerun_blocks"] > 0
     assert np.array_equal(o_on, o_off)
-    rows = (60, 72)  # a band of block rows against the reference restatement
-    ref = oracle.reconstruct_image(px, mask, 4, 14, I, 0.7, 0.5, "tree", block_rows=rows)
+    rows = (30, 36)  # a band of block rows against the reference restatement
+    ref = oracle.reconstruct_image(px, mask, 4, L, I, 0.7, 0.5, red, block_rows=rows)
     y0, y1 = rows[0] * 4, rows[1] * 4
     assert float(np.abs(o_on[y0:y1] - ref[y0:y1]).max()) <= FP32_TOL
