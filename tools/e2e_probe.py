@@ -17,7 +17,8 @@ img = synth.frame(H, W, 7, "natural")
 mask = frames.quarter_sample_mask(H, W, 42)
 px = np.where(mask, img, 0.0)
 m8 = mask.astype(np.uint8)
-p = _lib.make_params(4, 14, 100, precision="fp32")
+NS = int(os.environ.get("SUPPORT", "32"))
+p = _lib.make_params(4, (NS - 4) // 2, 100, precision="fp32")
 eng = _lib.default_engine()
 
 
@@ -31,7 +32,7 @@ def timed(fn, reps=8):
 
 out = np.zeros((H, W))
 brows = -(-H // 4)
-print("api fresh out   %.2f ms" % timed(lambda: fsr.reconstruct(px, mask, 4, 32, 100, precision="fp32")))
+print("api fresh out   %.2f ms" % timed(lambda: fsr.reconstruct(px, mask, 4, NS, 100, precision="fp32")))
 print("rows reused out %.2f ms" % timed(lambda: eng.reconstruct_rows(px, m8, p, 0, brows, out)))
 hp = torch.from_numpy(px).pin_memory().numpy()
 hm = torch.from_numpy(m8).pin_memory().numpy()
