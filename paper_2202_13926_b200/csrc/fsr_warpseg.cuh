@@ -35,7 +35,6 @@ template <int N>
 struct SegCfg {
     static constexpr int P = N / 2;
     static constexpr int BPW = 32 / N;                 // blocks (segments) per warp
-    static constexpr int LV = N == 16 ? 4 : N == 8 ? 3 : 2;  // log2 N
     static constexpr uint32_t KMASK = ~31u;            // 5 low key bits: the pair index
     static constexpr uint32_t SEGMASK = N == 32 ? 0xffffffffu : (1u << N) - 1u;
     static constexpr int TILE = N * (N + 1) * 16;
@@ -65,7 +64,7 @@ __device__ __forceinline__ uint32_t seg_max(uint32_t k) {
 template <int N, bool GUARD, bool HERM, bool UPDATE, uint32_t KMASK>
 __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2], const float2 (&wf2)[N / 2],
                                          const float4 *up, float gr, float gi, uint32_t canon,
-                                         const uint32_t (&tag)[N / 2], uint32_t &m1, uint32_t &m2) {
+                                         uint32_t &m1, uint32_t &m2) {
     constexpr int P = N / 2;
     m1 = 0;
     m2 = 0;
@@ -91,7 +90,7 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
             ox = ((canon >> i) & 1u) ? ox : 0.f;
             oy = ((canon >> (i + P)) & 1u) ? oy : 0.f;
         }
-        const uint32_t h = and_or(f2u(fmaxf(ox, oy)), KMASK, tag[i]);
+        const uint32_t h = and_or(f2u(fmaxf(ox, oy)), KMASK, (uint32_t)i);  // the pair index
         if (!GUARD || P == 1) {
             m1 = max(m1, h);
         } else if ((i & 1) == 0) {
@@ -138,12 +137,8 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
         canon |= (uint32_t)(tie_rank(tt, a.tree != 0) <= tie_rank(mt, a.tree != 0)) << u;
     }
     float2 wf2[P];
-    uint32_t tag[P];
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-        wf2[i] = make_float2(__ldg(a.wf + i * N + v), __ldg(a.wf + (i + P) * N + v));
-        tag[i] = (uint32_t)i;
-    }
+    for (int i = 0; i < P; ++i) wf2[i] = make_float2(__ldg(a.wf + i * N + v), __ldg(a.wf + (i + P) * N + v));
     const int64_t stride = (int64_t)gridDim.x * WARPS * C::BPW;
     for (int64_t base = ((int64_t)blockIdx.x * WARPS + wid) * C::BPW; base < a.nblocks; base += stride) {
         const int64_t bi = base + sg;
@@ -250,9 +245,9 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
             const uint32_t cn = (H && herm) ? canon : 0xffffffffu;
             uint32_t m1, m2;
             if (H && it == 0)
-                seg_pass<N, GUARD, true, false, C::KMASK>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
+                seg_pass<N, GUARD, true, false, C::KMASK>(re, im, wf2, up, gr, gi, cn, m1, m2);
             else
-                seg_pass<N, GUARD, H, true, C::KMASK>(re, im, wf2, up, gr, gi, cn, tag, m1, m2);
+                seg_pass<N, GUARD, H, true, C::KMASK>(re, im, wf2, up, gr, gi, cn, m1, m2);
             if (!live) m1 = m2 = 0u;
             const uint32_t kmax = seg_max<N>(m1);
             const uint32_t bal = (__ballot_sync(0xffffffffu, m1 == kmax) >> sbase) & C::SEGMASK;
