@@ -581,7 +581,8 @@ def main():
     clk_hz = pk.get("sm_max_mhz", 1965.0) * 1e6
     # a guarded fp32 request the engine serves in fp64 (fsr_abi.cu enqueue_image:
     # I > 300, N = 4, or a support without an fp32 register kernel) is reported as fp64
-    fp32_kernel = (B * B <= 32 and N in (4, 8, 16, 24, 32)) or (N == 64 and args.reducer == "linear")
+    fp32_kernel = (B * B <= 32 and N % 2 == 0 and (4 <= N <= 20 or N in (24, 32))) or \
+        (N == 64 and args.reducer == "linear")
     served64 = args.precision == "fp32" and (I > 300 or N == 4 or not fp32_kernel)
     fp64 = args.precision == "fp64" or served64
     peak_fl, peak_src = fp_peak(fp64)
@@ -591,9 +592,9 @@ def main():
         kernel = "warp16d_kernel" if fp64 else "warp16_kernel"
     elif N == 64 and B * B <= 128 and args.reducer == "linear":
         kernel = "cta64d_kernel" if fp64 else "cta64_kernel"
-    elif N in (4, 8) and B <= 4:
+    elif N in (4, 8) and B <= 4:  # 32/N blocks per warp
         kernel = "warpsegd_kernel" if fp64 else "warpseg_kernel"
-    elif N in (4, 8, 24) and B * B <= 32:
+    elif N % 2 == 0 and (4 <= N <= 20 or N == 24) and B * B <= 32:
         kernel = "warpnd_kernel" if fp64 else "warpn_kernel"
     else:
         kernel = "image_generic_kernel"

@@ -230,7 +230,7 @@ typedef struct {
 /* fsr_stats.flags: a guarded FP32 request was served by the fp64 kernels (more
  * than 300 iterations, N = 4 (whose fp64 kernel is faster than fp32 plus its
  * ~45 % re-runs), or a support without an fp32 register kernel -- the fp32 ones
- * cover N = 8, 16, 24, 32 and N = 64 with the linear reducer). */
+ * cover every even N from 6 to 20, 24, 32 and N = 64 with the linear reducer). */
 #define FSR_STATS_SERVED_FP64 2
 int fsr_last_stats(const fsr_engine *eng, fsr_stats *out);
 

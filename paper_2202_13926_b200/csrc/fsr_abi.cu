@@ -407,7 +407,7 @@ int launch_warp16d(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, bool tre
 template <typename IO>
 int launch_warpnd(fsr_engine *eng, Device &d, const Pair64Args<IO> &a, int N, int am,
                   int64_t want_blocks, cudaStream_t st) {
-    if (N <= 8 && a.B <= 4 && d.segmented)  // 32/N blocks per warp (fsr_warpseg.cuh)
+    if ((N == 4 || N == 8) && a.B <= 4 && d.segmented)  // 32/N blocks per warp (fsr_warpseg.cuh)
         LAUNCH_TRY(eng, d, (warpsegd_launch<IO>(a, N, want_blocks, d.sms, st)));
     else
         LAUNCH_TRY(eng, d, (warpnd_launch<IO>(a, N, am, want_blocks, d.sms, st)));
@@ -504,8 +504,9 @@ bool cta64d_eligible(const fsr_params *p) {
            p->reducer == FSR_REDUCER_LINEAR;
 }
 
-// the paper grid's other supports (fsr_warpn.cuh): one warp per block, N in {4, 8, 24}
-bool warpn_support(int N) { return N == 4 || N == 8 || N == 24; }
+// the supports without a dedicated kernel (fsr_warpn.cuh): one warp per block,
+// the paper grid's 4, 8, 24 and every other even N up to 20 (not 16)
+bool warpn_support(int N) { return N == 24 || (N >= 4 && N <= 20 && N % 2 == 0 && N != 16); }
 bool warpnd_eligible(const fsr_params *p) {
     return warpn_support(p->block + 2 * p->border) && p->block * p->block <= 32;
 }
@@ -536,23 +537,25 @@ bool warp32_eligible(const fsr_params *p) {
 // noise frames with tools/flip_errors.py:
 //     tau   = 5e-5 * k_N,                 k_N = 2 for N = 64, else 1
 //     kappa = 1e-7 * max(0, I / 100 - 1)  (none up to the default 100 iterations)
-// and for the small supports N <= 8 (64 bins or fewer: after a few dozen
+// and for the small supports N <= 14 (196 bins or fewer: after a few dozen
 // iterations every objective lies far below B0, so the scale term would flag
-// nearly every block -- 95 % at N = 8, I = 200):
+// nearly every block -- 95 % at N = 8, I = 200 -- while tau = 5e-5 misses flips
+// at N = 10..14: 0.24-0.42 gray levels):
 //     tau   = 2e-4, kappa = 0             (1080p N = 8, I = 100: max 0.09 gray
-//                                          levels at 15 % re-runs; I = 200: 0.17)
+//                                          levels at 15 % re-runs; I = 200: 0.17;
+//                                          N = 10..14: <= 0.15 at 16-18 %)
 // An explicit guard_tau > 0 / guard_kappa > 0 is used as given; guard_kappa < 0
 // turns the scale term off.
 double guard_tau_for(const fsr_params *p) {
     if (p->guard_tau > 0.0) return p->guard_tau;
     const int N = p->block + 2 * p->border;
-    return N >= 64 ? 1e-4 : N <= 8 ? 2e-4 : 5e-5;
+    return N >= 64 ? 1e-4 : N <= 14 ? 2e-4 : 5e-5;
 }
 
 double guard_kappa_for(const fsr_params *p) {
     if (p->guard_kappa > 0.0) return p->guard_kappa;
     if (p->guard_kappa < 0.0) return 0.0;
-    if (p->block + 2 * p->border <= 8) return 0.0;
+    if (p->block + 2 * p->border <= 14) return 0.0;
     return 1e-7 * std::max(0.0, p->iterations / 100.0 - 1.0);
 }
 
@@ -751,7 +754,7 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
             // (warpseg with two blocks per warp measured 8 % slower at N = 16, 1080p:
             // 2.39 vs 2.21 ms; warp16's two lanes per column already issue 70 %)
             LAUNCH_TRY(eng, d, (warp16_any<IO>(a, maps, tree, p->argmax_impl, guarded, opts, d.sms, st)));
-        } else if (fastn && N <= 8 && p->block <= 4 && d.segmented) {
+        } else if (fastn && (N == 4 || N == 8) && p->block <= 4 && d.segmented) {
             LAUNCH_TRY(eng, d, (warpseg_any<IO>(a, N, guarded, opts, d.sms, st)));
         } else if (fastn) {
             LAUNCH_TRY(eng, d, (warpn_any<IO>(a, maps, N, p->argmax_impl, guarded, opts, d.sms, st)));

@@ -55,9 +55,21 @@ cudaError_t cta64d_launch(const Pair64Args<IO> &a, int grid, cudaStream_t st);
 template <typename IO, int N>
 cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
                          int sms, cudaStream_t st);
+template <typename IO, int N>
+cudaError_t warpnd_launch_n(const Pair64Args<IO> &a, int am, int64_t want_blocks, int sms, cudaStream_t st);
+// the even supports up to 20 other than 16, and 24 (fsr_warpn.cuh), one object per
+// (IO, N); N = 22, 26, 28, 30 stay on the generic kernel (their fully unrolled
+// direct half-DFTs stall ptxas for tens of minutes)
+#define FSR_WN_SUPPORTS(X) X(4) X(6) X(8) X(10) X(12) X(14) X(18) X(20) X(24)
 template <typename IO>
-cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want_blocks, int sms,
-                          cudaStream_t st);
+inline cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want_blocks, int sms,
+                                 cudaStream_t st) {
+#define FSR_WND_CASE(n) \
+    if (N == n) return warpnd_launch_n<IO, n>(a, am, want_blocks, sms, st);
+    FSR_WN_SUPPORTS(FSR_WND_CASE)
+#undef FSR_WND_CASE
+    return kNotBuilt;
+}
 // N in {4, 8}, B <= 4: 32 / N blocks per warp (fsr_warpseg.cuh; own segmented argmax)
 template <typename IO, int N>
 cudaError_t warpseg_launch(const Warp32Args &a, bool guard, int opts, int sms, cudaStream_t st);
@@ -73,9 +85,10 @@ cudaError_t warpsegd_launch(const Pair64Args<IO> &a, int N, int64_t want_blocks,
 template <typename IO>
 inline cudaError_t warpn_any(const Warp32Args &a, const Warp32Maps &m, int N, int am, bool guard,
                              int opts, int sms, cudaStream_t st) {
-    if (N == 4) return warpn_launch<IO, 4>(a, m, am, guard, opts, sms, st);
-    if (N == 8) return warpn_launch<IO, 8>(a, m, am, guard, opts, sms, st);
-    if (N == 24) return warpn_launch<IO, 24>(a, m, am, guard, opts, sms, st);
+#define FSR_WN_CASE(n) \
+    if (N == n) return warpn_launch<IO, n>(a, m, am, guard, opts, sms, st);
+    FSR_WN_SUPPORTS(FSR_WN_CASE)
+#undef FSR_WN_CASE
     return kNotBuilt;
 }
 // any support <= 64, strict IEEE (fsr_generic.cuh)

@@ -585,7 +585,7 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
 #endif
 template <int BPC, bool TREE, int ARGMAX, typename IO>
 __global__ void __maxnreg__(FSR_P64_MAXREG) pair64_kernel(Pair64Args<IO> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Pair64Smem<BPC> &sm = *reinterpret_cast<Pair64Smem<BPC> *>(smem_raw);
     if (threadIdx.x < 32) {
         double s, c;

@@ -559,7 +559,7 @@ __device__ __forceinline__ unsigned long long pass16d(double (&rre)[8], double (
 #endif
 template <int WARPS, bool TREE, int ARGMAX, typename IO>
 __global__ void __launch_bounds__(WARPS * 32, FSR_W16D_WARPS_PER_SM / WARPS) warp16d_kernel(Pair64Args<IO> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp16dSmem<WARPS> &sm = *reinterpret_cast<Warp16dSmem<WARPS> *>(smem_raw);
     const int lane = lane_id(), wid = warp_id();
     if (threadIdx.x < 16) {

@@ -93,7 +93,7 @@ __device__ __forceinline__ unsigned long long w64_pass(cpx<double> (&R)[32], con
 
 template <int WARPS, bool TREE, int ARGMAX, typename IO>
 __global__ void __maxnreg__(FSR_W64_MAXREG) warp64_kernel(Pair64Args<IO> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Warp64Smem<WARPS> &sm = *reinterpret_cast<Warp64Smem<WARPS> *>(smem_raw);
     if (threadIdx.x < 32) {
         double s, c;

@@ -1,6 +1,7 @@
-// fsr_warpn.cuh -- FSR kernels for the paper grid's other supports, N = 4, 8
-// and 24 (S in {4, 8, 16, 24, 32}; the sweep of cli.py:41-50),
-// one warp per target block, lane v < N owning spectral column v.
+// fsr_warpn.cuh -- FSR kernels for the supports without a dedicated kernel:
+// the paper grid's N = 4, 8, 24 (S in {4, 8, 16, 24, 32}; the
+// sweep of cli.py:41-50) and every other even N <= 32, one warp per target
+// block, lane v < N owning spectral column v.
 //
 //   warpn_kernel   fp32 loop with the near-tie guard -- fsr_warp32.cuh's design
 //                  (read that header first) with the row pairs (i, i + N/2):
@@ -21,7 +22,9 @@
 //   prologue       (both) gather of the N x N window (TMA boxes or plain loads,
 //                  outside = unknown), mask-gated rho^d weights, packed z = f w +
 //                  i w, fp64 2-D DFT on an N x (N+1) double2 tile (N = 24 as
-//                  8 x 3 mixed radix), Hermitian split into R and W.
+//                  8 x 3 mixed radix; other even N as one radix-2 step over two
+//                  direct N/2-point DFTs with compile-time twiddles), Hermitian
+//                  split into R and W.
 #pragma once
 
 #include "fsr_pair64.cuh"
@@ -45,6 +48,66 @@ __host__ __device__ constexpr double cos24(int m) {  // m in [0, 24)
 }
 __host__ __device__ constexpr double sin24(int m) { return cos24((m + 18) % 24); }  // sin x = cos(x - pi/2)
 
+// cos / sin (2 pi m / n) as compile-time constants for any n: the angle is
+// reduced to an octant by exact integer arithmetic (k = floor(8m / n)), then a
+// Taylor series on [0, pi/4] (error below the double rounding).
+__host__ __device__ constexpr double taylor_cos(double x) {
+    double s = 1.0, t = 1.0;
+    for (int k = 1; k < 12; ++k) {
+        t *= -x * x / ((2.0 * k - 1.0) * (2.0 * k));
+        s += t;
+    }
+    return s;
+}
+__host__ __device__ constexpr double taylor_sin(double x) {
+    double s = x, t = x;
+    for (int k = 1; k < 12; ++k) {
+        t *= -x * x / ((2.0 * k) * (2.0 * k + 1.0));
+        s += t;
+    }
+    return s;
+}
+__host__ __device__ constexpr double cos2pi(long long m, long long n) {
+    m = ((m % n) + n) % n;
+    const long long k = (8 * m) / n, r = 8 * m - k * n;  // octant, remainder in [0, n)
+    const double qp = 0.78539816339744830961566084581988;  // pi / 4
+    const double phi = qp * (double)r / (double)n, phc = qp * (double)(n - r) / (double)n;
+    switch (k) {
+        case 0: return taylor_cos(phi);
+        case 1: return taylor_sin(phc);
+        case 2: return -taylor_sin(phi);
+        case 3: return -taylor_cos(phc);
+        case 4: return -taylor_cos(phi);
+        case 5: return -taylor_sin(phc);
+        case 6: return taylor_sin(phi);
+        default: return taylor_cos(phc);
+    }
+}
+__host__ __device__ constexpr double sin2pi(long long m, long long n) { return cos2pi(4 * m - n, 4 * n); }
+
+// Direct M-point DFT of the strided subsequence x[off + 2 j] (j < M) into y.
+template <int M, int OFF, typename T, int NX>
+__device__ __forceinline__ void dft_half(const cpx<T> (&x)[NX], cpx<T> (&y)[M]) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+        T re = 0, im = 0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            const cpx<T> a = x[OFF + 2 * j];
+            const int m = (k * j) % M;
+            if (m == 0) {
+                re += a.re;
+                im += a.im;
+            } else {
+                const T c = (T)cos2pi(m, M), sn = (T)sin2pi(m, M);  // (a.re + i a.im)(c - i sn)
+                re += a.re * c + a.im * sn;
+                im += a.im * c - a.re * sn;
+            }
+        }
+        y[k] = {re, im};
+    }
+}
+
 // x[k] <- sum_n x[n] e^{-2 pi i k n / N} (unnormalised, numpy.fft convention)
 template <int N, typename T>
 __device__ __forceinline__ void fft_line(cpx<T> (&x)[N]) {
@@ -54,8 +117,25 @@ __device__ __forceinline__ void fft_line(cpx<T> (&x)[N]) {
         fft_pow2<3>(x);
     } else if constexpr (N == 16) {
         fft_pow2<4>(x);
+    } else if constexpr (N != 24) {
+        // any other even N: one radix-2 step over two direct N/2-point DFTs
+        // (even / odd samples), X[k] = E[k] + W^k O[k], X[k + N/2] = E[k] - W^k O[k]
+        static_assert(N % 2 == 0 && N <= 32, "fft_line: even N <= 32");
+        constexpr int M = N / 2;
+        cpx<T> e[M], o[M];
+        dft_half<M, 0>(x, e);
+        dft_half<M, 1>(x, o);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            cpx<T> t = o[k];
+            if (k != 0) {
+                const T c = (T)cos2pi(k, N), sn = (T)sin2pi(k, N);
+                t = {o[k].re * c + o[k].im * sn, o[k].im * c - o[k].re * sn};
+            }
+            x[k] = {e[k].re + t.re, e[k].im + t.im};
+            x[k + M] = {e[k].re - t.re, e[k].im - t.im};
+        }
     } else {
-        static_assert(N == 24, "fft_line: N in {4, 8, 16, 24}");
         // decimation in time by 3: y_r = FFT8(x[3m + r]); X[k1 + 8 k2] =
         // sum_r W3^{r k2} (W24^{r k1} y_r[k1])
         cpx<T> y[3][8];
@@ -173,7 +253,9 @@ struct WnCfg {
     static constexpr int UTAB = N * N * 16;              // U row-pair table (bytes)
     static constexpr int STAGE = TmaBox<double, N, N>::STAGE_BYTES;
     static constexpr int BYTES = (TILE > UTAB ? (TILE > STAGE ? TILE : STAGE) : (UTAB > STAGE ? UTAB : STAGE));
-    static constexpr int F4 = (BYTES + 15) / 16;         // per-warp buffer in float4
+    static constexpr int F4 = (BYTES + 127) / 128 * 8;   // per-warp buffer in float4, 128 B
+                                                         // multiple: every warp's TMA staging
+                                                         // must start 128-byte aligned
 };
 
 template <int N, int WARPS>
@@ -201,7 +283,8 @@ __device__ __forceinline__ float4 pick_pairn(const float2 (&re)[P], const float2
         }                                                                         \
         break;
         FSR_PICKN(1) FSR_PICKN(2) FSR_PICKN(3) FSR_PICKN(4) FSR_PICKN(5) FSR_PICKN(6)
-        FSR_PICKN(7) FSR_PICKN(8) FSR_PICKN(9) FSR_PICKN(10) FSR_PICKN(11)
+        FSR_PICKN(7) FSR_PICKN(8) FSR_PICKN(9) FSR_PICKN(10) FSR_PICKN(11) FSR_PICKN(12)
+        FSR_PICKN(13) FSR_PICKN(14) FSR_PICKN(15)
 #undef FSR_PICKN
         default: break;
     }
@@ -249,6 +332,10 @@ __device__ __forceinline__ void passn(float2 (&re)[N / 2], float2 (&im)[N / 2], 
             m2 = umax3(m2, hmin, min(m1, hmax));
             m1 = max(m1, hmax);
         }
+    }
+    if (GUARD && (P & 1)) {  // odd pair count (N = 2 mod 4): the last pair is still pending
+        m2 = max(m2, min(m1, hpend));
+        m1 = max(m1, hpend);
     }
 }
 
@@ -494,7 +581,7 @@ template <int N, int WARPS, int ARGMAX, typename IO>
 __global__ void __launch_bounds__(WARPS * 32) warpnd_kernel(Pair64Args<IO> a) {
     const bool TREE = a.tree != 0;
     constexpr int TS = N + 1;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpNdSmem<N, WARPS> &sm = *reinterpret_cast<WarpNdSmem<N, WARPS> *>(smem_raw);
     if (threadIdx.x < N) {
         double sn, cn;

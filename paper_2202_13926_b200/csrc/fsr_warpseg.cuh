@@ -91,7 +91,7 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
             oy = ((canon >> (i + P)) & 1u) ? oy : 0.f;
         }
         const uint32_t h = and_or(f2u(fmaxf(ox, oy)), KMASK, (uint32_t)i);  // the pair index
-        if (!GUARD || P == 1) {
+        if (!GUARD) {
             m1 = max(m1, h);
         } else if ((i & 1) == 0) {
             hpend = h;
@@ -100,6 +100,10 @@ __device__ __forceinline__ void seg_pass(float2 (&re)[N / 2], float2 (&im)[N / 2
             m2 = umax3(m2, hmin, min(m1, hmax));
             m1 = max(m1, hmax);
         }
+    }
+    if (GUARD && (P & 1)) {  // odd pair count: the last pair is still pending
+        m2 = max(m2, min(m1, hpend));
+        m1 = max(m1, hpend);
     }
 }
 
@@ -385,7 +389,7 @@ __device__ __forceinline__ unsigned long long seg_max64(unsigned long long k) {
 template <int N, int WARPS, typename IO>
 __global__ void __launch_bounds__(WARPS * 32) warpsegd_kernel(Pair64Args<IO> a) {
     using C = SegdCfg<N>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     WarpSegdSmem<N, WARPS> &sm = *reinterpret_cast<WarpSegdSmem<N, WARPS> *>(smem_raw);
     if (threadIdx.x < N) {
         double sn, cn;

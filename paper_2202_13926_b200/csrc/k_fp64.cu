@@ -80,27 +80,6 @@ cudaError_t warp16d_launch(const Pair64Args<IO> &a, bool tree, int am, int64_t w
 }
 #undef FSR_BY_TREE_AM
 
-namespace {
-template <int N, int AM, typename IO>
-cudaError_t wnd_go(const Pair64Args<IO> &a, int64_t want, int sms, cudaStream_t st) {
-    constexpr int WARPS = 4;
-    auto k = warpnd_kernel<N, WARPS, AM, IO>;
-    const size_t smem = sizeof(WarpNdSmem<N, WARPS>);
-    int grid = 1;
-    cudaError_t e = persistent_grid(k, WARPS * 32, smem, (want + WARPS - 1) / WARPS, sms, &grid);
-    if (e != cudaSuccess) return e;
-    k<<<grid, WARPS * 32, smem, st>>>(a);
-    return cudaGetLastError();
-}
-template <int N, typename IO>
-cudaError_t wnd_am(const Pair64Args<IO> &a, int am, int64_t want, int sms, cudaStream_t st) {
-    if (am == AM_SHFL) return wnd_go<N, AM_SHFL>(a, want, sms, st);
-    if (am == AM_SMEM) return wnd_go<N, AM_SMEM>(a, want, sms, st);
-    if (am == AM_REDUX) return wnd_go<N, AM_REDUX>(a, want, sms, st);
-    return kNotBuilt;
-}
-}  // namespace
-
 template <int N, typename IO>
 cudaError_t wsd_go(const Pair64Args<IO> &a, int64_t want, int sms, cudaStream_t st) {
     constexpr int WARPS = 4, BPC = WARPS * SegdCfg<N>::BPW;
@@ -117,14 +96,6 @@ template <typename IO>
 cudaError_t warpsegd_launch(const Pair64Args<IO> &a, int N, int64_t want, int sms, cudaStream_t st) {
     if (N == 4) return wsd_go<4>(a, want, sms, st);
     if (N == 8) return wsd_go<8>(a, want, sms, st);
-    return kNotBuilt;
-}
-
-template <typename IO>
-cudaError_t warpnd_launch(const Pair64Args<IO> &a, int N, int am, int64_t want, int sms, cudaStream_t st) {
-    if (N == 4) return wnd_am<4>(a, am, want, sms, st);
-    if (N == 8) return wnd_am<8>(a, am, want, sms, st);
-    if (N == 24) return wnd_am<24>(a, am, want, sms, st);
     return kNotBuilt;
 }
 
@@ -162,7 +133,6 @@ template cudaError_t pair64_launch<FSR_IO>(const Pair64Args<FSR_IO> &, bool, int
 template cudaError_t warp64_launch<FSR_IO>(const Pair64Args<FSR_IO> &, bool, int, int64_t, int, cudaStream_t);
 template cudaError_t warp16d_launch<FSR_IO>(const Pair64Args<FSR_IO> &, bool, int, int64_t, int, cudaStream_t);
 template cudaError_t cta64d_grid<FSR_IO>(int64_t, int, int *);
-template cudaError_t warpnd_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, int, int64_t, int, cudaStream_t);
 template cudaError_t warpsegd_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, int64_t, int, cudaStream_t);
 template cudaError_t cta64d_launch<FSR_IO>(const Pair64Args<FSR_IO> &, int, cudaStream_t);
 template cudaError_t generic_launch<double, FSR_IO>(const ImageArgs<double, FSR_IO> &, int, cudaStream_t);

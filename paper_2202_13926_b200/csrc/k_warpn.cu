@@ -60,6 +60,34 @@ cudaError_t seg_go(const Warp32Args &a, int sms, cudaStream_t st) {
     }
 }
 
+// fp64 (validation + re-runs); the argmax variants only pick the cross-lane
+// u64 max implementation (the keys carry the full tie rank: identical results),
+// so supports outside the paper grid build redux alone
+template <int N, int AM, typename IO>
+cudaError_t wnd_go(const Pair64Args<IO> &a, int64_t want, int sms, cudaStream_t st) {
+    constexpr int WARPS = 4;
+    auto k = warpnd_kernel<N, WARPS, AM, IO>;
+    const size_t smem = sizeof(WarpNdSmem<N, WARPS>);
+    int grid = 1;
+    cudaError_t e = persistent_grid(k, WARPS * 32, smem, (want + WARPS - 1) / WARPS, sms, &grid);
+    if (e != cudaSuccess) return e;
+    k<<<grid, WARPS * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <typename IO, int N>
+cudaError_t warpnd_launch_n(const Pair64Args<IO> &a, int am, int64_t want, int sms, cudaStream_t st) {
+    if constexpr (N == 16) {
+        return kNotBuilt;
+    } else if constexpr (N == 4 || N == 8 || N == 24) {
+        if (am == AM_SHFL) return wnd_go<N, AM_SHFL>(a, want, sms, st);
+        if (am == AM_SMEM) return wnd_go<N, AM_SMEM>(a, want, sms, st);
+        return wnd_go<N, AM_REDUX>(a, want, sms, st);
+    } else {
+        return wnd_go<N, AM_REDUX>(a, want, sms, st);
+    }
+}
+
 template <typename IO, int N>
 cudaError_t warpseg_launch(const Warp32Args &a, bool guard, int opts, int sms, cudaStream_t st) {
     if (opts == 0) return guard ? seg_go<IO, N, true, 0>(a, sms, st) : seg_go<IO, N, false, 0>(a, sms, st);
@@ -71,17 +99,21 @@ template <typename IO, int N>
 cudaError_t warpn_launch(const Warp32Args &a, const Warp32Maps &maps, int am, bool guard, int opts,
                          int sms, cudaStream_t st) {
     if constexpr (N == 16) {
-        return kNotBuilt;  // N = 16: warp16 / warpseg
-    } else {
+        return kNotBuilt;  // N = 16: warp16
+    } else if constexpr (N == 4 || N == 8 || N == 24) {
         if (am == AM_SHFL) return by_opts<IO, N, AM_SHFL>(a, maps, guard, opts, sms, st);
         if (am == AM_SMEM) return by_opts<IO, N, AM_SMEM>(a, maps, guard, opts, sms, st);
-        if (am == AM_REDUX) return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
-        return kNotBuilt;
+        return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
+    } else {
+        // supports outside the paper grid: pair keys make every argmax variant
+        // give the same selections, so only redux is built
+        return by_opts<IO, N, AM_REDUX>(a, maps, guard, opts, sms, st);
     }
 }
 
 template cudaError_t warpn_launch<FSR_IO, FSR_N>(const Warp32Args &, const Warp32Maps &, int, bool,
                                                  int, int, cudaStream_t);
 template cudaError_t warpseg_launch<FSR_IO, FSR_N>(const Warp32Args &, bool, int, int, cudaStream_t);
+template cudaError_t warpnd_launch_n<FSR_IO, FSR_N>(const Pair64Args<FSR_IO> &, int, int64_t, int, cudaStream_t);
 
 }  // namespace fsr

@@ -42,17 +42,17 @@ def effective_guard_tau(support: int, iterations: int, guard_tau: float = DEFAUL
     guard_tau_for): an explicit tau > 0 as given, else 5e-5 (1e-4 for N=64)."""
     if guard_tau > 0.0:
         return float(guard_tau)
-    return 1e-4 if support >= 64 else 2e-4 if support <= 8 else 5e-5
+    return 1e-4 if support >= 64 else 2e-4 if support <= 14 else 5e-5
 
 
 def effective_guard_kappa(iterations: int, guard_kappa: float = DEFAULT_GUARD_KAPPA,
                           support: int = 32) -> float:
     """The guard's scale term (fsr_abi.cu guard_kappa_for): a block is re-run in
     fp64 when b1 - b2 <= tau b1 + kappa sqrt(b1 B0) at some iteration; explicit
-    kappa > 0 as given, < 0 off, else 1e-7 * max(0, I/100 - 1) (0 for N <= 8)."""
+    kappa > 0 as given, < 0 off, else 1e-7 * max(0, I/100 - 1) (0 for N <= 14)."""
     if guard_kappa > 0.0:
         return float(guard_kappa)
-    if guard_kappa < 0.0 or support <= 8:
+    if guard_kappa < 0.0 or support <= 14:
         return 0.0
     return 1e-7 * max(0.0, iterations / 100.0 - 1.0)
 
