@@ -26,8 +26,8 @@ def main():
     fails = 0
     t0 = time.time()
     for c in range(n):
-        N = int(rng.choice([4, 8, 16, 24, 32, 64]))
-        B = int(rng.choice([2, 4] if N == 4 else [2, 4, 6] if N < 64 else [4, 6, 8]))
+        N = int(rng.choice([4, 6, 8, 10, 12, 14, 16, 18, 20, 24, 32, 64]))
+        B = int(rng.choice([2, 4] if N <= 6 else [2, 4, 6] if N < 64 else [4, 6, 8]))
         if (N - B) % 2:
             B += 1
         reducer = "linear" if N == 64 else str(rng.choice(["tree", "linear"]))
