@@ -82,11 +82,13 @@ def main():
                                    (64, False): "cta64, in-warp redux (+cta64d fp64 re-runs)",
                                    (64, True): "cta64d",
                                    (24, False): "warpn (+warpnd re-runs)", (24, True): "warpnd",
-                                   (8, False): "warpseg, 4 blocks/warp (+warpnd re-runs)",
-                                   (8, True): "warpnd",
-                                   (4, False): "warpseg, 8 blocks/warp (+warpnd re-runs)",
-                                   (4, True): "warpnd"}
-                                  .get((N, args.precision == "fp64" or I > 300), "generic")}
+                                   (8, False): "warpseg, 4 blocks/warp (+warpsegd re-runs)",
+                                   (8, True): "warpsegd",
+                                   (4, False): "warpsegd (a guarded N=4 request is served in fp64)",
+                                   (4, True): "warpsegd"}
+                                  .get((N, args.precision == "fp64" or I > 300),
+                                       ("warpnd" if args.precision == "fp64" or I > 300 else
+                                        "warpn (+warpnd re-runs)") if N % 2 == 0 and N <= 20 else "generic")}
                 line["served_fp64"] = stats.get("served_fp64")
                 print(json.dumps(line), flush=True)
 
