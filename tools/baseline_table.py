@@ -46,10 +46,13 @@ def main():
     fl = [ln for ln in full if ln.startswith("fp")]
     out.append(row("configs[1] 1080p, N=32, I=100, guarded fp32", load("bench_1080p_n32.json"),
                    f"≈ {4 * cb['value']:.3f} (4× the 4K rate)", "; ".join(fl) + " (whole frame)"))
+    if os.path.exists(os.path.join(D, "bench_1080p_n32_i200.json")):
+        out.append(row("configs[4]: 1080p, N=32, I=200, guarded fp32 (replayed re-runs)",
+                       load("bench_1080p_n32_i200.json"), "—", "whole frame: fp32 max\\|Δ\\| 3.6e-4"))
     d = load("bench_stream64.json")
     out.append(f"| configs[3] 64 × 1080p stream, N=32 | 1 | {d['value']:.1f} (e2e {d['e2e']['value']:.1f}) | "
                f"{d['mpixel_per_s']:.0f} | as configs[1] | — | — | as configs[1] |")
-    for n in (16, 64, 24, 8, 4):
+    for n in (16, 64, 24, 20, 12, 8, 4):
         f = f"bench_1080p_n{n}.json"
         if os.path.exists(os.path.join(D, f)):
             out.append(row(f"configs[4] / paper grid: 1080p, N={n}, I=100, guarded fp32", load(f), "—",

@@ -8,7 +8,7 @@ timeout 900 python -m pytest tests -m gpu -q --timeout 300 2>&1 | tail -2 > $O/p
 timeout 900 python -m pytest tests/test_gpu_fullframe.py -m gpu -q -s 2>&1 | grep -oE "N=[0-9]+ 1080p.*|fp(32|64) 1080p.*|[0-9]+ passed.*|[0-9]+ failed.*" > $O/fullframe_1080p.txt
 timeout 600 python bench.py > $O/bench_4k_default.json 2> $O/e1.err
 timeout 600 python bench.py --precision fp64 --no-cpu > $O/bench_4k_fp64.json 2> $O/e2.err
-for s in 32 16 24 8 4; do
+for s in 32 16 24 20 12 8 4; do
   timeout 300 python bench.py --workload 1080p --support $s --no-cpu > $O/bench_1080p_n$s.json 2> $O/e_$s.err
 done
 timeout 300 python bench.py --workload 1080p --support 64 --reducer linear --no-cpu > $O/bench_1080p_n64.json 2> $O/e_64.err
