@@ -120,7 +120,8 @@ def reconstruct(image, mask, block: int = 4, support: int = 32, iterations: int 
 
 def reconstruct_image(sampled: SampledImage, params: FsrParams, reducer: str = "tree",
                       early_stop: bool = False, *, precision: str = "fp64", devices=None,
-                      argmax: str = "redux", guard_tau: float = DEFAULT_GUARD_TAU) -> GrayImage:
+                      argmax: str = "redux", guard_tau: float = DEFAULT_GUARD_TAU,
+                      guard_kappa: float = DEFAULT_GUARD_KAPPA) -> GrayImage:
     """Drop-in for fsrkit.reconstruct_image: every target block reconstructed
     independently on the GPU and stitched; empty-support blocks get the mean of
     the known samples ("no known samples" ValueError if there is none).
@@ -129,7 +130,7 @@ def reconstruct_image(sampled: SampledImage, params: FsrParams, reducer: str = "
     out = reconstruct(sampled.image.pixels, sampled.mask, params.block, params.support,
                       params.iterations, params.rho, params.gamma, reducer=reducer,
                       early_stop=early_stop, precision=precision, devices=devices,
-                      argmax=argmax, guard_tau=guard_tau)
+                      argmax=argmax, guard_tau=guard_tau, guard_kappa=guard_kappa)
     return GrayImage(out)
 
 
