@@ -336,7 +336,7 @@ def run_stream(args):
     def step():
         for j in range(len(mine)):
             eng.reconstruct_device(d_px[j].data_ptr(), W, d_mk[j].data_ptr(), W, H, W, 0, brows,
-                                   d_out.data_ptr(), W, params, stream.cuda_stream)
+                                   d_out.data_ptr(), W, params, stream.cuda_stream, io="f32")
 
     def barrier():
         if world > 1:

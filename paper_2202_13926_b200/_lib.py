@@ -272,9 +272,10 @@ class Engine:
 
     def reconstruct_device(self, d_px, px_pitch, d_mask, mask_pitch, height, width, row0, row1,
                            d_out, out_pitch, params: FsrParamsC, stream=0,
-                           fill: float = float("nan"), io: str = "f32"):
+                           fill: float = float("nan"), *, io: str):
         """Device pointers (ints), asynchronous on ``stream`` (a cudaStream_t as int).
-        ``io``: pixel type "f32" or "f64"; ``fill`` as in reconstruct_rows (NaN:
+        ``io`` (required: raw pointers carry no dtype): pixel type "f32" or "f64"
+        of d_px and d_out; ``fill`` as in reconstruct_rows (NaN:
         the device computes the mean from all ``height`` rows of d_px/d_mask)."""
         fn = {"f32": self._L.fsr_reconstruct_device_f32, "f64": self._L.fsr_reconstruct_device_f64}[io]
         self._check(fn(self._h, ctypes.byref(params), ctypes.c_void_p(d_px), px_pitch,

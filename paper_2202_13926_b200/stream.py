@@ -62,7 +62,7 @@ class FrameStream:
         self.s_run.wait_event(self.ev_in[s])
         self.eng.reconstruct_device(self.d_px[s].data_ptr(), self.W, self.d_mk[s].data_ptr(), self.W,
                                     self.H, self.W, 0, n_block_rows, self.d_out[s].data_ptr(), self.W,
-                                    self.params, self.s_run.cuda_stream)
+                                    self.params, self.s_run.cuda_stream, io="f32")
         self.ev_run[s].record(self.s_run)
         self.s_out.wait_event(self.ev_run[s])
         with torch.cuda.stream(self.s_out):

@@ -229,7 +229,7 @@ def test_device_api_matches_host_api():
     p = _lib.make_params(4, 14, 100)
     H, W = px.shape
     eng.reconstruct_device(px.data_ptr(), W, mk.data_ptr(), W, H, W, 0, (H + 3) // 4,
-                           out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                           out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
     torch.cuda.synchronize()
     host = fsr.reconstruct(d["sampled"].astype(np.float32), d["mask"], 4, 32, 100)
     assert np.array_equal(out.cpu().numpy(), host.astype(np.float32))
@@ -346,7 +346,7 @@ def test_device_api_fill_and_no_samples():
     for _ in range(2):
         d_out = torch.empty_like(d_px)
         eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
-                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
         assert eng.last_stats()["empty_blocks"] > 0
         outs.append(d_out.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
@@ -357,7 +357,7 @@ def test_device_api_fill_and_no_samples():
     d_mk.zero_()
     d_px.zero_()
     eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
-                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
     with pytest.raises(ValueError, match="no known samples"):
         eng.last_stats()
 
@@ -543,7 +543,7 @@ def test_device_api_chunks_equal_unchunked(monkeypatch):
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
             eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
-                                   d_out.data_ptr(), W, p, s.cuda_stream)
+                                   d_out.data_ptr(), W, p, s.cuda_stream, io="f32")
             st = eng.last_stats()
         torch.cuda.synchronize()
         outs.append(d_out.cpu().numpy())
@@ -575,7 +575,7 @@ def test_host_api_chunks_tma_rows(support, reducer):
     d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
     d_out = torch.empty_like(d_px)
     eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
-                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
     torch.cuda.synchronize()
     want = d_out.cpu().numpy()
     for _ in range(2):
@@ -613,7 +613,7 @@ def test_host_api_chunk_pipeline(precision):
         d_mk = torch.tensor(mask.astype(np.uint8), device="cuda")
         d_out = torch.empty_like(d_px)
         eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, (H + 3) // 4,
-                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                               d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
         torch.cuda.synchronize()
         assert np.array_equal(d_out.cpu().numpy(), out)
     _, tr = fsr.reconstruct(px, mask, 4, 16, 40, precision=precision, argmax="redux", return_trace=True)
@@ -644,7 +644,7 @@ def test_full_size_properties(H, W, N, reducer):
     d_out = torch.empty_like(d_px)
     brows = H // B
     eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, brows,
-                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream)
+                           d_out.data_ptr(), W, p, torch.cuda.current_stream().cuda_stream, io="f32")
     st = eng.last_stats()
     out = d_out.cpu().numpy()
     assert 0.005 < st["rerun_blocks"] / st["blocks"] < 0.2  # tau doubles at N=64 (guard_tau_for)

@@ -45,7 +45,7 @@ do = torch.empty_like(dp)
 s = torch.cuda.current_stream()
 def dev():
     eng.reconstruct_device(dp.data_ptr(), W, dm.data_ptr(), W, H, W, 0, brows, do.data_ptr(), W, p,
-                           s.cuda_stream)
+                           s.cuda_stream, io="f64")
     s.synchronize()
 print("device          %.2f ms" % timed(dev))
 t0 = time.perf_counter(); a = np.empty((H, W)); a[:] = 1.0; t1 = time.perf_counter()

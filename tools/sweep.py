@@ -51,12 +51,12 @@ def main():
     def timed(p, rows, reps=1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, rows, d_out.data_ptr(), W,
-                               p, st.cuda_stream)
+                               p, st.cuda_stream, io="f32")
         torch.cuda.synchronize()
         e0.record(st)
         for _ in range(reps):
             eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, rows,
-                                   d_out.data_ptr(), W, p, st.cuda_stream)
+                                   d_out.data_ptr(), W, p, st.cuda_stream, io="f32")
         e1.record(st)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps, eng.last_stats()
