@@ -426,7 +426,13 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
             mbits |= (uint32_t)(in && __ldg(mp + k * mpitch) != 0) << k;
         }
     }
-    double2 *tl = t + lane;  // column `lane` of the tile
+    // Tile column layout (bank-conflict-free for every 16-byte access of the
+    // prologue): window column n is stored at p(n) = n/2 for even n and
+    // 16 + ((n/2 + 4) mod 16) for odd n -- any 8 consecutive lanes hit 8
+    // distinct 16-byte bank groups -- and the row FFT writes frequency f back
+    // at column f, so the column FFT and the split read consecutive columns.
+    const int pcol = (lane & 1) ? 16 + (((lane >> 1) + 4) & 15) : lane >> 1;
+    double2 *tl = t + pcol;  // window column `lane` of the tile
     double energy = 0.0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -440,33 +446,33 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
     }
     __syncwarp();
     // Each 32-point line is done as two 16-point halves (even / odd samples) with
-    // the radix-2 combine written back in place: line position 2m holds
-    // frequency m, position 2m+1 frequency m+16 (permutation s below).  Peak
-    // live data: 16 complex doubles.
-    const int cv = lane < 16 ? 2 * lane : 2 * (lane - 16) + 1;
+    // the radix-2 combine written back in place.  Rows: even sample j at column
+    // j, odd sample j at column 16 + ((j + 4) mod 16); frequency f ends at column
+    // f.  Columns: line position 2m holds frequency m, position 2m+1 frequency
+    // m+16 (permutation s below).  Peak live data: 16 complex doubles.
     {
         cpx<double> xv[16];
         // rows (lane = window row)
         double2 *tr_ = t + lane * W32_TS;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = tr_[2 * j]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tr_[j]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) tr_[2 * j] = make_double2(xv[j].re, xv[j].im);
+        for (int j = 0; j < 16; ++j) tr_[j] = make_double2(xv[j].re, xv[j].im);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) { const double2 z = tr_[2 * j + 1]; xv[j] = {z.x, z.y}; }
+        for (int j = 0; j < 16; ++j) { const double2 z = tr_[16 + ((j + 4) & 15)]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
-            const double2 e = tr_[2 * m];
+            const double2 e = tr_[m];
             const double c = tw_cos(m), sn = tw_sin(m);
             const double tr = xv[m].re * c + xv[m].im * sn, ti = xv[m].im * c - xv[m].re * sn;
-            tr_[2 * m] = make_double2(e.x + tr, e.y + ti);
-            tr_[2 * m + 1] = make_double2(e.x - tr, e.y - ti);
+            tr_[m] = make_double2(e.x + tr, e.y + ti);
+            tr_[m + 16] = make_double2(e.x - tr, e.y - ti);
         }
         __syncwarp();
-        // columns (lane = frequency v, stored at line position cv)
-        double2 *tc = t + cv;
+        // columns (lane = frequency v, at tile column v)
+        double2 *tc = t + lane;
 #pragma unroll
         for (int j = 0; j < 16; ++j) { const double2 z = tc[2 * j * W32_TS]; xv[j] = {z.x, z.y}; }
         fft_pow2<4>(xv);
@@ -485,13 +491,11 @@ __device__ __forceinline__ double w32_prologue_f64(const Warp32Args &a, const Wa
         }
         __syncwarp();
     }
-    // split: Z[u][v] sits at (s(u), s(v)), s(f) = f < 16 ? 2f : 2(f-16)+1.  This
+    // split: Z[u][v] sits at (s(u), v), s(f) = f < 16 ? 2f : 2(f-16)+1.  This
     // lane keeps spectral column v (its tie-rank order column, see the kernel).
     // R and W are rounded to fp32 once, W kept in registers until every read is done.
-    const int sv = v < 16 ? 2 * v : 2 * (v - 16) + 1;
     const int mv = (32 - v) & 31;
-    const int cm = mv < 16 ? 2 * mv : 2 * (mv - 16) + 1;
-    const double2 *tv = t + sv, *tm = t + cm;
+    const double2 *tv = t + v, *tm = t + mv;
     float2 Wf[32];
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
