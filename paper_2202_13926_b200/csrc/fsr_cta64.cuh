@@ -58,22 +58,30 @@ struct C64Smem {
 };
 
 __device__ __forceinline__ int c64_pos(int f) { return ((f & 15) << 2) | (f >> 4); }
+// Physical tile column of logical column c: the low two bits XOR-ed with bits
+// 3-4.  Eight consecutive columns stay in eight distinct 16-byte bank groups
+// (the window store, thread = column), and so do the columns c64_pos(v) of
+// eight consecutive frequencies v (the split) -- both 4-way conflicts without it.
+__device__ __forceinline__ int c64_col(int c) { return c ^ ((c >> 3) & 3); }
 
 // One 64-point forward DFT line of the tile, shared by 2 threads per line
 // (phase A: sub-FFTs r and r + 2; phase B: 8 combines each), all 64 lines.
-// Line `ln` element `e` is at t[ln * ls + e * es].
-__device__ __forceinline__ void c64_fft_lines(double2 *t, int ls, int es, const double2 *tw, int tid) {
+// ROWS: line `ln` is tile row ln, element e at physical column c64_col(e);
+// otherwise line `ln` is physical column ln, element e in row e.
+template <bool ROWS>
+__device__ __forceinline__ void c64_fft_lines(double2 *t, const double2 *tw, int tid) {
     const int ln = tid & 63, r0 = tid >> 6;  // r0 in {0, 1}
-    double2 *line = t + ln * ls;
+    double2 *line = ROWS ? t + ln * C64_TS : t + ln;
+    auto el = [&](int e) -> double2 & { return ROWS ? line[c64_col(e)] : line[e * C64_TS]; };
 #pragma unroll
     for (int q = 0; q < 2; ++q) {  // phase A: 16-point FFTs of samples 4m + r, in place at 4k + r
         const int r = r0 + 2 * q;
         cpx<double> xv[16];
 #pragma unroll
-        for (int m = 0; m < 16; ++m) { const double2 z = line[(4 * m + r) * es]; xv[m] = {z.x, z.y}; }
+        for (int m = 0; m < 16; ++m) { const double2 z = el(4 * m + r); xv[m] = {z.x, z.y}; }
         fft_pow2<4>(xv);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) line[(4 * k + r) * es] = make_double2(xv[k].re, xv[k].im);
+        for (int k = 0; k < 16; ++k) el(4 * k + r) = make_double2(xv[k].re, xv[k].im);
     }
     __syncthreads();
 #pragma unroll 2
@@ -82,7 +90,7 @@ __device__ __forceinline__ void c64_fft_lines(double2 *t, int ls, int es, const 
         double2 a[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            const double2 f = line[(4 * k + r) * es];
+            const double2 f = el(4 * k + r);
             if (r == 0) {
                 a[0] = f;
             } else {
@@ -95,10 +103,10 @@ __device__ __forceinline__ void c64_fft_lines(double2 *t, int ls, int es, const 
         const double2 s13 = make_double2(a[1].x + a[3].x, a[1].y + a[3].y);
         const double2 d13 = make_double2(a[1].x - a[3].x, a[1].y - a[3].y);
         // y_q = sum_r a_r (-i)^{rq}
-        line[(4 * k + 0) * es] = make_double2(s02.x + s13.x, s02.y + s13.y);
-        line[(4 * k + 1) * es] = make_double2(d02.x + d13.y, d02.y - d13.x);
-        line[(4 * k + 2) * es] = make_double2(s02.x - s13.x, s02.y - s13.y);
-        line[(4 * k + 3) * es] = make_double2(d02.x - d13.y, d02.y + d13.x);
+        el(4 * k + 0) = make_double2(s02.x + s13.x, s02.y + s13.y);
+        el(4 * k + 1) = make_double2(d02.x + d13.y, d02.y - d13.x);
+        el(4 * k + 2) = make_double2(s02.x - s13.x, s02.y - s13.y);
+        el(4 * k + 3) = make_double2(d02.x - d13.y, d02.y + d13.x);
     }
     __syncthreads();
 }
@@ -248,16 +256,16 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 f = (double)pf[k];
                 w = __ldg(a.decay64 + r * 64 + v);
             }
-            t[r * C64_TS + v] = make_double2(f * w, w);
+            t[r * C64_TS + c64_col(v)] = make_double2(f * w, w);
             energy = fma(f * f, w, energy);
         }
         __syncthreads();
-        c64_fft_lines(t, C64_TS, 1, sm.tw, tid);  // rows
-        c64_fft_lines(t, 1, C64_TS, sm.tw, tid);  // columns
+        c64_fft_lines<true>(t, sm.tw, tid);   // rows
+        c64_fft_lines<false>(t, sm.tw, tid);  // columns
         // ---- split (thread (v, h): rows 16h + i and + 32 of column v)
         float2 re[16], im[16], Wl[16], Wh[16];
         {
-            const int pv = c64_pos(v), pmv = c64_pos((64 - v) & 63);
+            const int pv = c64_col(c64_pos(v)), pmv = c64_col(c64_pos((64 - v) & 63));
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
 #pragma unroll
@@ -617,18 +625,18 @@ __global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a
                     f = (double)a.px[y * a.px_pitch + x];
                     w = __ldg(a.decay + r * 64 + v);
                 }
-                sm.tile[r * C64_TS + v] = make_double2(f * w, w);
+                sm.tile[r * C64_TS + c64_col(v)] = make_double2(f * w, w);
                 energy = fma(f * f, w, energy);
             }
         }
         __syncthreads();
-        c64_fft_lines(sm.tile, C64_TS, 1, sm.tw, tid);  // rows
-        c64_fft_lines(sm.tile, 1, C64_TS, sm.tw, tid);  // columns
+        c64_fft_lines<true>(sm.tile, sm.tw, tid);   // rows
+        c64_fft_lines<false>(sm.tile, sm.tw, tid);  // columns
         // ---- Hermitian split: R to registers, W staged through global memory
         double2 *gW = a.scratch + (int64_t)blockIdx.x * 4096;
         double2 rl[16], rh[16];
         {
-            const int pv_ = c64_pos(v), pmv = c64_pos((64 - v) & 63);
+            const int pv_ = c64_col(c64_pos(v)), pmv = c64_col(c64_pos((64 - v) & 63));
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
 #pragma unroll

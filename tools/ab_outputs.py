@@ -19,6 +19,7 @@ CASES = [  # (H, W, N, I, reducer, precision)
     (540, 960, 16, 100, "tree", "fp32"),
     (540, 960, 16, 100, "tree", "fp64"),
     (540, 960, 64, 100, "linear", "fp32"),
+    (270, 480, 64, 60, "linear", "fp64"),
     (540, 960, 24, 100, "tree", "fp32"),
     (540, 960, 8, 100, "tree", "fp32"),
     (540, 960, 12, 100, "tree", "fp32"),
