@@ -724,10 +724,15 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
                     kp = (f2u(po) & a.key_mask) | (31u ^ prk);
                     if (H && !((canon >> up_row) & 1u)) kp = 0u;
                 }
-                // lane id from the tail's opaque tid read (not a second S2R)
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu,
-                                                      ((int)(tid & 31u) == wl) ? max(m2, kp) : m1);
-                const float b2 = __uint_as_float(k2 & ~31u);
+                // this lane's candidate (lane id from the tail's opaque tid read)
+                const uint32_t cand = ((int)(tid & 31u) == wl) ? max(m2, kp) : m1;
+                // b2 is the warp maximum of the candidates.  The test below is made per
+                // lane on its own candidate instead: the largest per-lane result IS the
+                // test of b2 (IEEE rounding is monotonic), so fl and the first flagged
+                // iteration are reduced over the warp once, after the loop, and no
+                // second cross-lane reduction sits in the iteration's dependency chain
+                // (the guard study keeps the warp value for its gap statistics).
+                const float b2 = __uint_as_float((STUDY ? __reduce_max_sync(0xffffffffu, cand) : cand) & ~31u);
                 // near-tie iff b2 >= b1 (1 - tau) - ks sqrt(b1), ks = kappa sqrt(B0)
                 float gtest;
                 if (KAPPA) {
@@ -767,7 +772,11 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
         }
-        flagged |= fl >= 0.f;
+        flagged |= __any_sync(0xffffffffu, fl >= 0.f);  // the per-lane guard tests (above)
+        if (REC) {  // the first flagged iteration over the lanes
+            const uint32_t k = __reduce_min_sync(0xffffffffu, kf < 0 ? 0xffffffffu : (uint32_t)kf);
+            kf = k == 0xffffffffu ? -1 : (int)k;
+        }
         if (has_pend) {
             const float2 e = w32_cs[sidx];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));
