@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             uint32_t kw;
             int wl;
             cross_lane_best<ARGMAX, PK>(m1, kw, wl, sm.red_key[wid], sm.red_rank[wid]);
-            uint32_t k1w = kw, k2w = 0u;
+            uint32_t k1w = kw, cand2 = 0u;  // cand2: this thread's b2 candidate if its warp wins
             float cre, cim;
             if (PK) {
                 // the warp's winning pair (row 16h + i and + 32): both halves'
@@ -364,9 +364,9 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
                 cim = __shfl_sync(0xffffffffu, cim, wl);
                 const int ur = ur0 + (hi ? 32 : 0);
                 k1w = (kw & a.key_mask) | (uint32_t)(63 - ur);  // the bin's row for phase 2
-                k2w = __reduce_max_sync(0xffffffffu, lane == wl ? max(m2, f2u(po) & a.key_mask) : m1);
+                cand2 = lane == wl ? max(m2, f2u(po) & a.key_mask) : m1;
             } else {
-                k2w = GUARD ? __reduce_max_sync(0xffffffffu, lane == wl ? m2 : m1) : 0u;
+                cand2 = GUARD ? (lane == wl ? m2 : m1) : 0u;
                 const int ur = 63 - (int)(kw & 63u);
                 float4 q;
                 switch ((ur & 31) & 15) {
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             C64Slot *sl = sm.slot[it & 1];
             if (lane == 0) {
                 sl[wid].k1 = k1w;
-                sl[wid].k2 = k2w;
+                sl[wid].k2 = 0u;  // the guard tests per thread (below)
                 sl[wid].cre = cre;
                 sl[wid].cim = cim;
                 sl[wid].lane = wl;
@@ -423,7 +423,14 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             pu = bu;
             pv = bv;
             if (GUARD) {
-                const float b2 = __uint_as_float(second & ~63u);
+                // b2 is the CTA maximum of the threads' candidates (the winning
+                // thread's runner-up, everyone else's best); the test is made per
+                // thread on its own candidate -- the largest per-thread result is the
+                // test of b2, rounding being monotonic -- and OR-ed over the CTA after
+                // the loop, so no reduction of b2 sits before the slot barrier
+                (void)second;
+                const uint32_t c2 = (wid == bw && lane == wl) ? cand2 : m1;
+                const float b2 = __uint_as_float(c2 & ~63u);
                 const float sb1 = sqrt_approx(b1);  // scale term (see warp32)
                 if (H && it == 0) ks = a.kappa * sb1;
                 const bool g = b2 >= fmaf(-ks, sb1, b1 * one_minus_tau) || b1 * one_minus_tau < thr;
@@ -441,6 +448,14 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         }
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
+        }
+        if (GUARD) flagged = __syncthreads_or(flagged) != 0;  // the per-thread guard tests
+        if (REC && flagged) {  // the first flagged iteration over the CTA
+            const uint32_t k = __reduce_min_sync(0xffffffffu, kf < 0 ? 0xffffffffu : (uint32_t)kf);
+            if (lane == 0) sm.red_key[wid][0] = k;
+            __syncthreads();
+            const uint32_t km = min(min(sm.red_key[0][0], sm.red_key[1][0]), min(sm.red_key[2][0], sm.red_key[3][0]));
+            kf = km == 0xffffffffu ? -1 : (int)km;
         }
         const int done = it;
         if (sel_b)

@@ -352,8 +352,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             pu = bu;
             pv = bv;
             if (GUARD) {
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu, (lane == wl) ? m2 : m1);
-                const float b2 = __uint_as_float(k2 & ~31u);
+                // per-lane test on the lane's own b2 candidate, warp OR after the loop
+                // (no second reduction in the iteration chain; see warp32)
+                const float b2 = __uint_as_float(((lane == wl) ? m2 : m1) & ~31u);
                 float gtest;
                 if (KAPPA) {  // scale term (see warp32)
                     const float sb1 = sqrt_approx(b1);
@@ -382,7 +383,11 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
         }
-        flagged |= fl >= 0.f;
+        flagged |= __any_sync(0xffffffffu, fl >= 0.f);  // per-lane guard tests (see warp32)
+        if (REC) {  // the first flagged iteration over the lanes
+            const uint32_t k = __reduce_min_sync(0xffffffffu, kf < 0 ? 0xffffffffu : (uint32_t)kf);
+            kf = k == 0xffffffffu ? -1 : (int)k;
+        }
         if (has_pend) {
             const float2 e = sm.cs[sidx];
             acc = fmaf(gr, e.x, fmaf(-gi, e.y, acc));

@@ -504,8 +504,9 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
             pv = bv;
             if (GUARD) {
                 const uint32_t kp = f2u(po) & a.key_mask;
-                const uint32_t k2 = __reduce_max_sync(0xffffffffu, lane == wl ? max(m2, kp) : m1);
-                const float b2 = __uint_as_float(k2 & ~31u);
+                // per-lane test on the lane's own b2 candidate, warp OR after the loop
+                // (no second reduction in the iteration chain; see warp32)
+                const float b2 = __uint_as_float((lane == wl ? max(m2, kp) : m1) & ~31u);
                 float gtest;
                 if (KAPPA) {
                     const float sb1 = sqrt_approx(b1);
@@ -532,7 +533,11 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
         }
-        flagged |= fl >= 0.f;
+        flagged |= __any_sync(0xffffffffu, fl >= 0.f);  // per-lane guard tests (see warp32)
+        if (REC) {  // the first flagged iteration over the lanes
+            const uint32_t k = __reduce_min_sync(0xffffffffu, kf < 0 ? 0xffffffffu : (uint32_t)kf);
+            kf = k == 0xffffffffu ? -1 : (int)k;
+        }
         const int done = it;
         if (sel_b)
             for (int jj = done + lane; jj < a.iterations; jj += 32) sel_b[jj] = -1;

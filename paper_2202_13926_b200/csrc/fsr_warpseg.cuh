@@ -299,8 +299,9 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
             }
             if (GUARD) {
                 const uint32_t kp = f2u(po) & C::KMASK;
-                const uint32_t k2 = seg_max<N>(v == wl ? max(m2, kp) : m1);
-                const float b2 = __uint_as_float(k2 & C::KMASK);
+                // per-lane test on the lane's own b2 candidate, OR over the segment
+                // after the loop (no butterfly in the iteration chain; see warp32)
+                const float b2 = __uint_as_float((v == wl ? max(m2, kp) : m1) & C::KMASK);
                 const float omt = a.omt;
                 float gap;
                 if (KAPPA) {
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(WARPS * 32, seg_warps_per_sm<N>() / WARPS)
             step(std::false_type{}, it);
             ++it;
         }
-        flagged |= fl >= 0.f;
+        flagged |= ((__ballot_sync(0xffffffffu, fl >= 0.f) >> sbase) & C::SEGMASK) != 0u;
         if (sel_b)
             for (int jj = done + v; jj < a.iterations; jj += N) sel_b[jj] = -1;
         if (real && !empty && v == 0) {
