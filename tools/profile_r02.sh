@@ -24,8 +24,8 @@ FSR_NO_CHUNK=1 timeout 600 $NCU -k regex:warpn_kernel -s 2 -c 1 -o /tmp/wn24 pyt
 python tools/ncu_summary.py /tmp/wn24.ncu-rep $O/warpn24_1080p_ncu > /dev/null 2>&1
 FSR_NO_CHUNK=1 timeout 600 $NCU -k regex:warpnd_kernel -s 2 -c 1 -o /tmp/wnd24 python bench.py --workload 1080p --support 24 --precision fp64 --steps 1 --warmup 3 --no-cpu --no-e2e > $O/ncu_wnd24.log 2>&1
 python tools/ncu_summary.py /tmp/wnd24.ncu-rep $O/warpnd24_1080p_fp64_ncu > /dev/null 2>&1
-FSR_NO_CHUNK=1 timeout 600 $NCU -k regex:warpn_kernel -s 2 -c 1 -o /tmp/wn8 python bench.py --workload 1080p --support 8 --steps 1 --warmup 3 --no-cpu --no-e2e > $O/ncu_wn8.log 2>&1
-python tools/ncu_summary.py /tmp/wn8.ncu-rep $O/warpn8_1080p_ncu > /dev/null 2>&1
+
+
 rm -f $O/w32_4k.ncu-rep
 ls $O
 for f in $O/*_ncu.txt; do echo "== $f"; head -12 $f | grep -E "time_duration|issue_active|warps_active|registers|stall share"; done
