@@ -22,6 +22,9 @@ CASES = [  # (H, W, N, I, reducer, precision)
     (270, 480, 64, 60, "linear", "fp64"),
     (540, 960, 24, 100, "tree", "fp32"),
     (540, 960, 8, 100, "tree", "fp32"),
+    (540, 960, 8, 100, "linear", "fp64"),
+    (540, 960, 4, 100, "tree", "fp32"),
+    (540, 960, 4, 200, "linear", "fp64"),
     (540, 960, 12, 100, "tree", "fp32"),
     (270, 480, 32, 100, "tree", "fp32"),
     (540, 960, 32, 200, "tree", "fp32"),
