@@ -448,6 +448,12 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
         }
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
+            // replay build: a flagged block's remaining fp32 iterations are wasted
+            // work (its fp64 re-run replays only the prefix), see warp32.  Past 100
+            // iterations only (W32_EXIT build): the check is a CTA barrier, which at
+            // I = 100 (11 % flagged blocks) costs more than it saves (1080p 30.6 ->
+            // 32.1 ms; 33.0 with a run-time I test)
+            if (REC && (OPTS & W32_EXIT) && (it & 3) == 0 && __syncthreads_or(flagged)) break;
         }
         if (GUARD) flagged = __syncthreads_or(flagged) != 0;  // the per-thread guard tests
         if (REC && flagged) {  // the first flagged iteration over the CTA

@@ -532,6 +532,9 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
         }
         while (live && it < a.iterations) {
             if (step(std::false_type{})) ++it; else live = false;
+            // replay build: a flagged block's remaining fp32 iterations are wasted
+            // work (its fp64 re-run replays only the prefix), see warp32
+            if (REC && (it & 3) == 0 && __any_sync(0xffffffffu, fl >= 0.f)) break;
         }
         flagged |= __any_sync(0xffffffffu, fl >= 0.f);  // per-lane guard tests (see warp32)
         if (REC) {  // the first flagged iteration over the lanes

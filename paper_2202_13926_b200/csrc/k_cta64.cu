@@ -30,7 +30,9 @@ template <typename IO, int AM>
 cudaError_t cta64_launch(const Warp32Args &a, const Warp32Maps &maps, bool guard, int opts, int sms,
                          cudaStream_t st) {
     if constexpr (AM == AM_REDUX)
-        if (guard && (opts & LOPT_REPLAY)) return go<IO, AM, true, W32_REPLAY>(a, maps, sms, st);
+        if (guard && (opts & LOPT_REPLAY))
+            return a.iterations > 100 ? go<IO, AM, true, W32_REPLAY | W32_EXIT>(a, maps, sms, st)
+                                      : go<IO, AM, true, W32_REPLAY>(a, maps, sms, st);
     return guard ? go<IO, AM, true>(a, maps, sms, st) : go<IO, AM, false>(a, maps, sms, st);
 }
 

@@ -30,6 +30,7 @@ CASES = [  # (H, W, N, I, reducer, precision)
     (540, 960, 32, 200, "tree", "fp32"),
     (540, 960, 16, 200, "tree", "fp32"),
     (540, 960, 64, 200, "linear", "fp32"),
+    (540, 960, 24, 200, "tree", "fp32"),
 ]
 for H, W, N, I, red, prec in CASES:
     img = synth.frame(H, W, 7, "natural")
