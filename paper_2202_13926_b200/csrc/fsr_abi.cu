@@ -581,7 +581,11 @@ int enqueue_image(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px,
     // served by the fp64 kernels directly -- faster, and exact.
     const fsr_params *p_req = p;
     fsr_params pl = *p;
-    if (pl.precision == FSR_PREC_FP32 && pl.iterations > 300) pl.precision = FSR_PREC_FP64;
+    // (FSR_FP64_ABOVE: A/B knob.  Re-measured with the replay builds' early exit,
+    // 1080p: at I = 400 fp32 + replayed re-runs and fp64 tie within 5 % either way
+    // -- N=32 15.1 / 15.1, N=64 3.2 / 3.1, N=16 60 / 69, N=24 21 / 23 fps)
+    static const int fp64_above = [] { const char *e = std::getenv("FSR_FP64_ABOVE"); return e ? atoi(e) : 300; }();
+    if (pl.precision == FSR_PREC_FP32 && pl.iterations > fp64_above) pl.precision = FSR_PREC_FP64;
     // N = 4 (L = 0 at B = 4: the window is the block) re-runs ~45 % of the blocks,
     // and its segmented fp64 kernel is faster than fp32 + re-runs (1080p: 2226 vs
     // 1702 fps) -- and exact
