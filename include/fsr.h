@@ -24,14 +24,16 @@
 #ifndef FSR_H_
 #define FSR_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define FSR_ABI_VERSION 3  /* 2: f64 pixels on every path, explicit empty-support fill for strips;
-                              3: guard_kappa */
+#define FSR_ABI_VERSION 4  /* 2: f64 pixels on every path, explicit empty-support fill for strips;
+                              3: guard_kappa; 4: fsr_pin_host / fsr_unpin_host, direct DMA for
+                              page-locked host buffers */
 
 typedef enum {
     FSR_OK = 0,
@@ -94,6 +96,13 @@ const char *fsr_last_error(const fsr_engine *eng);
 const char *fsr_status_string(int status);
 int32_t fsr_abi_version(void);
 
+/* Page-lock (cudaHostRegister, portable) / release a host range, so host-buffer
+ * calls DMA to and from it directly instead of staging through the engine's
+ * pinned buffers.  Python's result arrays live in such a recycled pool.  The
+ * range must stay allocated until fsr_unpin_host. */
+int fsr_pin_host(void *p, size_t bytes);
+int fsr_unpin_host(void *p);
+
 /*
  * Whole-path call with HOST buffers (reconstruct_image).  px: H*W pixels on the
  * 0..255 scale, row-major; unknown pixels are ignored (the reference requires
@@ -109,6 +118,8 @@ int32_t fsr_abi_version(void);
  * The caller's buffers may be pageable: each device's chunks are staged
  * through engine-owned pinned buffers by a small host thread pool, and the
  * engine's devices run their strips concurrently (one host thread each).
+ * Page-locked buffers (cudaHostAlloc'd, or registered with fsr_pin_host) skip
+ * the staging: px/mask are copied to the device and results to `out` directly.
  */
 int fsr_reconstruct_f64(fsr_engine *eng, const fsr_params *p, const double *px,
                         const uint8_t *mask, int64_t height, int64_t width, double *out,

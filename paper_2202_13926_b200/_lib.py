@@ -8,6 +8,7 @@ every call raises.
 from __future__ import annotations
 
 import ctypes
+import mmap
 import os
 import threading
 
@@ -83,6 +84,10 @@ def load():
         L.fsr_last_error.restype = ctypes.c_char_p
         L.fsr_status_string.argtypes = [ctypes.c_int]
         L.fsr_status_string.restype = ctypes.c_char_p
+        L.fsr_pin_host.argtypes = [P, ctypes.c_size_t]
+        L.fsr_pin_host.restype = ctypes.c_int
+        L.fsr_unpin_host.argtypes = [P]
+        L.fsr_unpin_host.restype = ctypes.c_int
         L.fsr_abi_version.restype = i32
         L.fsr_reconstruct_f64.argtypes = [P, pp, P, P, i64, i64, P, P, P]
         L.fsr_reconstruct_f64.restype = ctypes.c_int
@@ -114,7 +119,8 @@ EXPORTED = ["fsr_params_init", "fsr_params_validate", "fsr_engine_create", "fsr_
             "fsr_last_error", "fsr_status_string", "fsr_abi_version", "fsr_reconstruct_f64",
             "fsr_reconstruct_f32", "fsr_reconstruct_rows_f32", "fsr_reconstruct_rows_f64",
             "fsr_reconstruct_device_f32", "fsr_reconstruct_device_f64", "fsr_iterate_spectra",
-            "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats", "fsr_spatial_oracle"]
+            "fsr_quarter_sample_device", "fsr_sq_error_device", "fsr_last_stats", "fsr_spatial_oracle",
+            "fsr_pin_host", "fsr_unpin_host"]
 
 
 def _ptr(a):
@@ -152,9 +158,14 @@ class _OutputPool:
 
     A fresh 4K f64 output (66 MB) costs ~1.5 ms of first-touch page faults per
     call inside the engine's copy-out; the pool hands out memory that was
-    faulted in by an earlier call.  Every call still returns a NEW array (the
-    reference returns a fresh GrayImage, core.py:24): its memory goes back to
-    the pool only when the array and every view of it are gone (_Lease)."""
+    faulted in by an earlier call.  Buffers of PIN_MIN bytes or more are
+    anonymous mappings (whole pages of their own) page-locked once with
+    fsr_pin_host, so the engine DMAs results straight into them (no staging
+    copy-out).  Every call still returns a NEW array (the reference returns a
+    fresh GrayImage, core.py:24): its memory goes back to the pool only when
+    the array and every view of it are gone (_Lease)."""
+
+    PIN_MIN = 1 << 20
 
     def __init__(self, max_cached_bytes=1 << 30):
         self._free = {}
@@ -162,19 +173,40 @@ class _OutputPool:
         self._max = max_cached_bytes
         self._lock = threading.Lock()
 
+    @staticmethod
+    def _addr(buf):
+        c = ctypes.c_char.from_buffer(buf)
+        a = ctypes.addressof(c)
+        del c
+        return a
+
     def take(self, nbytes):
         with self._lock:
             lst = self._free.get(nbytes)
             if lst:
                 self._cached -= nbytes
                 return lst.pop()
-        return bytearray(nbytes)
+        if nbytes < self.PIN_MIN:
+            return bytearray(nbytes)
+        buf = mmap.mmap(-1, nbytes)
+        try:  # page-locking is an optimisation: on failure the engine stages as usual
+            load().fsr_pin_host(self._addr(buf), nbytes)
+        except Exception:
+            pass
+        return buf
 
     def give_back(self, buf):
         with self._lock:
             if self._cached + len(buf) <= self._max:
                 self._free.setdefault(len(buf), []).append(buf)
                 self._cached += len(buf)
+                return
+        if isinstance(buf, mmap.mmap):
+            try:
+                load().fsr_unpin_host(self._addr(buf))
+            except Exception:
+                pass
+            buf.close()
 
 
 class _Lease:

@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -895,7 +896,12 @@ int chunk_count(const Device &d, int64_t block_rows) {
 #ifndef FSR_LANES
 #define FSR_LANES 8  // one stream per chunk at 4K (2 lanes: e2e 37.6, 4: 38.2, 8: 38.4 fps; device 38.8)
 #endif
-constexpr int kLanes = FSR_LANES;  // streams a chunked call alternates over
+// streams a chunked call alternates over (FSR_LANES_RT: run-time A/B knob, 1..16)
+static const int kLanes = [] {
+    const char *e = std::getenv("FSR_LANES_RT");
+    const int n = e ? atoi(e) : FSR_LANES;
+    return n < 1 ? 1 : n > 16 ? 16 : n;
+}();
 
 #ifndef FSR_STAGE_THREADS
 #define FSR_STAGE_THREADS 4  // host threads per device for the staging copies (incl. the caller)
@@ -1059,13 +1065,43 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
     // order: the persistent grids of the lanes' kernels run nearly one after the
     // other, so chunk c's copy-out overlaps chunks c+1.. on the GPU and only the
     // last chunk's is exposed.
+    // page-locked caller buffers (cudaHostAlloc / fsr_pin_host) are DMA'd directly:
+    // no staging copy of the input, no copy-out of the result
+    auto locked = [](const void *p, size_t bytes) {
+        auto one = [](const void *q) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+                (void)cudaGetLastError();
+                return false;
+            }
+            return at.type == cudaMemoryTypeHost;
+        };
+        return bytes > 0 && one(p) && one(static_cast<const char *>(p) + bytes - 1);
+    };
+    const int64_t ya_all = std::max<int64_t>(0, hp.row0 * B - L), yb_all = std::min<int64_t>(H, hp.row1 * B + L);
+    const int64_t oa_all = std::min<int64_t>(H, hp.row0 * B), ob_all = std::min<int64_t>(H, hp.row1 * B);
+    const bool direct_in = locked(px + ya_all * W, (size_t)(yb_all - ya_all) * W * sizeof(IO)) &&
+                           locked(mask + ya_all * W, (size_t)(yb_all - ya_all) * W);
+    const bool direct_out = locked(out + oa_all * W, (size_t)(ob_all - oa_all) * W * sizeof(IO));
     std::deque<Device *> fifo;  // lanes with a pending chunk, oldest first
+    // FSR_HOST_TRACE: host-side timeline of the call (stderr, ms since entry)
+    static const bool htrace = std::getenv("FSR_HOST_TRACE") != nullptr;
+    const auto t_entry = std::chrono::steady_clock::now();
+    auto ms_now = [&]() {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
+    };
     auto drain_one = [&]() -> int {  // the oldest pending chunk -> caller's buffer
         Device &ld = *fifo.front();
         fifo.pop_front();
+        const double t0 = htrace ? ms_now() : 0.0;
         CUDA_TRY(eng, cudaEventSynchronize(ld.ev1));
-        pool_copy(d.pool.get(), out + ld.pend_oa * W, ld.hout.p, ld.pend_ob - ld.pend_oa,
-                  (size_t)W * sizeof(IO));
+        const double t1 = htrace ? ms_now() : 0.0;
+        if (!direct_out)
+            pool_copy(d.pool.get(), out + ld.pend_oa * W, ld.hout.p, ld.pend_ob - ld.pend_oa,
+                      (size_t)W * sizeof(IO));
+        if (htrace)
+            fprintf(stderr, "host: drain rows %lld..%lld wait %.3f..%.3f copy-out ..%.3f ms\n",
+                    (long long)ld.pend_oa, (long long)ld.pend_ob, t0, t1, ms_now());
         ld.pending = false;
         return FSR_OK;
     };
@@ -1082,15 +1118,21 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         CUDA_TRY(eng, ld.px.ensure(px_bytes));
         CUDA_TRY(eng, ld.mask.ensure(mk_bytes));
         CUDA_TRY(eng, ld.out.ensure((size_t)rows_out * W * sizeof(IO)));
-        CUDA_TRY(eng, ld.hin.ensure(px_bytes + mk_bytes));
-        CUDA_TRY(eng, ld.hout.ensure((size_t)rows_out * W * sizeof(IO)));
+        if (!direct_in) CUDA_TRY(eng, ld.hin.ensure(px_bytes + mk_bytes));
+        if (!direct_out) CUDA_TRY(eng, ld.hout.ensure((size_t)rows_out * W * sizeof(IO)));
         if (sel) CUDA_TRY(eng, ld.sel.ensure((size_t)nb * it_stride * sizeof(int32_t)));
         if (done) CUDA_TRY(eng, ld.done.ensure((size_t)nb * sizeof(int32_t)));
-        pool_copy(d.pool.get(), ld.hin.p, px + ya * W, rows_in, (size_t)W * sizeof(IO));
-        pool_copy(d.pool.get(), ld.hin.as<char>() + px_bytes, mask + ya * W, rows_in, (size_t)W);
-        CUDA_TRY(eng, cudaMemcpyAsync(ld.px.p, ld.hin.p, px_bytes, cudaMemcpyHostToDevice, ld.stream));
-        CUDA_TRY(eng, cudaMemcpyAsync(ld.mask.p, ld.hin.as<char>() + px_bytes, mk_bytes,
-                                      cudaMemcpyHostToDevice, ld.stream));
+        const double ts0 = htrace ? ms_now() : 0.0;
+        const void *src_px = px + ya * W, *src_mk = mask + ya * W;
+        if (!direct_in) {
+            pool_copy(d.pool.get(), ld.hin.p, px + ya * W, rows_in, (size_t)W * sizeof(IO));
+            pool_copy(d.pool.get(), ld.hin.as<char>() + px_bytes, mask + ya * W, rows_in, (size_t)W);
+            src_px = ld.hin.p;
+            src_mk = ld.hin.as<char>() + px_bytes;
+        }
+        if (htrace) fprintf(stderr, "host: chunk %d staged %.3f..%.3f ms\n", c, ts0, ms_now());
+        CUDA_TRY(eng, cudaMemcpyAsync(ld.px.p, src_px, px_bytes, cudaMemcpyHostToDevice, ld.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(ld.mask.p, src_mk, mk_bytes, cudaMemcpyHostToDevice, ld.stream));
         const IO *vpx = ld.px.as<IO>() - ya * W;
         const uint8_t *vmask = ld.mask.as<uint8_t>() - ya * W;
         IO *vout = ld.out.as<IO>() - oa * W;
@@ -1100,8 +1142,9 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
                                ld.stream, d.chunk_ctrs.as<ChunkCtr>() + c, call,
                                d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
         if (rc) return rc;
-        CUDA_TRY(eng, cudaMemcpyAsync(ld.hout.p, ld.out.p, (size_t)rows_out * W * sizeof(IO),
-                                      cudaMemcpyDeviceToHost, ld.stream));
+        CUDA_TRY(eng, cudaMemcpyAsync(direct_out ? (void *)(out + oa * W) : ld.hout.p, ld.out.p,
+                                      (size_t)rows_out * W * sizeof(IO), cudaMemcpyDeviceToHost,
+                                      ld.stream));
         // traces (validation only) go straight to the caller's buffers
         if (sel)
             CUDA_TRY(eng, cudaMemcpyAsync(sel + r0 * bcols * it_stride, ld.sel.p,
@@ -1118,8 +1161,10 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
         d.used_tma = ld.used_tma;
         d.served_fp64 = ld.served_fp64;
     }
+    if (htrace) fprintf(stderr, "host: all chunks enqueued %.3f ms\n", ms_now());
     while (!fifo.empty())
         if ((rc = drain_one())) return rc;
+    if (htrace) fprintf(stderr, "host: drained %.3f ms\n", ms_now());
     for (int l = 0; l < nl; ++l) {
         Device &ld = *d.lanes[l];
         d.launches += ld.launches;
@@ -1269,6 +1314,24 @@ int fsr_params_validate(const fsr_params *p, char *msg, int msg_len) {
 }
 
 int32_t fsr_abi_version(void) { return FSR_ABI_VERSION; }
+
+int fsr_pin_host(void *p, size_t bytes) {
+    if (!p || bytes == 0) return FSR_EINVAL;
+    if (cudaHostRegister(p, bytes, cudaHostRegisterPortable) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return FSR_ECUDA;
+    }
+    return FSR_OK;
+}
+
+int fsr_unpin_host(void *p) {
+    if (!p) return FSR_EINVAL;
+    if (cudaHostUnregister(p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return FSR_ECUDA;
+    }
+    return FSR_OK;
+}
 
 const char *fsr_status_string(int status) {
     switch (status) {

@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for name in names:
         assert hasattr(L, name), name
     assert set(names) == set(_lib.EXPORTED)
-    assert L.fsr_abi_version() == 3
+    assert L.fsr_abi_version() == 4
 
 
 def test_params_validation_messages():
@@ -144,3 +144,14 @@ def test_output_pool_never_recycles_live_memory():
     assert pool._cached == 320
     c = _lib.new_image((3, 7), np.float32)
     assert c.flags.c_contiguous and c.flags.writeable and c.dtype == np.float32 and c.shape == (3, 7)
+    # large buffers: whole-page anonymous mappings, page-locked where a GPU is present
+    # (fsr_pin_host; without one the engine simply stages), unlocked when dropped
+    big = _lib._OutputPool(max_cached_bytes=0)
+    n = big.PIN_MIN * 2
+    d = np.frombuffer(_lib._Lease(big.take(n), big), dtype=np.float64)
+    assert d.size == n // 8 and d.flags.writeable and d.ctypes.data % 4096 == 0
+    d[:] = 3.0
+    assert float(d.sum()) == 3.0 * d.size
+    del d
+    gc.collect()
+    assert big._cached == 0  # over the cache limit: unpinned and unmapped
