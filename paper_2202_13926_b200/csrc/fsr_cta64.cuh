@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
             const int bv = (bw * 32 + sl[bw].lane) & 63;
             const float b1 = __uint_as_float(best & ~63u);
             if (sel_b && tid == 0) sel_b[it] = bu * 64 + bv;
-            if (REC && tid == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 64 + bv);
+            if (REC) seqw[it] = (uint16_t)(bu * 64 + bv);  // CTA-uniform: every thread stores it (see warp32)
             if (b1 < thr) {
                 if (GUARD && b1 >= thr * one_minus_tau) {
                     flagged = true;

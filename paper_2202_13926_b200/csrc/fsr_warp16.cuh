@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W16_WARPS_PER_SM / WARPS)
             const int bv = LT ? (int)bitrev4((uint32_t)(wl >> 1)) : (wl >> 1);
             const float b1 = __uint_as_float(kmax & ~31u);
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 16 + bv;
-            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 16 + bv);
+            if (REC) seqw[it] = (uint16_t)(bu * 16 + bv);  // uniform: every lane stores it (see warp32)
             if (EARLY && b1 < thr) {
                 if (GUARD && b1 >= thr * a.omt) {
                     flagged = true;

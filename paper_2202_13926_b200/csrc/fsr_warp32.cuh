@@ -703,7 +703,9 @@ __global__ void __launch_bounds__(WARPS * 32, FSR_W32_WARPS_PER_SM / WARPS)
             }
             const bool lo = bu < 16;
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * 32 + bv;
-            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * 32 + bv);
+            // every lane stores the same (warp-uniform) record: one wavefront, no branch
+            // (it < a.iterations == a.seq_stride here)
+            if (REC) seqw[it] = (uint16_t)(bu * 32 + bv);
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             gr = c.x * ginv;

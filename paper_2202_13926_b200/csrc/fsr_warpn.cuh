@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(WARPS * 32, wn_warps_per_sm<N>() / WARPS)
             const bool hi = __shfl_sync(0xffffffffu, (int)hl, wl) != 0;
             const int bu = j + (hi ? P : 0), bv = wl % N;
             if (TRACE && sel_b && lane == 0) sel_b[it] = bu * N + bv;
-            if (REC && lane == 0 && it < a.seq_stride) seqw[it] = (uint16_t)(bu * N + bv);
+            if (REC) seqw[it] = (uint16_t)(bu * N + bv);  // uniform: every lane stores it (see warp32)
             c.x = __shfl_sync(0xffffffffu, c.x, wl);
             c.y = __shfl_sync(0xffffffffu, c.y, wl);
             const float2 cs = sm.cs[(bu * pm + bv * pn) % N];
