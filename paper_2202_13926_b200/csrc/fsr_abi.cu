@@ -889,7 +889,12 @@ int chunk_count(const Device &d, int64_t block_rows) {
 #define FSR_MIN_CHUNKS 3
 #endif
     if (d.gap_debug || !d.chunking || block_rows < 8 * FSR_MIN_CHUNKS) return 1;
-    return (int)std::min<int64_t>(FSR_MAX_CHUNKS,
+    static const int max_chunks = [] {  // FSR_MAX_CHUNKS_RT: run-time A/B knob (<= 16)
+        const char *e = std::getenv("FSR_MAX_CHUNKS_RT");
+        const int n = e ? atoi(e) : FSR_MAX_CHUNKS;
+        return n < 1 ? 1 : n > 16 ? 16 : n;
+    }();
+    return (int)std::min<int64_t>(max_chunks,
                                   std::max<int64_t>(FSR_MIN_CHUNKS, block_rows / FSR_CHUNK_ROWS));
 }
 
