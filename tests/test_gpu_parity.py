@@ -584,6 +584,48 @@ def test_host_api_chunks_tma_rows(support, reducer):
         assert np.array_equal(out, want)
 
 
+@pytest.mark.gpu
+def test_host_api_page_locked_buffers():
+    """Page-locked host buffers (fsr_pin_host) are DMA'd directly -- input, output
+    or both -- instead of staged; every combination equals the pageable call
+    bitwise, including the empty-support fill written into the locked output."""
+    import mmap
+
+    from paper_2202_13926_b200 import _lib
+    H, W = 4 * 259, 256
+    img = oracle.synthetic_frame(H, W, 43)
+    sampled, mask = oracle.quarter_sample(img, 5)
+    mask[600:660, 100:160] = False  # empty supports: the host-side fill
+    px = np.where(mask, sampled, 0.0)
+    m8 = mask.astype(np.uint8)
+    p = _lib.make_params(4, 14, 40, precision="fp32")
+    eng = _lib.Engine([0])
+    L = _lib.load()
+    want = np.zeros((H, W))
+    eng.reconstruct_rows(px, m8, p, 0, H // 4, want)
+    assert eng.last_stats()["empty_blocks"] > 0
+
+    maps = []
+
+    def locked(a):
+        mm = mmap.mmap(-1, a.nbytes)
+        b = np.frombuffer(mm, dtype=a.dtype).reshape(a.shape)
+        b[...] = a
+        assert L.fsr_pin_host(b.ctypes.data, b.nbytes) == 0
+        maps.append((mm, b))
+        return b
+
+    lpx, lm8, lout = locked(px), locked(m8), locked(np.zeros((H, W)))
+    for a_px, a_m8, a_out in ((lpx, lm8, np.zeros((H, W))), (px, m8, lout), (lpx, lm8, lout)):
+        a_out[...] = -1.0
+        eng.reconstruct_rows(a_px, a_m8, p, 0, H // 4, a_out)
+        assert np.array_equal(a_out, want)
+    for mm, b in maps:
+        assert L.fsr_unpin_host(b.ctypes.data) == 0
+    del b, lpx, lm8, lout
+    maps.clear()
+
+
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
 def test_host_api_chunk_pipeline(precision):
     """Host-buffer calls on tall strips are pipelined in chunks over two streams
