@@ -208,6 +208,7 @@ struct Device {
     std::unique_ptr<Pool> pool;  // host staging copies (host-buffer calls)
     int last_chunks = 0;         // chunks of the last call (for its statistics)
     cudaEvent_t ck0[16] = {}, ck1[16] = {};  // per-chunk main-kernel brackets (K <= 16)
+    cudaEvent_t ck2[16] = {};  // FSR_CHUNK_TRACE: end of each chunk's work (main kernel + re-run)
     // host pipeline: the chunk whose output is still in this lane's pinned staging
     bool pending = false;
     int64_t pend_oa = 0, pend_ob = 0;
@@ -929,8 +930,15 @@ int ensure_lanes(fsr_engine *eng, Device &d) {
         if (!d.ck0[c]) {
             CUDA_TRY(eng, cudaEventCreate(&d.ck0[c]));
             CUDA_TRY(eng, cudaEventCreate(&d.ck1[c]));
+            CUDA_TRY(eng, cudaEventCreate(&d.ck2[c]));
         }
     return FSR_OK;
+}
+
+// FSR_CHUNK_TRACE: print each chunk's main-kernel bracket and end of work (stderr)
+static bool chunk_trace() {
+    static const bool t = std::getenv("FSR_CHUNK_TRACE") != nullptr;
+    return t;
 }
 
 // Chunk c of K over block rows [row0, row1)
@@ -960,15 +968,16 @@ int read_call_stats(fsr_engine *eng, Device &d, CallCtr &call, int64_t &reruns, 
     ms = 0.f;
     main_ms = 0.f;
     if (cudaEventElapsedTime(&ms, d.ev0, d.ev1) != cudaSuccess) ms = 0.f;
-    static const bool trace = std::getenv("FSR_CHUNK_TRACE") != nullptr;  // pipeline timeline (stderr)
+    const bool trace = chunk_trace();  // pipeline timeline (stderr)
     for (int c = 0; c < d.last_chunks; ++c) {  // the chunks' main-kernel brackets
         float t = 0.f;
         if (cudaEventElapsedTime(&t, d.ck0[c], d.ck1[c]) == cudaSuccess) main_ms += t;
         if (trace) {
-            float t0 = 0.f, t1 = 0.f;
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f;
             cudaEventElapsedTime(&t0, d.ev0, d.ck0[c]);
             cudaEventElapsedTime(&t1, d.ev0, d.ck1[c]);
-            fprintf(stderr, "chunk %2d: main kernel %7.3f .. %7.3f ms\n", c, t0, t1);
+            cudaEventElapsedTime(&t2, d.ev0, d.ck2[c]);
+            fprintf(stderr, "chunk %2d: main kernel %7.3f .. %7.3f ms, work done %7.3f ms\n", c, t0, t1, t2);
         }
     }
     if (trace) fprintf(stderr, "call: %.3f ms\n", ms);
@@ -1008,6 +1017,7 @@ int device_call(fsr_engine *eng, Device &d, const fsr_params *p, const IO *d_px,
                                r0, r1, nullptr, nullptr, ld.stream, d.chunk_ctrs.as<ChunkCtr>() + c,
                                call, d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
         if (rc) return rc;
+        if (chunk_trace()) CUDA_TRY(eng, cudaEventRecord(d.ck2[c], ld.stream));
         d.used_tma = ld.used_tma;
         d.served_fp64 = ld.served_fp64;
     }
@@ -1147,6 +1157,7 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
                                ld.stream, d.chunk_ctrs.as<ChunkCtr>() + c, call,
                                d.empty_list.as<int32_t>(), d.ck0[c], d.ck1[c]);
         if (rc) return rc;
+        if (chunk_trace()) CUDA_TRY(eng, cudaEventRecord(d.ck2[c], ld.stream));
         CUDA_TRY(eng, cudaMemcpyAsync(direct_out ? (void *)(out + oa * W) : ld.hout.p, ld.out.p,
                                       (size_t)rows_out * W * sizeof(IO), cudaMemcpyDeviceToHost,
                                       ld.stream));
@@ -1191,6 +1202,13 @@ int host_strip(fsr_engine *eng, Device &d, const fsr_params *p, const IO *px, co
 // (concurrently, one host thread per device).  Empty-support blocks get
 // `fill`, or (fill = NaN) the mean of the known samples of the caller's full
 // image (reconstruction.py:236-237; "no known samples" if there is none).
+// [a, a + an) and [b, b + bn) share a byte (the output must never alias an input:
+// chunks write rows that later chunks' halos still read)
+bool overlaps(const void *a, size_t an, const void *b, size_t bn) {
+    const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+    return an > 0 && bn > 0 && x < y + bn && y < x + an;
+}
+
 template <typename IO>
 int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const uint8_t *mask,
                      int64_t H, int64_t W, IO *out, int32_t *sel, int32_t *done,
@@ -1201,6 +1219,11 @@ int reconstruct_host(fsr_engine *eng, const fsr_params *p, const IO *px, const u
     if (rc) return rc;
     if (H < 1 || W < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
     if (!px || !mask || !out) return fail(eng, FSR_EINVAL, "null image buffer");
+    {
+        const size_t n = (size_t)H * (size_t)W;
+        if (overlaps(out, n * sizeof(IO), px, n * sizeof(IO)) || overlaps(out, n * sizeof(IO), mask, n))
+            return fail(eng, FSR_EINVAL, "output buffer overlaps an input buffer");
+    }
     const int B = p->block;
     const int64_t brows_all = (H + B - 1) / B, bcols = (W + B - 1) / B;
     if (rend < 0) rend = brows_all;
@@ -1279,6 +1302,15 @@ int reconstruct_device(fsr_engine *eng, const fsr_params *p, const IO *d_px, int
     if (rc) return rc;
     if (height < 1 || width < 1) return fail(eng, FSR_EINVAL, "image must have at least one pixel");
     if (!d_px || !d_mask || !d_out) return fail(eng, FSR_EINVAL, "null image buffer");
+    if (px_pitch < width || mask_pitch < width || out_pitch < width)
+        return fail(eng, FSR_EINVAL, "row pitch smaller than the width");
+    {
+        const size_t npx = (size_t)((height - 1) * px_pitch + width) * sizeof(IO);
+        const size_t nmk = (size_t)((height - 1) * mask_pitch + width);
+        const size_t nout = (size_t)((height - 1) * out_pitch + width) * sizeof(IO);
+        if (overlaps(d_out, nout, d_px, npx) || overlaps(d_out, nout, d_mask, nmk))
+            return fail(eng, FSR_EINVAL, "output buffer overlaps an input buffer");
+    }
     const int64_t brows = (height + p->block - 1) / p->block;
     if (row0 < 0 || row1 > brows || row0 > row1) return fail(eng, FSR_EINVAL, "block-row range out of bounds");
     Device &d = *eng->devs[0];
@@ -1429,6 +1461,7 @@ void fsr_engine_destroy(fsr_engine *eng) {
             if (d.ck0[c]) {
                 cudaEventDestroy(d.ck0[c]);
                 cudaEventDestroy(d.ck1[c]);
+                cudaEventDestroy(d.ck2[c]);
             }
         cudaEventDestroy(d.ev0);
         cudaEventDestroy(d.ev1);

@@ -362,6 +362,40 @@ def test_device_api_fill_and_no_samples():
         eng.last_stats()
 
 
+def test_output_aliasing_an_input_is_rejected():
+    """The output never aliases the input (fsr.h; the reference returns a fresh
+    copy, core.py:24): a chunked call writes rows that later chunks' halos still
+    read, so an overlapping output buffer is refused with FSR_EINVAL (host strip
+    call, and the device call with overlapping pitched ranges) instead of
+    returning a silently corrupted frame."""
+    torch = pytest.importorskip("torch")
+    from paper_2202_13926_b200 import _lib
+    H, W = 64, 80
+    img = oracle.synthetic_frame(H, W, 9)
+    sampled, mask = oracle.quarter_sample(img, 4)
+    sampled = np.ascontiguousarray(np.where(mask, sampled, 0.0))
+    mk = np.ascontiguousarray(mask.astype(np.uint8))
+    p = _lib.make_params(4, 6, 20, precision="fp64")
+    eng = _lib.Engine([0])
+    with pytest.raises(ValueError, match="overlaps an input"):
+        eng.reconstruct_rows(sampled, mk, p, 0, H // 4, sampled)
+    d_px = torch.tensor(sampled, device="cuda")
+    d_mk = torch.tensor(mk, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(ValueError, match="overlaps an input"):
+        eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                               d_px.data_ptr() + 8 * W * 8, W, p, stream, io="f64")
+    with pytest.raises(ValueError, match="pitch"):
+        eng.reconstruct_device(d_px.data_ptr(), W - 1, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                               d_px.data_ptr(), W, p, stream, io="f64")
+    # disjoint buffers still work, and equal the host call
+    d_out = torch.empty_like(d_px)
+    eng.reconstruct_device(d_px.data_ptr(), W, d_mk.data_ptr(), W, H, W, 0, H // 4,
+                           d_out.data_ptr(), W, p, stream, io="f64")
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy(), eng.reconstruct(sampled, mask, p))
+
+
 def test_frame_stream_matches_single_frames():
     """The pipelined frame stream (H2D / kernels / D2H on three streams,
     double-buffered) returns exactly the per-frame results."""
