@@ -14,9 +14,10 @@
 //     u -> -u mod 32:  H=0: {0..7, 16, 25..31},  H=1: {8..15, 17..24}, so the
 //     folded frequency prior needs 9 / 8 doubles and the conjugate split never
 //     crosses halves.  R[u][v] for the 16 rows: 64 registers.
-//   * one 16 KiB shared buffer per block: XOR-swizzled transpose tile during the
-//     2-D FFT, then W[u][v] row-major for the loop (rows read across lanes:
-//     conflict-free; the circular row shift costs two ALU ops per row).
+//   * one 24 KiB shared buffer per block: XOR-swizzled transpose tile during the
+//     2-D FFT, then W[u][v] row-major for the loop, rows 0..15 repeated as rows
+//     32..47 (rows read across lanes: conflict-free; the circular row shift is
+//     one base address per iteration plus compile-time row offsets).
 //   * FFT: each 32-point line is split radix-2 between the halves (16-point
 //     in-register FFT of the even / odd samples, exchanged through the tile).
 //   * per iteration: fused residual update + objective + running max over
@@ -36,6 +37,15 @@ namespace fsr {
 #ifndef FSR_P64_BRX
 #define FSR_P64_BRX 1
 #endif
+// W table rows per block: 48 = rows 0..31 plus copies of rows 0..15, so each
+// half's rows (one circular run of 15 or 17 rows, plus row 16 for H=0) are read
+// at compile-time offsets from one per-iteration base (no wrap); 32 = the
+// 16 KiB-aligned table with a masked row shift (two ALU ops per row)
+#ifndef FSR_P64_ROWS
+#define FSR_P64_ROWS 48
+#endif
+constexpr int kP64Rows = FSR_P64_ROWS;
+static_assert(kP64Rows == 32 || kP64Rows == 48, "FSR_P64_ROWS must be 32 or 48");
 
 template <typename IO>
 struct Pair64Args {
@@ -85,8 +95,8 @@ struct __align__(16) SelEntry {
 
 template <int BPC>
 struct Pair64Smem {
-    double2 buf[BPC][32 * 32];    // 16 KiB per block; the kernel aligns &buf to 16 KiB
-    double2 align_pad[1024];      // room for that alignment
+    double2 buf[BPC][kP64Rows * 32];  // FFT tile (rows 0..31), then the W table
+    double2 align_pad[kP64Rows == 32 ? 1024 : 1];  // 32 rows: room to align &buf to 16 KiB
     PairSlot slot[BPC][2][2];     // [block][parity][half]
     unsigned int red_hi[BPC][2][32];
     unsigned int red_lo[BPC][2][32];
@@ -201,14 +211,39 @@ __device__ __forceinline__ unsigned long long u64max(unsigned long long a, unsig
     return a > b ? a : b;
 }
 
+// Shared address of W[(u - pu) & 31][(v - pv) & 31] for slot i of half H.
+//   48 rows: P = address of row (S_H - pu) & 31 (S_0 = 25, S_1 = 8) plus the
+//            column, ycv = address of row (16 - pu) & 31 plus the column (H=0);
+//   32 rows: P = ((32 - pu) & 31) << 9, ycv = table | ((v - pv) & 31) << 4.
+template <int H>
+__device__ __forceinline__ uint32_t p64_waddr(int i, uint32_t P, uint32_t ycv) {
+    const int u = p64_row(H, i);
+    if (kP64Rows == 32) return ((P + ((uint32_t)u << 9)) & 0x3E00u) | ycv;
+    if (H == 0 && u == 16) return ycv;
+    const int k = H == 0 ? (u - 25) & 31 : u - 8;  // position in the half's circular run
+    return P + ((uint32_t)k << 9);
+}
+// The per-iteration (P, ycv) of p64_waddr for selection (pu, pv).
+template <int H>
+__device__ __forceinline__ void p64_wbase(uint32_t wb, int lane, int pu, int pv, uint32_t &P,
+                                          uint32_t &ycv) {
+    const uint32_t col = (uint32_t)((lane - pv) & 31) << 4;
+    if (kP64Rows == 32) {
+        P = (uint32_t)((32 - pu) & 31) << 9;
+        ycv = wb | col;
+    } else {
+        P = wb + ((uint32_t)(((H == 0 ? 25 : 8) - pu) & 31) << 9) + col;
+        ycv = wb + ((uint32_t)((16 - pu) & 31) << 9) + col;
+    }
+}
+
 // The residual update alone (replayed iterations): R -= gp W(. - pu, . - pv).
 template <int H>
 __device__ __forceinline__ void p64_update(cpx<double> (&R)[16], uint32_t P, uint32_t ycv, double gr,
                                            double gi) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        const int u = p64_row(H, i);
-        const uint32_t addr = ((P + ((uint32_t)u << 9)) & 0x3E00u) | ycv;
+        const uint32_t addr = p64_waddr<H>(i, P, ycv);
         double2 w;
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "r"(addr));
         double re = R[i].re, im = R[i].im;
@@ -234,8 +269,8 @@ __device__ __forceinline__ unsigned long long p64_pass(cpx<double> (&R)[16], con
         const int u = p64_row(H, i);
         double re = R[i].re, im = R[i].im;
         if (UPDATE) {
-            // W[(u - pu) & 31][(v - pv) & 31]: row shift wraps inside the 16 KiB window
-            const uint32_t addr = ((P + ((uint32_t)u << 9)) & 0x3E00u) | ycv;
+            // W[(u - pu) & 31][(v - pv) & 31]
+            const uint32_t addr = p64_waddr<H>(i, P, ycv);
             double2 w;
             asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "r"(addr));
             re = fma(-gr, w.x, re);
@@ -307,8 +342,8 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
                                          double2 *bufs, int pair) {
     const int lane = lane_id();
     const int bar_id = 1 + pair;
-    double2 *buf = bufs + pair * 1024;
-    const uint32_t wb = (uint32_t)__cvta_generic_to_shared(buf);  // 16 KiB aligned
+    double2 *buf = bufs + pair * (kP64Rows * 32);
+    const uint32_t wb = (uint32_t)__cvta_generic_to_shared(buf);  // 16 KiB aligned when kP64Rows == 32
     const uint32_t lrank = TREE ? bitrev5(lane) : (uint32_t)lane;
     double wfr[17];
 #pragma unroll
@@ -420,6 +455,10 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
             __syncwarp();
             buf[u * 32 + lane] = wp;
             if (nu != u) buf[nu * 32 + lane] = wn;
+            if (kP64Rows == 48) {  // rows 32..47 repeat rows 0..15 (outside the FFT tile)
+                if (u < 16) buf[(u + 32) * 32 + lane] = wp;
+                if (nu != u && nu < 16) buf[(nu + 32) * 32 + lane] = wn;
+            }
             __syncwarp();
         }
         bar_pair(bar_id);
@@ -473,8 +512,7 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
                 if (H == 0 && sel_b && lane == 0) sel_b[it] = wu * 32 + wv;
                 gr = c.x * ginv;
                 gi = c.y * ginv;
-                P = (uint32_t)((32 - wu) & 31) << 9;
-                ycv = wb | ((uint32_t)((lane - wv) & 31) << 4);
+                p64_wbase<H>(wb, lane, wu, wv, P, ycv);
                 if ((it & 1) == H && lane == 0) hist[(it >> 1) & 15] = SelEntry{gr, gi, wu, wv, {0, 0}};
                 if ((it & 31) == 31) {
                     __syncwarp();
@@ -543,8 +581,7 @@ __device__ __forceinline__ void p64_half(const Pair64Args<IO> &a, Pair64Smem<BPC
             if (thr > 0.0 && __longlong_as_double((long long)wkey) < thr) break;
             gr = c.x * ginv;
             gi = c.y * ginv;
-            P = (uint32_t)((32 - wu) & 31) << 9;
-            ycv = wb | ((uint32_t)((lane - wv) & 31) << 4);
+            p64_wbase<H>(wb, lane, wu, wv, P, ycv);
             // record every other selection per half; both halves flush together every 32
             if ((it & 1) == H && lane == 0) hist[(it >> 1) & 15] = SelEntry{gr, gi, wu, wv, {0, 0}};
             if ((it & 31) == 31) {
@@ -593,9 +630,10 @@ __global__ void __maxnreg__(FSR_P64_MAXREG) pair64_kernel(Pair64Args<IO> a) {
         sm.cs[threadIdx.x] = make_double2(c, s);
     }
     __syncthreads();
-    // align the block buffers to 16 KiB in the shared window (row shift by masking)
+    // 32-row tables: align the block buffers to 16 KiB in the shared window (row
+    // shift by masking); 48-row tables need no alignment
     const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(&sm.buf[0][0]);
-    const uint32_t pad = (0x4000u - (b0 & 0x3FFFu)) & 0x3FFFu;
+    const uint32_t pad = kP64Rows == 32 ? (0x4000u - (b0 & 0x3FFFu)) & 0x3FFFu : 0u;
     double2 *bufs = reinterpret_cast<double2 *>(reinterpret_cast<char *>(&sm.buf[0][0]) + pad);
     // warps p and p + BPC form block p's pair: same SMSP (warp % 4) when BPC % 4 == 0,
     // so the per-iteration pair barrier never waits on another scheduler's queue
