@@ -106,8 +106,8 @@ int fsr_unpin_host(void *p);
 /*
  * Whole-path call with HOST buffers (reconstruct_image).  px: H*W pixels on the
  * 0..255 scale, row-major; unknown pixels are ignored (the reference requires
- * them to be zero).  mask: H*W bytes, nonzero = known.  out: H*W, never
- * aliases px.  sel (nullable): [n_blocks, iterations] selected flat bins
+ * them to be zero).  mask: H*W bytes, nonzero = known.  out: H*W, must not
+ * overlap px or mask (FSR_EINVAL "output buffer overlaps an input buffer").  sel (nullable): [n_blocks, iterations] selected flat bins
  * (u*N+v) per block in partition order, -1 after an early stop; done
  * (nullable): [n_blocks] iterations run.  Synchronous.
  *
@@ -157,7 +157,9 @@ int fsr_reconstruct_rows_f64(fsr_engine *eng, const fsr_params *p, const double 
  * be valid.  With no known sample anywhere the call's fsr_last_stats returns
  * FSR_ENOSAMPLES ("no known samples").  Calls on one engine are serialised in
  * issue order even across different streams (each waits for the previous
- * call's end), because they share the engine's per-call scratch.
+ * call's end), because they share the engine's per-call scratch.  Pitches
+ * below the width and a d_out range overlapping d_px or d_mask are refused
+ * (FSR_EINVAL): later chunks still read rows that earlier chunks write.
  */
 int fsr_reconstruct_device_f32(fsr_engine *eng, const fsr_params *p, const float *d_px,
                                int64_t px_pitch, const uint8_t *d_mask, int64_t mask_pitch,
