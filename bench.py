@@ -94,6 +94,8 @@ def parse():
                     help="pixel type in and out: f64 is the reference's own (core.py:24)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--ref-seconds", type=float, default=None,
+                    help="reference arm: CPU seconds per step (default: the whole run ~150 s)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -271,7 +273,7 @@ def run_reference(args):
     sampled, mask, _ = make_frame(H, W, args.image)
     total = -(-H // B) * -(-W // B)
     threads = os.cpu_count() or 1
-    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_s = args.ref_seconds or max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     times = []
     for i in range(args.warmup + args.steps):
         t, nb, k, _ = cpu_port_sample(sampled, mask, B, N, I, args.reducer, per_step_s, threads)
