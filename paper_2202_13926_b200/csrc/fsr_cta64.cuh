@@ -502,7 +502,8 @@ __global__ void __launch_bounds__(C64_THREADS, 3)
 // double table (64 KiB) NEXT TO the FFT tile, so the split writes W while the
 // tile is still being read: W goes to a per-CTA global staging buffer (L2)
 // and is copied into the tile's space once the tile is consumed, so a CTA
-// needs 66.5 KiB of shared memory and two CTAs share an SM.
+// needs 81 KiB of shared memory (W with rows 0..14 repeated after row 63)
+// and two CTAs share an SM.
 // Keys: the fp64 objective wf * fma(re, re, im*im) with its 6 low mantissa bits
 // replaced by 63 - u (comparisons exact to 2^-46 relative, as pair64's 2^-47),
 // warp max by a redux on the high word (the low word only breaks exact ties
@@ -516,8 +517,13 @@ struct __align__(16) C64dSlot {
     int32_t pad[3];
 };
 
+// W rows in shared memory: 64 plus copies of rows 0..14, so a thread's run of
+// 16 rows (u - pu) & 63, u = 16h + i (+ 32), starts at one base row and never
+// wraps: compile-time row offsets instead of a masked shift per row
+constexpr int C64D_WROWS = 79;
+constexpr int C64D_TILE = 64 * C64_TS > C64D_WROWS * 64 ? 64 * C64_TS : C64D_WROWS * 64;
 struct C64dSmem {
-    double2 tile[64 * C64_TS];  // fp64 FFT tile (66 560 B), then W[u][v] (65 536 B)
+    double2 tile[C64D_TILE];  // fp64 FFT tile (66 560 B), then W[u][v] (79 rows, 80 896 B)
     double2 tw[64];             // e^{-2 pi i j / 64}
     double2 cs[64];             // (cos, sin)(2 pi j / 64)
     C64dSlot slot[2][4];
@@ -535,13 +541,15 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
                                                         double gr, double gi) {
     unsigned long long m = 0ull;
     const int col = (v - pv) & 63;
+    const double2 *wlo = Wt + ((16 * h - pu) & 63) * 64 + col;       // row (u - pu) & 63, i = 0
+    const double2 *whi = Wt + ((16 * h + 32 - pu) & 63) * 64 + col;  // row (u + 32 - pu) & 63
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const int u = 16 * h + i;
         double2 a = rl[i], b = rh[i];
         if (UPDATE) {
-            const double2 wa = Wt[((u - pu) & 63) * 64 + col];
-            const double2 wb = Wt[((u + 32 - pu) & 63) * 64 + col];
+            const double2 wa = wlo[i * 64];
+            const double2 wb = whi[i * 64];
             a.x = fma(-gr, wa.x, a.x);
             a.x = fma(gi, wa.y, a.x);
             a.y = fma(-gr, wa.y, a.y);
@@ -677,7 +685,7 @@ __global__ void __launch_bounds__(C64_THREADS, 2) cta64d_kernel(Pair64Args<IO> a
         __syncthreads();  // the tile is consumed: W moves into its space
         double2 *Wt = sm.tile;
 #pragma unroll 4
-        for (int e = tid; e < 4096; e += C64_THREADS) Wt[e] = gW[e];
+        for (int e = tid; e < C64D_WROWS * 64; e += C64_THREADS) Wt[e] = gW[e & 4095];
         __syncthreads();
         const double w00 = Wt[0].x;  // W[0][0] = sum of the weights
         int32_t *sel_b = a.sel ? a.sel + bid * (int64_t)max(a.iterations, 1) : nullptr;
