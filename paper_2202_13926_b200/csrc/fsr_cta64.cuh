@@ -539,7 +539,7 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
                                                         const double (&wl)[16], const double (&wh)[16],
                                                         const double2 *Wt, int h, int v, int pu, int pv,
                                                         double gr, double gi) {
-    unsigned long long m = 0ull;
+    unsigned long long mk[2] = {0ull, 0ull};
     const int col = (v - pv) & 63;
     const double2 *wlo = Wt + ((16 * h - pu) & 63) * 64 + col;       // row (u - pu) & 63, i = 0
     const double2 *whi = Wt + ((16 * h + 32 - pu) & 63) * 64 + col;  // row (u + 32 - pu) & 63
@@ -564,10 +564,10 @@ __device__ __forceinline__ unsigned long long c64d_pass(double2 (&rl)[16], doubl
         if (OBJ) {
             const unsigned long long ka = c64d_key(fma(a.x, a.x, a.y * a.y) * wl[i], u);
             const unsigned long long kb = c64d_key(fma(b.x, b.x, b.y * b.y) * wh[i], u + 32);
-            m = max(m, max(ka, kb));
+            mk[i & 1] = max(mk[i & 1], max(ka, kb));  // two independent max chains
         }
     }
-    return m;
+    return max(mk[0], mk[1]);
 }
 
 // Row pair i = u mod 16 of this thread in fp64, (rl[i], rh[i]), by one indirect branch
